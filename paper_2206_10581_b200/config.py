@@ -1,0 +1,243 @@
+"""TTConfig: the factorisation plan, mirroring ttgnn/tt_config.hpp.
+
+Same fields, invariants and error behaviour as the reference
+(`TTConfig` tt_config.hpp:33-52, `validate` tt_config.cpp:92-113,
+`plan_factorization` :144-174, `balanced_factors` :115-142,
+`index_to_coordinate` :176-189, `count_params` :204-208).  Errors are raised
+as ValueError (std::invalid_argument) and IndexError (std::out_of_range).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Sequence
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class OutOfRange(IndexError):
+    """std::out_of_range in the reference."""
+
+
+@dataclass
+class TTConfig:
+    num_nodes: int = 0
+    emb_dim: int = 0
+    row_factors: List[int] = field(default_factory=list)
+    col_factors: List[int] = field(default_factory=list)
+    ranks: List[int] = field(default_factory=list)
+
+    # short aliases used throughout the engine and tests
+    @property
+    def d(self) -> int:
+        return len(self.row_factors)
+
+    @property
+    def m(self) -> List[int]:
+        return self.row_factors
+
+    @property
+    def n(self) -> List[int]:
+        return self.col_factors
+
+    @property
+    def R(self) -> List[int]:
+        return self.ranks
+
+    def num_cores(self) -> int:
+        return len(self.row_factors)
+
+    def padded_rows(self) -> int:
+        return math.prod(self.row_factors)
+
+    def padded_cols(self) -> int:
+        return math.prod(self.col_factors)
+
+    def core_shape(self, k: int):
+        return (self.ranks[k], self.row_factors[k], self.col_factors[k], self.ranks[k + 1])
+
+    def core_size(self, k: int) -> int:
+        return math.prod(self.core_shape(k))
+
+    def validate(self) -> None:
+        """TTConfig::validate (tt_config.cpp:92-113), same messages."""
+        if self.num_nodes <= 0:
+            raise InvalidArgument("TTConfig: num_nodes must be positive")
+        if self.emb_dim <= 0:
+            raise InvalidArgument("TTConfig: emb_dim must be positive")
+        d = self.num_cores()
+        if d < 2:
+            raise InvalidArgument("TTConfig: need at least 2 cores")
+        if len(self.col_factors) != d:
+            raise InvalidArgument("TTConfig: row/col factor lists differ in length")
+        if len(self.ranks) != d + 1:
+            raise InvalidArgument("TTConfig: rank list must have d+1 entries")
+        if self.ranks[0] != 1 or self.ranks[-1] != 1:
+            raise InvalidArgument("TTConfig: boundary ranks R_0 and R_d must be 1")
+        if any(r <= 0 for r in self.ranks):
+            raise InvalidArgument("TTConfig: ranks must be positive")
+        if any(x <= 0 for x in self.row_factors) or any(x <= 0 for x in self.col_factors):
+            raise InvalidArgument("TTConfig: factors must be positive")
+        if self.padded_rows() < self.num_nodes:
+            raise InvalidArgument("TTConfig: prod(row_factors) < num_nodes")
+        if self.padded_cols() < self.emb_dim:
+            raise InvalidArgument("TTConfig: prod(col_factors) < emb_dim")
+
+
+def _best_factorization(value: int, d: int, lo_f: int, hi_f: int) -> List[int]:
+    """tt_config.cpp:37-76 (smallest spread, ties lexicographically smallest)."""
+    if d == 1:
+        return [value] if lo_f <= value <= hi_f else []
+    best: List[int] = []
+    best_spread = None
+    cur: List[int] = []
+
+    def rec(rem: int, parts: int, lo: int) -> None:
+        nonlocal best, best_spread
+        if parts == 1:
+            if rem < lo or rem > hi_f:
+                return
+            cand = cur + [rem]
+            spread = cand[-1] - cand[0]
+            if best_spread is None or spread < best_spread or (spread == best_spread and cand < best):
+                best, best_spread = cand, spread
+            return
+        cap = min(hi_f, int(math.floor(float(rem) ** (1.0 / parts))) + 1)
+        for f in range(lo, cap + 1):
+            if rem % f:
+                continue
+            cur.append(f)
+            rec(rem // f, parts - 1, f)
+            cur.pop()
+
+    rec(value, d, lo_f)
+    return best
+
+
+def balanced_factors(value: int, d: int) -> List[int]:
+    """tt_config.cpp:115-142."""
+    if value <= 0:
+        raise InvalidArgument("balanced_factors: value must be positive")
+    if d <= 0:
+        raise InvalidArgument("balanced_factors: d must be positive")
+    if value == 1:
+        return [1] * d
+    root = int(math.ceil(float(value) ** (1.0 / d)))
+    min_f = max(1, (2 * root) // 3)
+    max_f = max(2, (3 * root + 1) // 2)
+    window = max(8, value // 1000)
+    while True:
+        best: List[int] = []
+        best_spread = None
+        for padded in range(value, value + window + 1):
+            f = _best_factorization(padded, d, min_f, max_f)
+            if not f:
+                continue
+            spread = f[-1] - f[0]
+            if best_spread is None or spread < best_spread:
+                best, best_spread = f, spread
+                if spread == 0:
+                    break
+        if best:
+            return best
+        window *= 2
+
+
+def plan_factorization(num_nodes: int, emb_dim: int, d_or_row_factors, *args,
+                       ortho_friendly: bool = True) -> TTConfig:
+    """Both reference overloads (tt_config.hpp:69-78):
+
+    plan_factorization(M, N, d, ranks, ortho_friendly=True)      -- auto
+    plan_factorization(M, N, row_factors, col_factors, ranks)    -- explicit
+    """
+    if isinstance(d_or_row_factors, int):
+        d = d_or_row_factors
+        (ranks,) = args
+        if num_nodes <= 0 or emb_dim <= 0:
+            raise InvalidArgument("plan_factorization: dimensions must be positive")
+        if d < 2:
+            raise InvalidArgument("plan_factorization: d must be >= 2")
+        if len(ranks) != d + 1:
+            raise InvalidArgument("plan_factorization: rank list must have d+1 entries")
+        m = balanced_factors(num_nodes, d)
+        n = balanced_factors(emb_dim, d)
+        if ortho_friendly:
+            m = sorted(m)
+            n = sorted(n, reverse=True)
+        return plan_factorization(num_nodes, emb_dim, m, n, ranks)
+    col_factors, ranks = args
+    cfg = TTConfig(int(num_nodes), int(emb_dim), [int(x) for x in d_or_row_factors],
+                   [int(x) for x in col_factors], [int(x) for x in ranks])
+    cfg.validate()
+    return cfg
+
+
+def index_to_coordinate(cfg: TTConfig, row: int) -> List[int]:
+    """tt_config.cpp:176-189 (i_1 most significant)."""
+    if row < 0 or row >= cfg.padded_rows():
+        raise OutOfRange(f"index_to_coordinate: row index {row} out of [0, {cfg.padded_rows()})")
+    parts = [0] * cfg.d
+    rem = row
+    for k in range(cfg.d - 1, -1, -1):
+        parts[k] = rem % cfg.m[k]
+        rem //= cfg.m[k]
+    return parts
+
+
+def coordinate_to_index(cfg: TTConfig, parts: Sequence[int]) -> int:
+    """tt_config.cpp:191-202."""
+    if len(parts) != cfg.d:
+        raise InvalidArgument("coordinate_to_index: wrong coordinate length")
+    row = 0
+    for k in range(cfg.d):
+        if parts[k] < 0 or parts[k] >= cfg.m[k]:
+            raise OutOfRange("coordinate_to_index: digit out of range")
+        row = row * cfg.m[k] + parts[k]
+    return row
+
+
+def count_params(cfg: TTConfig) -> int:
+    return sum(cfg.core_size(k) for k in range(cfg.d))
+
+
+def compression_ratio(cfg: TTConfig) -> float:
+    return float(cfg.num_nodes) * float(cfg.emb_dim) / float(count_params(cfg))
+
+
+# ---- BASELINE.json workloads ------------------------------------------------
+# num_nodes is the ID-range bound; factors are explicit (SURVEY 8a row a1:
+# the auto planner orders n descending and cannot produce (4,4,8)/(4,8,4)).
+WORKLOADS = {
+    "small": dict(cfg=lambda: plan_factorization(169_343, 128, [56, 56, 56], [8, 4, 4], [1, 16, 16, 1]),
+                  batch=4096, dist="uniform", opt="sgd"),
+    "products": dict(cfg=lambda: plan_factorization(2_449_029, 128, [126, 140, 140], [4, 4, 8], [1, 32, 32, 1]),
+                     batch=65_536, dist="zipf", alpha=1.1, opt="adagrad"),
+    "papers": dict(cfg=lambda: plan_factorization(111_059_956, 128, [480, 481, 482], [4, 8, 4], [1, 64, 64, 1]),
+                   batch=262_144, dist="zipf", alpha=1.05, opt="adagrad"),
+    "billion": dict(cfg=lambda: plan_factorization(1_003_875_856, 256, [178] * 4, [4] * 4, [1, 32, 32, 32, 1]),
+                    batch=1_048_576, dist="zipf", alpha=1.1, opt="sgd"),
+}
+for _r in (8, 16, 32, 64, 128):
+    WORKLOADS[f"sweep{_r}"] = dict(
+        cfg=(lambda r=_r: plan_factorization(2_449_029, 128, [126, 140, 140], [4, 4, 8], [1, r, r, 1])),
+        batch=131_072, dist="locality", block=140 * 140, opt="adagrad")
+
+
+def workload_inputs(name: str, seed: int = 2026, batch: int | None = None):
+    """(cfg, indices int64[B], upstream f32[B, emb_dim], cores f32 list) for a
+    BASELINE workload, from the portable generator in synth.py."""
+    from . import synth
+    w = WORKLOADS[name]
+    cfg = w["cfg"]()
+    B = w["batch"] if batch is None else batch
+    if w["dist"] == "uniform":
+        idx = synth.uniform_ids(seed, B, cfg.num_nodes)
+    elif w["dist"] == "zipf":
+        idx = synth.zipf_ids(seed, B, w["alpha"], cfg.num_nodes)
+    else:
+        idx = synth.locality_ids(seed, B, cfg.num_nodes, w["block"])
+    up = synth.normal(seed, 7, B * cfg.emb_dim).reshape(B, cfg.emb_dim)
+    cores = synth.gaussian_cores(cfg, seed, 0.1)
+    return cfg, idx, up, cores
