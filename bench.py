@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""TT-embedding training-step benchmark (BASELINE.json metric).
+
+One step = forward (lookup of the batch) + backward (core gradients) +
+optimizer update of the cores, on the workload BASELINE.json names
+(default: the papers100M-shaped config the north star's roofline target is
+quoted on; --config selects another).  Inputs are seeded synthetic data of the
+configs' shapes and distributions (paper_2206_10581_b200.synth).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config papers]
+  python bench.py --impl reference ...   # the reference algorithm on host CPUs
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL): the global batch is
+sharded by position, core gradients are all-reduced every step, and the
+device time is the max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT-emb rows/sec fwd+bwd+update at 1/2/4/8 B200; % of FP32 peak; vs host-CPU ref"
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x20: "sync_boost", 0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+           0x100: "hw_power_brake_slowdown", 0x200: "display_clock_setting"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="papers")
+    p.add_argument("--seed", type=int, default=2026)
+    p.add_argument("--path", default="auto", choices=["auto", "generic"])
+    p.add_argument("--cpu-sample", type=int, default=0, help="rows per CPU-baseline step (0 = auto)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons, sampled during the timed region."""
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id, self.rows, self.proc = gpu_id, [], None
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            parts = [x.strip() for x in r.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[3], 16) if parts[3].startswith("0x") else int(parts[3])
+            except ValueError:
+                continue
+            if bits & 0x1:  # idle sample, not under load
+                continue
+            sm.append(s)
+            mx = m
+            for b, name in REASONS.items():
+                if bits & b:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def level_costs(cfg):
+    """c_l = N_{l-1} R_{l-1} n_l R_l MACs for levels l = 2..d (0-based k = 1..d-1)."""
+    out, N = [], cfg.n[0]
+    for k in range(1, cfg.d):
+        out.append(N * cfg.R[k] * cfg.n[k] * cfg.R[k + 1])
+        N *= cfg.n[k]
+    return out
+
+
+def algorithmic_flops(cfg, U):
+    """Reuse-aware F = 6 sum_l U_l c_l (fwd 1 part, bwd 2 parts)."""
+    return 6.0 * sum(u * c for u, c in zip(U[1:], level_costs(cfg)))
+
+
+def cpu_baseline(cfg, name, idx, up, cores, sample, steps=1):
+    """The oracle (C restatement of the reference, fp64) on the host cores:
+    fwd + bwd on `sample` rows scaled to the full batch, plus the reference's
+    dense update over all parameters (autodiff.cpp:147-173)."""
+    import oracle
+    from paper_2206_10581_b200.config import WORKLOADS
+    B = len(idx)
+    S = min(sample, B)
+    nt = oracle.num_threads()
+    c64 = [c.astype(np.float64) for c in cores]
+    kind = {"sgd": oracle.SGD, "adagrad": oracle.ADAGRAD, "adam": oracle.ADAM}[WORKLOADS[name]["opt"]]
+    opt = oracle.OptState(cfg, kind, 0.01)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.lookup_batch(cfg, c64, idx[:S], nt)
+        t1 = time.perf_counter()
+        g, _ = oracle.backward_lookup(cfg, c64, idx[:S], up[:S], nt)
+        t2 = time.perf_counter()
+        oracle.apply_update(cfg, c64, g, opt)
+        t3 = time.perf_counter()
+        times.append((t1 - t0, t2 - t1, t3 - t2))
+    tf, tb, tu = np.median(np.array(times), axis=0)
+    step_s = (tf + tb) * B / S + tu
+    return {"value": B / step_s, "unit": "rows/s", "cores": nt, "kind": "port",
+            "sample": f"fwd+bwd on the first {S} of {B} batch rows (fp64, {nt} threads) scaled x{B / S:.1f}, "
+                      f"plus the dense {WORKLOADS[name]['opt']} update of all {sum(c.size for c in cores)} params; "
+                      f"median of {steps}",
+            "ms": {"fwd": tf * 1e3, "bwd": tb * 1e3, "upd": tu * 1e3}}
+
+
+def run_reference(a, rank):
+    """--impl reference: the reference algorithm (oracle port; the reference's
+    tt_embedding.cpp/autodiff.cpp need Eigen, absent here) on host cores."""
+    if rank != 0:
+        return
+    from paper_2206_10581_b200.config import workload_inputs, WORKLOADS
+    name = a.config
+    cfg, idx, up, cores = workload_inputs(name, a.seed)
+    sample = a.cpu_sample or (1024 if cfg.d >= 3 and max(cfg.R) >= 64 else 4096)
+    cb = cpu_baseline(cfg, name, idx, up, cores, sample, steps=max(1, a.warmup + a.steps) if a.steps <= 3 else 3)
+    v = cb["value"]
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "rows/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": len(idx) / v * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "batch": len(idx), "num_nodes": cfg.num_nodes,
+                       "row_factors": cfg.m, "col_factors": cfg.n, "ranks": cfg.R,
+                       "optimizer": WORKLOADS[name]["opt"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2206_10581_b200 import engine as E
+    from paper_2206_10581_b200.config import WORKLOADS, workload_inputs
+    from paper_2206_10581_b200.dist import DataParallelTT, shard_bounds
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = a.config
+    cfg, idx_all, up_all, cores = workload_inputs(name, a.seed)
+    Bg = len(idx_all)
+    lo, hi = shard_bounds(Bg, rank, world)
+    B = hi - lo
+    dev = torch.device("cuda", local)
+    idx = torch.tensor(idx_all[lo:hi], device=dev)
+    up = torch.tensor(up_all[lo:hi], device=dev)
+    emb = E.TTEmbedding(cfg, local)
+    emb.set_cores(cores)
+    emb.set_path(a.path)
+    opt = E.OptimizerState.make(cfg, getattr(E.OptKind, WORKLOADS[name]["opt"]), 0.01)
+    emb.configure_optimizer(opt)
+    dp = DataParallelTT(emb) if world > 1 else None
+    out = torch.empty((B, cfg.emb_dim), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def step():
+        emb.forward(idx, out)
+        emb.backward(up)
+        if dp:
+            dp.allreduce()
+        emb.step()
+
+    for _ in range(max(a.warmup, 3 if a.warmup >= 3 else a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    emb.sync()
+    U = emb.plan_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    props = torch.cuda.get_device_properties(local)
+    uuid = getattr(props, "uuid", None)
+    sampler = ClockSampler(f"GPU-{uuid}" if uuid else str(local))
+    sampler.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    l0 = emb.launch_count()
+    for i in range(a.steps):
+        flush.zero_()
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    launches = emb.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    emb.sync()
+    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    per_step = [s.elapsed_time(e) for s, e in ev]
+    tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+    value = Bg * a.steps / (t_max / 1e3)
+    ms_per_step = t_max / a.steps
+
+    # roofline: algorithmic FLOPs of this rank's step over the device time
+    flops = algorithmic_flops(cfg, U)
+    peak = E.ffma_peak_tflops(local, 8192)
+    achieved = flops / (ms_per_step * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(name)
+        except (OSError, ValueError):
+            traffic = None
+
+    # e2e through the C-ABI with pinned host buffers (H2D inputs, D2H output rows)
+    e2e = None
+    if not a.no_e2e:
+        h_idx = torch.tensor(idx_all[lo:hi]).pin_memory()
+        h_up = torch.tensor(up_all[lo:hi]).pin_memory()
+        h_out = torch.empty((B, cfg.emb_dim), dtype=torch.float32).pin_memory()
+        lib = E.load_library()
+
+        def e2e_step():
+            if dp is None:
+                E._raise(lib.tt_train_step_host(emb._h, h_idx.data_ptr(), B, h_up.data_ptr(), h_out.data_ptr()),
+                         "tt_train_step_host")
+            else:
+                d_idx = h_idx.to(dev, non_blocking=True)
+                d_up = h_up.to(dev, non_blocking=True)
+                emb.forward(d_idx, out)
+                h_out.copy_(out, non_blocking=True)
+                emb.backward(d_up)
+                dp.allreduce()
+                emb.step()
+                torch.cuda.synchronize()
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": Bg * a.steps / float(te.item()), "unit": "rows/s",
+               "h2d_bytes_per_step": int(h_idx.numel() * 8 + h_up.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 4),
+               "api": "tt_train_step_host (C-ABI)" if dp is None else "TTEmbedding + DataParallelTT (Python API)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        sample = a.cpu_sample or (1024 if max(cfg.R) >= 64 else 4096)
+        cpu = cpu_baseline(cfg, name, idx_all, up_all, cores, sample, steps=1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": name, "global_batch": Bg, "num_nodes": cfg.num_nodes, "row_factors": cfg.m,
+                       "col_factors": cfg.n, "ranks": cfg.R, "optimizer": WORKLOADS[name]["opt"],
+                       "parallelism": f"dp{world}", "path": emb.last_path(),
+                       "l2": "256 MB buffer written between timed steps (outside the events)",
+                       "unique_per_level_rank0": U},
+            "roofline": {"bound": "fp32", "kernel": "whole step", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
+                         "flops_per_step": flops,
+                         "peak_source": "FFMA microbenchmark (tt_ffma_peak_tflops) on this GPU, this run"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "ms_per_step_each": per_step,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * tt_engine.h -- C-ABI of the B200-native tensor-train embedding engine.
+ *
+ * This is the drop-in boundary for the reference's lookup/training hot path
+ * (namespace ttgnn, /root/reference/proj/core).  The reference has no FFI
+ * layer; its "operator API" is free functions over value types.  Each entry
+ * point below names the reference interface it replaces.  Plain pointers and
+ * sizes only; no torch or CUDA types appear in the signatures (streams are
+ * passed as `void*` holding a cudaStream_t, NULL = legacy default stream).
+ *
+ * Errors: every call returns a tt_status.  The reference throws
+ * std::invalid_argument (TT_ERR_ARG) and std::out_of_range (TT_ERR_INDEX) and
+ * rejects non-finite gradients before mutating anything (TT_ERR_NONFINITE).
+ * Device-side errors of the asynchronous calls are deferred: the batch is
+ * failed as a whole (no output row and no gradient is written) and the error
+ * is returned by tt_sync() / the next synchronous call.  tt_last_error()
+ * returns a thread-local message in the reference's wording.
+ *
+ * Threading: one handle per GPU; calls on a handle are serialised by the
+ * caller (SPEC.md:100,222 -- readers concurrent, updates exclusive).
+ */
+#ifndef TT_ENGINE_H
+#define TT_ENGINE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_MAX_CORES 8
+
+typedef enum {
+  TT_OK = 0,
+  TT_ERR_ARG = 1,       /* std::invalid_argument: config / shape / misuse     */
+  TT_ERR_INDEX = 2,     /* std::out_of_range: index outside [0, num_nodes)     */
+  TT_ERR_NONFINITE = 3, /* apply_update: non-finite gradient, update rejected  */
+  TT_ERR_CUDA = 4,      /* CUDA runtime failure                                */
+  TT_ERR_STATE = 5,     /* saved-plan backward without a matching forward      */
+  TT_ERR_NOMEM = 6
+} tt_status;
+
+typedef enum { TT_OPT_SGD = 0, TT_OPT_ADAM = 1, TT_OPT_ADAGRAD = 2 } tt_opt_kind;
+
+/* TTConfig (tt_config.hpp:33-52): d cores, core k of shape
+ * (ranks[k], row_factors[k], col_factors[k], ranks[k+1]). */
+typedef struct {
+  int64_t num_nodes;
+  int64_t emb_dim;
+  int32_t d;
+  int32_t reserved_;
+  int64_t row_factors[TT_MAX_CORES];
+  int64_t col_factors[TT_MAX_CORES];
+  int64_t ranks[TT_MAX_CORES + 1];
+} tt_config_c;
+
+typedef struct tt_engine tt_engine;
+
+/* ---- configuration (tt_config.cpp) --------------------------------------- */
+/* TTConfig::validate (tt_config.cpp:92-113). */
+int tt_config_validate(const tt_config_c* cfg);
+/* count_params (tt_config.cpp:204-208); -1 on an invalid config. */
+int64_t tt_count_params(const tt_config_c* cfg);
+
+/* ---- lifetime ------------------------------------------------------------- */
+/* TTEmbedding::zeros (tt_embedding.cpp:73-81): cores live on `device`,
+ * zero-filled; optimizer defaults to SGD lr=1e-3 until tt_opt_init. */
+int tt_engine_create(const tt_config_c* cfg, int device, tt_engine** out);
+void tt_engine_destroy(tt_engine* h);
+
+/* ---- cores: host buffers in the reference layout (R_{k-1}, m_k, n_k, R_k),
+ * row-major, one pointer per core (TTEmbedding::cores, tt_embedding.hpp:30-32).
+ * The device layout is private. */
+int tt_set_cores_f64(tt_engine* h, const double* const* cores);
+int tt_set_cores_f32(tt_engine* h, const float* const* cores);
+int tt_get_cores_f64(tt_engine* h, double* const* cores);
+int tt_get_cores_f32(tt_engine* h, float* const* cores);
+
+/* ---- optimizer: OptimizerState::make (autodiff.cpp:120-133) + Adagrad ------
+ * SGD: G -= lr g; Adam: bias-corrected (autodiff.cpp:135-145);
+ * Adagrad: h += g^2, G -= lr g / (sqrt(h) + eps), h0 = 0.  Resets state and
+ * the step counter.  Non-positive beta/eps arguments select the defaults
+ * (0.9, 0.999, 1e-8; Adagrad eps 1e-10). */
+int tt_opt_init(tt_engine* h, int kind, double lr, double beta1, double beta2, double eps);
+int tt_opt_get_step(tt_engine* h, int64_t* step); /* synchronises */
+
+/* ---- hot path: device buffers, stream-ordered, asynchronous ---------------
+ * tt_forward  ~ lookup_batch (tt_embedding.cpp:110-125): d_out is
+ *   batch x emb_dim row-major fp32; row b = embedding of d_indices[b].
+ * tt_backward ~ backward_lookup (autodiff.cpp:48-118): gradients (a sum over
+ *   rows, no 1/B) stay in the handle.  d_indices == NULL reuses the plan and
+ *   saved activations of the last tt_forward (the autograd pattern); the cores
+ *   must not have changed since (else TT_ERR_STATE).
+ * tt_step     ~ apply_update (autodiff.cpp:147-173): all-or-nothing; a
+ *   non-finite gradient leaves cores, optimizer state and step untouched. */
+int tt_forward(tt_engine* h, const int64_t* d_indices, int64_t batch, float* d_out, void* stream);
+int tt_backward(tt_engine* h, const int64_t* d_indices, int64_t batch, const float* d_grad_out,
+                void* stream);
+int tt_step(tt_engine* h, void* stream);
+/* Waits for `stream`, returns (and clears) the first deferred error. */
+int tt_sync(tt_engine* h, void* stream);
+
+/* ---- host-buffer entry points (synchronous; the reference call shapes) ---- */
+int tt_lookup_batch(tt_engine* h, const int64_t* h_indices, int64_t batch, float* h_out);
+int tt_backward_lookup(tt_engine* h, const int64_t* h_indices, int64_t batch,
+                       const float* h_upstream);
+int tt_apply_update(tt_engine* h);
+/* One training step through host memory: upload indices and upstream,
+ * forward (result copied to h_out, may be NULL), backward on the saved plan,
+ * update.  Returns after the step has completed. */
+int tt_train_step_host(tt_engine* h, const int64_t* h_indices, int64_t batch,
+                       const float* h_upstream, float* h_out);
+
+/* Dense gradients in the reference layout (CoreGradients, autodiff.hpp:29-34);
+ * untouched slices read as exactly 0.  batch_count may be NULL. */
+int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_count);
+
+/* Uploads caller-built gradients (reference layout, e.g. a CoreGradients a
+ * test constructed); every slice counts as touched by the next update. */
+int tt_set_core_grads_f64(tt_engine* h, const double* const* grads, int64_t batch_count);
+
+/* ---- data-parallel plumbing ------------------------------------------------
+ * The gradient buffer is one contiguous fp32 array: every core's gradient
+ * (device layout) followed by one touch counter per core slice.  With
+ * dense mode on, tt_backward zero-fills it first so that a sum all-reduce
+ * (NCCL over NVLink, issued by the caller on the same stream) yields the
+ * global gradient and the union of touched slices. */
+int tt_grad_buffer(tt_engine* h, float** d_ptr, int64_t* count);
+int tt_set_dense_grads(tt_engine* h, int on);
+/* Makes the engine use caller-owned device memory (>= the count that
+ * tt_grad_buffer reports, same device) as its gradient buffer, e.g. a tensor
+ * a torch.distributed NCCL all-reduce operates on.  NULL restores the
+ * engine's own buffer. */
+int tt_bind_grad_buffer(tt_engine* h, float* d_ptr, int64_t count);
+
+/* ---- introspection -------------------------------------------------------- */
+/* Distinct prefixes (i_1..i_l), l = 1..d, of the last planned batch
+ * (unique_per_level[d-1] = distinct IDs).  Synchronises. */
+int tt_plan_stats(tt_engine* h, int64_t* unique_per_level);
+/* Per-level digits of the last planned batch's distinct IDs, sorted
+ * ascending (digits[u*d + k] = i_{k+1}); returns U.  Synchronises. */
+int64_t tt_plan_digits(tt_engine* h, int64_t* ids_out, int32_t* digits_out, int64_t cap);
+/* The last planned batch's stable sort: keys (IDs) ascending and their batch
+ * positions (ties in position order); returns B.  Synchronises. */
+int64_t tt_plan_sorted(tt_engine* h, int64_t* keys_out, int32_t* pos_out, int64_t cap);
+/* Kernel launches issued by this handle since creation. */
+int64_t tt_launch_count(tt_engine* h);
+/* Selects the kernel family: 0 = auto (fused fast path where the shapes
+ * allow), 1 = generic path only. */
+int tt_set_path(tt_engine* h, int path);
+/* Which path the last forward used (0 generic, 1 fused). */
+int tt_last_path(tt_engine* h);
+/* Batch position (TT_ERR_INDEX) or core (TT_ERR_NONFINITE) of the last error. */
+int64_t tt_last_error_position(void);
+/* Offending index value of the last TT_ERR_INDEX. */
+int64_t tt_last_error_value(void);
+const char* tt_last_error(void);
+
+/* FP32 FFMA throughput microbenchmark (the roofline denominator): runs
+ * `iters` dependent-chain FFMA loops on every SM and returns TFLOP/s. */
+double tt_ffma_peak_tflops(int device, int iters);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TT_ENGINE_H */

@@ -1,0 +1,862 @@
+// engine.cu -- host side of the B200 TT-embedding engine and its C-ABI
+// (include/tt_engine.h).  One handle per GPU owns the device cores,
+// gradients, optimizer state and the per-batch plan; every hot-path call is
+// stream-ordered and host-sync free (counts that depend on the batch stay on
+// the device), so a whole training step can be captured in a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tt_engine.h"
+#include "common.cuh"
+#include "kernels_fused.cuh"
+#include "kernels_generic.cuh"
+#include "kernels_plan.cuh"
+#include "kernels_update.cuh"
+
+using namespace tt;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_err_pos = -1;
+thread_local int64_t g_err_val = 0;
+
+int fail(int code, const std::string& msg, int64_t pos = -1, int64_t val = 0) {
+  g_err = msg;
+  g_err_pos = pos;
+  g_err_val = val;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? TT_ERR_NOMEM : TT_ERR_CUDA,           \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+int64_t bitlen(uint64_t v) {
+  int64_t b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+int grid_for(int64_t total, int threads = 256, int64_t cap = 148 * 32) {
+  int64_t g = (total + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return (int)std::min<int64_t>(g, cap);
+}
+
+}  // namespace
+
+struct tt_engine {
+  tt_config_c cfg{};
+  DevCfg dc{};
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t own = nullptr;
+
+  // parameters / gradients / optimizer state (device layout)
+  float* params = nullptr;
+  float* grads = nullptr;  // nparams values + touch counters (own or bound)
+  float* own_grads = nullptr;
+  int64_t ntc = 0;         // number of touch counters (sum of m_k)
+  float* s1 = nullptr;
+  float* s2 = nullptr;
+  long long* d_step = nullptr;
+  DevStatus* st = nullptr;
+  int opt_kind = TT_OPT_SGD;
+  double lr = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  bool dense = false;
+
+  // plan (capacity grows, never shrinks)
+  int64_t cap = 0;
+  int64_t B = 0;
+  const int64_t* last_idx = nullptr;
+  unsigned long long *keys_a = nullptr, *keys_b = nullptr, *skeys = nullptr, *uniq = nullptr;
+  int *pos_a = nullptr, *pos_b = nullptr, *spos = nullptr;
+  int* hist = nullptr;
+  int* flag = nullptr;
+  int* seg = nullptr;
+  int* counts = nullptr;
+  int* d_B = nullptr;
+  int* lflags = nullptr;
+  int *digit = nullptr, *parent = nullptr, *first = nullptr, *cstart = nullptr;
+  unsigned* gk[TT_MAXD][2] = {};
+  int* gv[TT_MAXD][2] = {};
+  int* order[TT_MAXD] = {};
+  unsigned* sdig[TT_MAXD] = {};
+  int* goff[TT_MAXD] = {};
+  int* partial = nullptr;
+  int64_t partial_len = 0;
+  LevelBufs L{};
+  int64_t capk[TT_MAXD] = {};
+  FusedBufs F{};
+
+  // host-entry staging
+  int64_t stage_cap = 0;
+  int64_t* st_idx = nullptr;
+  float* st_out = nullptr;
+  float* st_up = nullptr;
+
+  // bookkeeping
+  bool plan_valid = false;
+  int64_t cores_version = 0, plan_version = -1;
+  int64_t batch_count = 0;
+  int64_t launches = 0;
+  int path_pref = 0;   // 0 auto, 1 generic
+  int last_path = 0;
+  bool fused_ok = false;
+  FusedShape fs{};
+};
+
+namespace {
+
+void free_plan(tt_engine* h) {
+  void* ptrs[] = {h->keys_a, h->keys_b, h->uniq, h->pos_a, h->pos_b, h->hist, h->flag, h->seg,
+                  h->lflags, h->digit, h->parent, h->first, h->cstart, h->partial};
+  for (void* p : ptrs) cudaFree(p);
+  for (int k = 0; k < TT_MAXD; ++k) {
+    for (int j = 0; j < 2; ++j) { cudaFree(h->gk[k][j]); cudaFree(h->gv[k][j]); h->gk[k][j] = nullptr; h->gv[k][j] = nullptr; }
+    cudaFree(h->goff[k]); h->goff[k] = nullptr;
+    h->sdig[k] = nullptr; h->order[k] = nullptr;
+    cudaFree(h->L.P[k]); cudaFree(h->L.dP[k]); cudaFree(h->L.dPc[k]);
+    h->L.P[k] = h->L.dP[k] = h->L.dPc[k] = nullptr;
+  }
+  free_fused(h->F);
+  h->keys_a = h->keys_b = h->uniq = nullptr;
+  h->pos_a = h->pos_b = h->hist = h->flag = h->seg = h->lflags = nullptr;
+  h->digit = h->parent = h->first = h->cstart = h->partial = nullptr;
+  h->cap = 0;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, int64_t count) {
+  return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1));
+}
+
+int ensure_plan(tt_engine* h, int64_t B) {
+  if (B <= h->cap) return TT_OK;
+  free_plan(h);
+  const int64_t cap = std::max<int64_t>(B, 1024);
+  const DevCfg& c = h->dc;
+  const int d = c.d;
+  const int64_t ntiles = (cap + RS_TILE - 1) / RS_TILE;
+  CU(dalloc(&h->keys_a, cap));
+  CU(dalloc(&h->keys_b, cap));
+  CU(dalloc(&h->uniq, cap));
+  CU(dalloc(&h->pos_a, cap));
+  CU(dalloc(&h->pos_b, cap));
+  CU(dalloc(&h->hist, ntiles * RS_BINS));
+  CU(dalloc(&h->flag, cap));
+  CU(dalloc(&h->seg, cap + 1));
+  CU(dalloc(&h->lflags, (int64_t)d * cap));
+  CU(dalloc(&h->digit, (int64_t)d * cap));
+  CU(dalloc(&h->parent, (int64_t)d * cap));
+  CU(dalloc(&h->first, (int64_t)d * cap));
+  CU(dalloc(&h->cstart, (int64_t)d * (cap + 1)));
+  const int64_t nblk = (cap + SC_BLOCK - 1) / SC_BLOCK;
+  h->partial_len = nblk;
+  CU(dalloc(&h->partial, nblk * TT_MAXD));
+  int64_t prod = 1;
+  for (int k = 0; k < d; ++k) {
+    prod = (prod > (int64_t)1 << 40) ? prod : prod * c.m[k];
+    h->capk[k] = std::min<int64_t>(cap, prod);
+    CU(dalloc(&h->gk[k][0], cap));
+    CU(dalloc(&h->gk[k][1], cap));
+    CU(dalloc(&h->gv[k][0], cap));
+    CU(dalloc(&h->gv[k][1], cap));
+    CU(dalloc(&h->goff[k], c.m[k] + 1));
+  }
+  h->cap = cap;
+  return TT_OK;
+}
+
+// generic-path level buffers (allocated on first generic use)
+int ensure_generic(tt_engine* h) {
+  const DevCfg& c = h->dc;
+  for (int k = 0; k < c.d; ++k) {
+    if (k >= 1 && k + 1 < c.d && !h->L.P[k]) CU(dalloc(&h->L.P[k], h->capk[k] * c.rows[k] * c.cols[k]));
+    if (!h->L.dP[k]) CU(dalloc(&h->L.dP[k], h->capk[k] * c.rows[k] * c.cols[k]));
+    if (k >= 1 && !h->L.dPc[k]) CU(dalloc(&h->L.dPc[k], h->capk[k] * c.rows[k] * c.R[k]));
+  }
+  return TT_OK;
+}
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)            \
+  do {                                                            \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);   \
+    ++h->launches;                                                \
+  } while (0)
+
+template <class K>
+K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, const int* n_dev, int n_host,
+              int64_t nmax, int nbits, int** vout) {
+  const int ntiles = (int)((nmax + RS_TILE - 1) / RS_TILE);
+  K* kin = ka; K* kout = kb;
+  int* vin = va; int* vo = vb;
+  for (int shift = 0; shift < nbits; shift += 8) {
+    LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, h->hist, ntiles);
+    LAUNCH(k_scan_excl_single, 1, 1024, 0, s, h->hist, ntiles * RS_BINS);
+    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, 0, s, kin, vin, kout, vo, n_dev, n_host, shift, h->hist, ntiles);
+    std::swap(kin, kout);
+    std::swap(vin, vo);
+  }
+  *vout = vin;
+  return kin;
+}
+
+void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax) {
+  const int nblk = (int)((nmax + SC_BLOCK - 1) / SC_BLOCK);
+  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
+  LAUNCH(k_scan_partials, narr, 1024, 0, s, h->partial, nblk);
+  LAUNCH(k_scan_add, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
+}
+
+__global__ void k_set_int(int* p, int v) { *p = v; }
+__global__ void k_reset_status(DevStatus* st, int which) {
+  if (which & 1) st->bad_pos = TT_NO_POS;
+  if (which & 2) st->bad_core = INT_MAX;
+}
+
+// Build the plan for a batch: validate, sort, unique, prefix levels, groups.
+int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
+  int rc = ensure_plan(h, B);
+  if (rc) return rc;
+  const DevCfg& c = h->dc;
+  const int d = c.d;
+  const int64_t cap = h->cap;
+  h->B = B;
+  h->last_idx = d_idx;
+  LAUNCH(k_set_int, 1, 1, 0, s, h->counts + TT_MAXD, (int)B);
+  h->d_B = h->counts + TT_MAXD;
+  LAUNCH(k_decompose_validate, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, c.num_nodes, h->keys_a, h->pos_a, h->st);
+  const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
+  h->skeys = radix_sort<unsigned long long>(h, s, h->keys_a, h->pos_a, h->keys_b, h->pos_b, nullptr, (int)B, B,
+                                            idbits, &h->spos);
+  LAUNCH(k_unique_flags, grid_for(B, 256, INT_MAX), 256, 0, s, h->skeys, (int)B, h->flag, h->st);
+  scan_inclusive(h, s, h->flag, 0, 1, h->d_B, B);
+  LAUNCH(k_unique_emit, grid_for(B, 256, INT_MAX), 256, 0, s, h->skeys, (int)B, h->flag, h->uniq, h->seg, h->counts,
+         d, h->st);
+  const int* U = h->counts + (d - 1);
+  LAUNCH(k_level_flags, grid_for(B, 256, INT_MAX), 256, 0, s, c, h->uniq, h->counts, h->lflags, cap);
+  scan_inclusive(h, s, h->lflags, cap, d - 1, U, B);
+  LAUNCH(k_level_emit, grid_for(B, 256, INT_MAX), 256, 0, s, c, h->uniq, h->counts, h->lflags, cap, h->digit,
+         h->parent, h->first);
+  LAUNCH(k_children, dim3(grid_for(B + 1, 256, INT_MAX), d - 1), 256, 0, s, c, h->counts, h->lflags, cap, h->first,
+         h->cstart);
+  // digit groups: level 0 is already digit-sorted and distinct
+  LAUNCH(k_iota, grid_for(B, 256, INT_MAX), 256, 0, s, h->gv[0][0], h->counts);
+  LAUNCH(k_digits_copy_u32, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit, h->counts, h->gk[0][0]);
+  h->order[0] = h->gv[0][0];
+  h->sdig[0] = h->gk[0][0];
+  LAUNCH(k_group_offsets, grid_for(c.m[0] + 1, 256, INT_MAX), 256, 0, s, h->gk[0][0], h->counts, (int)c.m[0],
+         h->goff[0]);
+  for (int k = 1; k < d; ++k) {
+    LAUNCH(k_digits_to_keys, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit + k * cap, h->counts + k, h->gk[k][0],
+           h->gv[k][0]);
+    const int nb = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.m[k] - 1)));
+    h->sdig[k] = radix_sort<unsigned>(h, s, h->gk[k][0], h->gv[k][0], h->gk[k][1], h->gv[k][1], h->counts + k, 0,
+                                      h->capk[k], nb, &h->order[k]);
+    LAUNCH(k_group_offsets, grid_for(c.m[k] + 1, 256, INT_MAX), 256, 0, s, h->sdig[k], h->counts + k, (int)c.m[k],
+           h->goff[k]);
+  }
+  return TT_OK;
+}
+
+int gen_forward(tt_engine* h, float* d_out, cudaStream_t s) {
+  int rc = ensure_generic(h);
+  if (rc) return rc;
+  const DevCfg& c = h->dc;
+  const int64_t cap = h->cap;
+  for (int k = 1; k < c.d; ++k) {
+    const int64_t total = h->capk[k] * c.rows[k] * c.cols[k];
+    LAUNCH(k_gen_fwd_level, grid_for(total), 256, 0, s, c, k, h->params, h->L, h->counts, h->digit + k * cap,
+           h->parent + k * cap, h->digit, h->seg, h->spos, d_out, h->st);
+  }
+  return TT_OK;
+}
+
+int gen_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
+  int rc = ensure_generic(h);
+  if (rc) return rc;
+  const DevCfg& c = h->dc;
+  const int d = c.d;
+  const int64_t cap = h->cap;
+  LAUNCH(k_gen_dy, grid_for(h->capk[d - 1] * c.npad), 256, 0, s, c, d_up, h->counts, h->seg, h->spos,
+         h->L.dP[d - 1], h->st);
+  for (int k = d - 1; k >= 1; --k) {
+    LAUNCH(k_gen_bwd_input, grid_for(h->capk[k] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->params, h->L, h->counts,
+           h->digit + k * cap, h->st);
+    LAUNCH(k_gen_bwd_weight, grid_for(c.m[k] * c.R[k] * c.cols[k]), 256, 0, s, c, k, h->params, h->L, h->goff[k],
+           h->order[k], h->parent + k * cap, h->digit, h->grads, h->st);
+    LAUNCH(k_gen_reduce_children, grid_for(h->capk[k - 1] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->L, h->counts,
+           h->cstart + (k - 1) * (cap + 1), h->st);
+  }
+  LAUNCH(k_gen_bwd_core0, grid_for(h->capk[0] * c.cols[0]), 256, 0, s, c, h->L, h->counts, h->digit, h->grads,
+         h->st);
+  return TT_OK;
+}
+
+void touch_counters(tt_engine* h, cudaStream_t s) {
+  const DevCfg& c = h->dc;
+  for (int k = 0; k < c.d; ++k)
+    LAUNCH(k_touch_counters, grid_for(c.m[k], 256, INT_MAX), 256, 0, s, c, k, h->goff[k], h->grads, 0, h->st);
+}
+
+bool use_fused(tt_engine* h) { return h->path_pref == 0 && h->fused_ok; }
+
+int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cudaStream_t s, bool write_out) {
+  LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 1);
+  int rc = build_plan(h, d_idx, B, s);
+  if (rc) return rc;
+  if (use_fused(h)) {
+    rc = fused_forward(h->fs, h->dc, h->F, h->cap, h->capk, h->params, h->counts, h->digit, h->parent, h->goff,
+                       h->order, h->seg, h->spos, write_out ? d_out : nullptr, h->st, s, h->launches);
+    h->last_path = 1;
+  } else {
+    rc = gen_forward(h, write_out ? d_out : nullptr, s);
+    h->last_path = 0;
+  }
+  if (rc) return rc;
+  h->plan_valid = true;
+  h->plan_version = h->cores_version;
+  CU(cudaGetLastError());
+  return TT_OK;
+}
+
+int do_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
+  if (h->dense) CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
+  int rc;
+  if (h->last_path == 1)
+    rc = fused_backward(h->fs, h->dc, h->F, h->cap, h->capk, h->params, h->grads, h->counts, h->digit, h->parent,
+                        h->cstart, h->goff, h->order, h->seg, h->spos, d_up, h->st, s, h->launches);
+  else
+    rc = gen_backward(h, d_up, s);
+  if (rc) return rc;
+  touch_counters(h, s);
+  h->batch_count = h->B;
+  CU(cudaGetLastError());
+  return TT_OK;
+}
+
+int set_cfg(tt_engine* h, const tt_config_c* in) {
+  h->cfg = *in;
+  DevCfg& c = h->dc;
+  memset(&c, 0, sizeof(c));
+  c.d = in->d;
+  c.num_nodes = in->num_nodes;
+  c.emb_dim = in->emb_dim;
+  c.npad = 1;
+  for (int k = 0; k < c.d; ++k) {
+    c.m[k] = in->row_factors[k];
+    c.n[k] = in->col_factors[k];
+    c.npad *= c.n[k];
+  }
+  for (int k = 0; k <= c.d; ++k) c.R[k] = in->ranks[k];
+  int64_t acc = 1;
+  for (int k = c.d - 1; k >= 0; --k) { c.S[k] = acc; acc *= c.m[k]; }
+  acc = 1;
+  int64_t off = 0;
+  for (int k = 0; k < c.d; ++k) {
+    c.rows[k] = acc;
+    acc *= c.n[k];
+    c.cols[k] = c.n[k] * c.R[k + 1];
+    c.slice[k] = c.R[k] * c.cols[k];
+    c.core_off[k] = off;
+    off += c.m[k] * c.slice[k];
+  }
+  c.nparams = off;
+  int64_t toff = off;
+  for (int k = 0; k < c.d; ++k) { c.tc_off[k] = toff; toff += c.m[k]; }
+  h->ntc = toff - off;
+  return TT_OK;
+}
+
+int validate_cfg(const tt_config_c* c, std::string* why) {
+  auto bad = [&](const char* m) { if (why) *why = m; return TT_ERR_ARG; };
+  if (!c) return bad("TTConfig: null config");
+  if (c->num_nodes <= 0) return bad("TTConfig: num_nodes must be positive");
+  if (c->emb_dim <= 0) return bad("TTConfig: emb_dim must be positive");
+  if (c->d < 2) return bad("TTConfig: need at least 2 cores");
+  if (c->d > TT_MAX_CORES) return bad("TTConfig: at most TT_MAX_CORES cores supported");
+  if (c->ranks[0] != 1 || c->ranks[c->d] != 1) return bad("TTConfig: boundary ranks R_0 and R_d must be 1");
+  for (int k = 0; k <= c->d; ++k)
+    if (c->ranks[k] <= 0) return bad("TTConfig: ranks must be positive");
+  long double pr = 1, pc = 1;
+  for (int k = 0; k < c->d; ++k) {
+    if (c->row_factors[k] <= 0 || c->col_factors[k] <= 0) return bad("TTConfig: factors must be positive");
+    pr *= c->row_factors[k];
+    pc *= c->col_factors[k];
+  }
+  if (pr < c->num_nodes) return bad("TTConfig: prod(row_factors) < num_nodes");
+  if (pc < c->emb_dim) return bad("TTConfig: prod(col_factors) < emb_dim");
+  if (pr > 9.0e18L) return bad("TTConfig: prod(row_factors) overflows int64");
+  return TT_OK;
+}
+
+// index into the reference layout (R_{k-1}, m, n, R_k) from the device
+// layout [m][R_{k-1}][n][R_k]
+inline int64_t dev_index(const DevCfg& c, int k, int64_t r, int64_t i, int64_t j, int64_t s) {
+  return ((i * c.R[k] + r) * c.n[k] + j) * c.R[k + 1] + s;
+}
+
+template <class T>
+void to_device_layout(const DevCfg& c, const T* const* cores, std::vector<float>& out) {
+  out.assign((size_t)c.nparams, 0.f);
+  for (int k = 0; k < c.d; ++k) {
+    const T* src = cores[k];
+    float* dst = out.data() + c.core_off[k];
+    int64_t e = 0;
+    for (int64_t r = 0; r < c.R[k]; ++r)
+      for (int64_t i = 0; i < c.m[k]; ++i)
+        for (int64_t j = 0; j < c.n[k]; ++j)
+          for (int64_t s = 0; s < c.R[k + 1]; ++s) dst[dev_index(c, k, r, i, j, s)] = (float)src[e++];
+  }
+}
+
+template <class T>
+void from_device_layout(const DevCfg& c, const std::vector<float>& in, T* const* cores, const float* tc) {
+  for (int k = 0; k < c.d; ++k) {
+    T* dst = cores[k];
+    const float* src = in.data() + c.core_off[k];
+    int64_t e = 0;
+    for (int64_t r = 0; r < c.R[k]; ++r)
+      for (int64_t i = 0; i < c.m[k]; ++i) {
+        const bool live = !tc || tc[c.tc_off[k] - c.nparams + i] > 0.f;
+        for (int64_t j = 0; j < c.n[k]; ++j)
+          for (int64_t s = 0; s < c.R[k + 1]; ++s) dst[e++] = live ? (T)src[dev_index(c, k, r, i, j, s)] : (T)0;
+      }
+  }
+}
+
+int ensure_stage(tt_engine* h, int64_t B) {
+  if (B <= h->stage_cap) return TT_OK;
+  cudaFree(h->st_idx); cudaFree(h->st_out); cudaFree(h->st_up);
+  const int64_t cap = std::max<int64_t>(B, 1024);
+  CU(dalloc(&h->st_idx, cap));
+  CU(dalloc(&h->st_out, cap * h->dc.emb_dim));
+  CU(dalloc(&h->st_up, cap * h->dc.emb_dim));
+  h->stage_cap = cap;
+  return TT_OK;
+}
+
+int read_status(tt_engine* h, cudaStream_t s) {
+  CU(cudaStreamSynchronize(s));
+  DevStatus st;
+  CU(cudaMemcpy(&st, h->st, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st.bad_pos != TT_NO_POS) {
+    int64_t val = 0;
+    if (h->last_idx) cudaMemcpy(&val, h->last_idx + st.bad_pos, sizeof(val), cudaMemcpyDeviceToHost);
+    LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 3);
+    CU(cudaStreamSynchronize(s));
+    h->plan_valid = false;
+    return fail(TT_ERR_INDEX,
+                "lookup_batch: index " + std::to_string(val) + " at batch position " +
+                    std::to_string((long long)st.bad_pos) + " out of [0, " + std::to_string(h->dc.num_nodes) + ")",
+                (int64_t)st.bad_pos, val);
+  }
+  if (st.bad_core != INT_MAX) {
+    LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 2);
+    CU(cudaStreamSynchronize(s));
+    return fail(TT_ERR_NONFINITE,
+                "apply_update: non-finite gradient in core " + std::to_string(st.bad_core) + "; update rejected",
+                st.bad_core);
+  }
+  return TT_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int tt_config_validate(const tt_config_c* cfg) {
+  std::string why;
+  int rc = validate_cfg(cfg, &why);
+  return rc ? fail(rc, why) : TT_OK;
+}
+
+int64_t tt_count_params(const tt_config_c* cfg) {
+  if (validate_cfg(cfg, nullptr)) return -1;
+  int64_t t = 0;
+  for (int k = 0; k < cfg->d; ++k)
+    t += cfg->ranks[k] * cfg->row_factors[k] * cfg->col_factors[k] * cfg->ranks[k + 1];
+  return t;
+}
+
+int tt_engine_create(const tt_config_c* cfg, int device, tt_engine** out) {
+  if (!out) return fail(TT_ERR_ARG, "tt_engine_create: null output handle");
+  *out = nullptr;
+  std::string why;
+  if (validate_cfg(cfg, &why)) return fail(TT_ERR_ARG, why);
+  CU(cudaSetDevice(device));
+  tt_engine* h = new tt_engine();
+  h->device = device;
+  set_cfg(h, cfg);
+  cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, device);
+  auto cleanup = [&](int code) { tt_engine_destroy(h); return code; };
+  if (cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking) != cudaSuccess) return cleanup(fail(TT_ERR_CUDA, "stream"));
+  if (dalloc(&h->params, h->dc.nparams) || dalloc(&h->own_grads, h->dc.nparams + h->ntc) ||
+      dalloc(&h->d_step, 1) || dalloc(&h->st, 1) || dalloc(&h->counts, 2 * TT_MAXD))
+    return cleanup(fail(TT_ERR_NOMEM, "tt_engine_create: device allocation failed"));
+  h->grads = h->own_grads;
+  cudaMemset(h->params, 0, sizeof(float) * (size_t)h->dc.nparams);
+  cudaMemset(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc));
+  cudaMemset(h->d_step, 0, sizeof(long long));
+  cudaMemset(h->counts, 0, sizeof(int) * 2 * TT_MAXD);
+  DevStatus st0{TT_NO_POS, INT_MAX, 0};
+  cudaMemcpy(h->st, &st0, sizeof(st0), cudaMemcpyHostToDevice);
+  h->fused_ok = fused_plan_shape(h->dc, &h->fs);
+  if (cudaGetLastError() != cudaSuccess) return cleanup(fail(TT_ERR_CUDA, "tt_engine_create: CUDA error"));
+  *out = h;
+  return TT_OK;
+}
+
+void tt_engine_destroy(tt_engine* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->own) cudaStreamSynchronize(h->own);
+  free_plan(h);
+  void* ptrs[] = {h->params, h->own_grads, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
+  for (void* p : ptrs) cudaFree(p);
+  if (h->own) cudaStreamDestroy(h->own);
+  delete h;
+}
+
+int tt_set_cores_f64(tt_engine* h, const double* const* cores) {
+  if (!h || !cores) return fail(TT_ERR_ARG, "tt_set_cores: null argument");
+  std::vector<float> buf;
+  to_device_layout(h->dc, cores, buf);
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(h->params, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  ++h->cores_version;
+  return TT_OK;
+}
+
+int tt_set_cores_f32(tt_engine* h, const float* const* cores) {
+  if (!h || !cores) return fail(TT_ERR_ARG, "tt_set_cores: null argument");
+  std::vector<float> buf;
+  to_device_layout(h->dc, cores, buf);
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(h->params, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  ++h->cores_version;
+  return TT_OK;
+}
+
+int tt_get_cores_f64(tt_engine* h, double* const* cores) {
+  if (!h || !cores) return fail(TT_ERR_ARG, "tt_get_cores: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  std::vector<float> buf((size_t)h->dc.nparams);
+  CU(cudaMemcpy(buf.data(), h->params, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  from_device_layout(h->dc, buf, cores, nullptr);
+  return TT_OK;
+}
+
+int tt_get_cores_f32(tt_engine* h, float* const* cores) {
+  if (!h || !cores) return fail(TT_ERR_ARG, "tt_get_cores: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  std::vector<float> buf((size_t)h->dc.nparams);
+  CU(cudaMemcpy(buf.data(), h->params, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  from_device_layout(h->dc, buf, cores, nullptr);
+  return TT_OK;
+}
+
+int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_count) {
+  if (!h || !grads) return fail(TT_ERR_ARG, "tt_get_core_grads: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  std::vector<float> buf((size_t)(h->dc.nparams + h->ntc));
+  CU(cudaMemcpy(buf.data(), h->grads, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  from_device_layout(h->dc, buf, grads, buf.data() + h->dc.nparams);
+  if (batch_count) *batch_count = h->batch_count;
+  return TT_OK;
+}
+
+int tt_set_core_grads_f64(tt_engine* h, const double* const* grads, int64_t batch_count) {
+  if (!h || !grads) return fail(TT_ERR_ARG, "tt_set_core_grads: null argument");
+  std::vector<float> buf;
+  to_device_layout(h->dc, grads, buf);
+  buf.resize((size_t)(h->dc.nparams + h->ntc), 1.f);  // all slices touched
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(h->grads, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  h->batch_count = batch_count;
+  return TT_OK;
+}
+
+int tt_opt_init(tt_engine* h, int kind, double lr, double beta1, double beta2, double eps) {
+  if (!h) return fail(TT_ERR_ARG, "tt_opt_init: null handle");
+  if (kind < 0 || kind > 2) return fail(TT_ERR_ARG, "tt_opt_init: unknown optimizer kind");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  h->opt_kind = kind;
+  h->lr = lr;
+  h->beta1 = beta1 > 0 ? beta1 : 0.9;
+  h->beta2 = beta2 > 0 ? beta2 : 0.999;
+  h->eps = eps > 0 ? eps : (kind == TT_OPT_ADAGRAD ? 1e-10 : 1e-8);
+  cudaFree(h->s1); cudaFree(h->s2);
+  h->s1 = h->s2 = nullptr;
+  if (kind != TT_OPT_SGD) {
+    CU(dalloc(&h->s1, h->dc.nparams));
+    CU(cudaMemset(h->s1, 0, sizeof(float) * (size_t)h->dc.nparams));
+  }
+  if (kind == TT_OPT_ADAM) {
+    CU(dalloc(&h->s2, h->dc.nparams));
+    CU(cudaMemset(h->s2, 0, sizeof(float) * (size_t)h->dc.nparams));
+  }
+  CU(cudaMemset(h->d_step, 0, sizeof(long long)));
+  return TT_OK;
+}
+
+int tt_opt_get_step(tt_engine* h, int64_t* step) {
+  if (!h || !step) return fail(TT_ERR_ARG, "tt_opt_get_step: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  long long v = 0;
+  CU(cudaMemcpy(&v, h->d_step, sizeof(v), cudaMemcpyDeviceToHost));
+  *step = v;
+  return TT_OK;
+}
+
+int tt_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_forward: null handle");
+  if (B < 0 || B > INT_MAX / 2) return fail(TT_ERR_ARG, "tt_forward: batch size out of range");
+  if (B > 0 && (!d_idx || !d_out)) return fail(TT_ERR_ARG, "tt_forward: null device buffer");
+  CU(cudaSetDevice(h->device));
+  if (B == 0) { h->plan_valid = false; return TT_OK; }  // empty batch -> 0 x N
+  return do_forward(h, d_idx, B, d_out, (cudaStream_t)stream, true);
+}
+
+int tt_backward(tt_engine* h, const int64_t* d_idx, int64_t B, const float* d_up, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_backward: null handle");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B < 0 || B > INT_MAX / 2) return fail(TT_ERR_ARG, "backward_lookup: upstream rows != index count");
+  if (B > 0 && !d_up) return fail(TT_ERR_ARG, "backward_lookup: null upstream buffer");
+  if (d_idx == nullptr) {
+    if (!h->plan_valid || h->plan_version != h->cores_version || B != h->B)
+      return fail(TT_ERR_STATE, "tt_backward: no matching forward plan (run tt_forward on this batch first)");
+  } else {
+    if (B == 0) {
+      CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
+      h->batch_count = 0;
+      return TT_OK;
+    }
+    int rc = do_forward(h, d_idx, B, nullptr, s, false);
+    if (rc) return rc;
+  }
+  return do_backward(h, d_up, s);
+}
+
+int tt_step(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_step: null handle");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevCfg& c = h->dc;
+  LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 2);
+  LAUNCH(k_check_finite, grid_for(c.nparams), 256, 0, s, c, h->grads, h->st);
+  LAUNCH(k_update, grid_for(c.nparams), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, h->opt_kind, (float)h->lr,
+         (float)h->beta1, (float)h->beta2, (float)h->eps, h->d_step, h->st);
+  LAUNCH(k_commit_step, 1, 1, 0, s, h->d_step, h->st);
+  ++h->cores_version;
+  CU(cudaGetLastError());
+  return TT_OK;
+}
+
+int tt_sync(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_sync: null handle");
+  CU(cudaSetDevice(h->device));
+  return read_status(h, (cudaStream_t)stream);
+}
+
+int tt_lookup_batch(tt_engine* h, const int64_t* h_idx, int64_t B, float* h_out) {
+  if (!h) return fail(TT_ERR_ARG, "lookup_batch: null handle");
+  if (B < 0) return fail(TT_ERR_ARG, "lookup_batch: negative batch");
+  if (B == 0) return TT_OK;
+  if (!h_idx || !h_out) return fail(TT_ERR_ARG, "lookup_batch: null buffer");
+  CU(cudaSetDevice(h->device));
+  int rc = ensure_stage(h, B);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, h->own));
+  rc = tt_forward(h, h->st_idx, B, h->st_out, h->own);
+  if (rc) return rc;
+  rc = read_status(h, h->own);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(h_out, h->st_out, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyDeviceToHost, h->own));
+  CU(cudaStreamSynchronize(h->own));
+  return TT_OK;
+}
+
+int tt_backward_lookup(tt_engine* h, const int64_t* h_idx, int64_t B, const float* h_up) {
+  if (!h) return fail(TT_ERR_ARG, "backward_lookup: null handle");
+  if (B < 0) return fail(TT_ERR_ARG, "backward_lookup: negative batch");
+  CU(cudaSetDevice(h->device));
+  if (B == 0) {  // CoreGradients::zeros with batch_count 0 (autodiff.cpp:40-46)
+    CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), h->own));
+    CU(cudaStreamSynchronize(h->own));
+    h->batch_count = 0;
+    return TT_OK;
+  }
+  if (!h_idx || !h_up) return fail(TT_ERR_ARG, "backward_lookup: null buffer");
+  int rc = ensure_stage(h, B);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, h->own));
+  CU(cudaMemcpyAsync(h->st_up, h_up, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyHostToDevice, h->own));
+  rc = tt_backward(h, h->st_idx, B, h->st_up, h->own);
+  if (rc) return rc;
+  rc = read_status(h, h->own);
+  if (rc == TT_ERR_INDEX) g_err = "backward_lookup" + g_err.substr(g_err.find(':'));
+  return rc;
+}
+
+int tt_apply_update(tt_engine* h) {
+  if (!h) return fail(TT_ERR_ARG, "apply_update: null handle");
+  int rc = tt_step(h, h->own);
+  if (rc) return rc;
+  return read_status(h, h->own);
+}
+
+int tt_train_step_host(tt_engine* h, const int64_t* h_idx, int64_t B, const float* h_up, float* h_out) {
+  if (!h) return fail(TT_ERR_ARG, "tt_train_step_host: null handle");
+  if (B <= 0 || !h_idx || !h_up) return fail(TT_ERR_ARG, "tt_train_step_host: empty batch or null buffer");
+  CU(cudaSetDevice(h->device));
+  int rc = ensure_stage(h, B);
+  if (rc) return rc;
+  cudaStream_t s = h->own;
+  CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h->st_up, h_up, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyHostToDevice, s));
+  rc = tt_forward(h, h->st_idx, B, h->st_out, s);
+  if (rc) return rc;
+  if (h_out) CU(cudaMemcpyAsync(h_out, h->st_out, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyDeviceToHost, s));
+  rc = tt_backward(h, nullptr, B, h->st_up, s);
+  if (rc) return rc;
+  rc = tt_step(h, s);
+  if (rc) return rc;
+  return read_status(h, s);
+}
+
+int tt_grad_buffer(tt_engine* h, float** d_ptr, int64_t* count) {
+  if (!h || !d_ptr || !count) return fail(TT_ERR_ARG, "tt_grad_buffer: null argument");
+  *d_ptr = h->grads;
+  *count = h->dc.nparams + h->ntc;
+  return TT_OK;
+}
+
+int tt_bind_grad_buffer(tt_engine* h, float* d_ptr, int64_t count) {
+  if (!h) return fail(TT_ERR_ARG, "tt_bind_grad_buffer: null handle");
+  const int64_t need = h->dc.nparams + h->ntc;
+  if (d_ptr && count < need) return fail(TT_ERR_ARG, "tt_bind_grad_buffer: buffer too small");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  float* target = d_ptr ? d_ptr : h->own_grads;
+  if (target != h->grads) {
+    CU(cudaMemcpy(target, h->grads, sizeof(float) * (size_t)need, cudaMemcpyDeviceToDevice));
+    h->grads = target;
+  }
+  return TT_OK;
+}
+
+int tt_set_dense_grads(tt_engine* h, int on) {
+  if (!h) return fail(TT_ERR_ARG, "tt_set_dense_grads: null handle");
+  h->dense = on != 0;
+  return TT_OK;
+}
+
+int tt_plan_stats(tt_engine* h, int64_t* out) {
+  if (!h || !out) return fail(TT_ERR_ARG, "tt_plan_stats: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  int c[TT_MAXD];
+  CU(cudaMemcpy(c, h->counts, sizeof(int) * h->dc.d, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < h->dc.d; ++k) out[k] = c[k];
+  return TT_OK;
+}
+
+int64_t tt_plan_digits(tt_engine* h, int64_t* ids, int32_t* digits, int64_t capn) {
+  if (!h || !h->cap) return -1;
+  if (cudaSetDevice(h->device) || cudaDeviceSynchronize()) return -1;
+  const int d = h->dc.d;
+  int c[TT_MAXD];
+  cudaMemcpy(c, h->counts, sizeof(int) * d, cudaMemcpyDeviceToHost);
+  const int64_t U = c[d - 1];
+  if (U > capn) return U;
+  std::vector<unsigned long long> uq(U);
+  std::vector<int> dig((size_t)d * h->cap), par((size_t)d * h->cap);
+  cudaMemcpy(uq.data(), h->uniq, sizeof(unsigned long long) * U, cudaMemcpyDeviceToHost);
+  cudaMemcpy(dig.data(), h->digit, sizeof(int) * dig.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(par.data(), h->parent, sizeof(int) * par.size(), cudaMemcpyDeviceToHost);
+  for (int64_t u = 0; u < U; ++u) {
+    ids[u] = (int64_t)uq[u];
+    int64_t node = u;
+    for (int k = d - 1; k >= 0; --k) {
+      digits[u * d + k] = dig[(size_t)k * h->cap + node];
+      node = par[(size_t)k * h->cap + node];
+    }
+  }
+  return U;
+}
+
+int64_t tt_plan_sorted(tt_engine* h, int64_t* keys, int32_t* pos, int64_t capn) {
+  if (!h || !h->cap) return -1;
+  if (cudaSetDevice(h->device) || cudaDeviceSynchronize()) return -1;
+  if (h->B > capn) return h->B;
+  std::vector<unsigned long long> k((size_t)h->B);
+  cudaMemcpy(k.data(), h->skeys, sizeof(unsigned long long) * h->B, cudaMemcpyDeviceToHost);
+  cudaMemcpy(pos, h->spos, sizeof(int) * h->B, cudaMemcpyDeviceToHost);
+  for (int64_t i = 0; i < h->B; ++i) keys[i] = (int64_t)k[i];
+  return h->B;
+}
+
+int64_t tt_launch_count(tt_engine* h) { return h ? h->launches : -1; }
+
+int tt_set_path(tt_engine* h, int path) {
+  if (!h || path < 0 || path > 1) return fail(TT_ERR_ARG, "tt_set_path: bad argument");
+  h->path_pref = path;
+  h->plan_valid = false;
+  return TT_OK;
+}
+
+int tt_last_path(tt_engine* h) { return h ? h->last_path : -1; }
+
+int64_t tt_last_error_position(void) { return g_err_pos; }
+int64_t tt_last_error_value(void) { return g_err_val; }
+const char* tt_last_error(void) { return g_err.c_str(); }
+
+double tt_ffma_peak_tflops(int device, int iters) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  cudaMalloc(&out, sizeof(float) * nsm * 8);
+  const int blocks = nsm * 8;
+  k_ffma_peak<<<blocks, 256>>>(out, 16, 1.0001f, 0.5f);  // warm-up
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_ffma_peak<<<blocks, 256>>>(out, iters, 1.0001f, 0.5f);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  const double flops = 2.0 * 8 * 16 * (double)iters * 256.0 * blocks;
+  return ms > 0 ? flops / (ms * 1e-3) / 1e12 : -1.0;
+}
+
+}  // extern "C"

@@ -1,0 +1,393 @@
+// kernels_plan.cuh -- K1 (decompose + validate) and K2 (radix sort, unique,
+// prefix levels, digit groups).  Integer work: HBM/latency bound, no tensor
+// cores.  Every count that depends on the batch's content stays on the
+// device; grids are sized by host-known upper bounds and kernels read the
+// live count, so the whole plan is stream-ordered (graph-capturable) with no
+// host round trip.
+#pragma once
+#include "common.cuh"
+
+namespace tt {
+
+// ---------------------------------------------------------------------------
+// K1: validate every index (tt_embedding.cpp:112-117, autodiff.cpp:57-60) and
+// emit (key, position) pairs.  The minimum offending position is recorded
+// (the reference reports the first in input order).
+__global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B, int64_t num_nodes,
+                                     unsigned long long* __restrict__ keys, int* __restrict__ pos,
+                                     DevStatus* st) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int64_t id = idx[b];
+  bool bad = id < 0 || id >= num_nodes;
+  unsigned ballot = __ballot_sync(__activemask(), bad);
+  if (ballot) {
+    // lowest bad lane of the warp reports: one atomic per warp
+    if (bad && (ballot & lanemask_lt()) == 0) atomicMin(&st->bad_pos, (unsigned long long)b);
+  }
+  keys[b] = bad ? 0ull : (unsigned long long)id;
+  pos[b] = (int)b;
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort, 8-bit digits, (key, int value) pairs.
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_PER_WARP = 512;
+constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;  // 4096 keys per tile
+constexpr int RS_BINS = 256;
+
+template <class K>
+__device__ __forceinline__ int rs_count(const int* n_dev, int n_host) {
+  return n_dev ? ld_count(n_dev) : n_host;
+}
+
+// per-tile digit histogram -> hist[digit * ntiles + tile]
+template <class K>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, const int* n_dev,
+                                                        int n_host, int shift, int* __restrict__ hist,
+                                                        int ntiles) {
+  __shared__ int cnt[RS_BINS];
+  const int n = rs_count<K>(n_dev, n_host);
+  for (int i = threadIdx.x; i < RS_BINS; i += RS_THREADS) cnt[i] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * RS_TILE;
+  if (base < n) {
+    for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
+      int g = base + i;
+      if (g < n) atomicAdd(&cnt[(int)((keys[g] >> shift) & 0xFF)], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < RS_BINS; i += RS_THREADS) hist[i * ntiles + blockIdx.x] = cnt[i];
+}
+
+// exclusive scan of an int array of host-known length (single block).
+__global__ void __launch_bounds__(1024) k_scan_excl_single(int* __restrict__ a, int len) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < len; base += 1024 * 8) {
+    int v[8];
+    int t = 0;
+    const int i0 = base + threadIdx.x * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = (i0 + j < len) ? a[i0 + j] : 0;
+      t += v[j];
+    }
+    // block exclusive scan of t
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane_id() >= (unsigned)o) x += y;
+    }
+    if (lane_id() == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = wsum[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane_id() >= (unsigned)o) w += y;
+      }
+      wsum[threadIdx.x] = w;  // inclusive per warp
+    }
+    __syncthreads();
+    int excl = carry + (x - t) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (i0 + j < len) a[i0 + j] = excl;
+      excl += v[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl;
+    __syncthreads();
+  }
+}
+
+// stable scatter of one tile using per-warp ranks (match_any peers).
+template <class K>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const int* __restrict__ vin,
+                                                           K* __restrict__ kout, int* __restrict__ vout,
+                                                           const int* n_dev, int n_host, int shift,
+                                                           const int* __restrict__ hist_scanned, int ntiles) {
+  __shared__ int cnt[RS_WARPS][RS_BINS];
+  const int n = rs_count<K>(n_dev, n_host);
+  const int tile = blockIdx.x;
+  if (tile * RS_TILE >= n) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int wbase = tile * RS_TILE + w * RS_PER_WARP;
+  for (int r = 0; r < RS_PER_WARP / 32; ++r) {
+    int g = wbase + r * 32 + lane;
+    int dig = g < n ? (int)((kin[g] >> shift) & 0xFF) : RS_BINS + lane;
+    unsigned peers = __match_any_sync(0xffffffffu, dig);
+    int leader = 31 - __clz(peers);
+    if (g < n && lane == leader) cnt[w][dig] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int dgt = threadIdx.x; dgt < RS_BINS; dgt += RS_THREADS) {
+    int run = hist_scanned[dgt * ntiles + tile];
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      int c = cnt[ww][dgt];
+      cnt[ww][dgt] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < RS_PER_WARP / 32; ++r) {
+    int g = wbase + r * 32 + lane;
+    K key = g < n ? kin[g] : (K)0;
+    int dig = g < n ? (int)((key >> shift) & 0xFF) : RS_BINS + lane;
+    unsigned peers = __match_any_sync(0xffffffffu, dig);
+    int leader = 31 - __clz(peers);
+    if (g < n) {
+      int dst = cnt[w][dig] + __popc(peers & lanemask_lt());
+      kout[dst] = key;
+      vout[dst] = vin[g];
+    }
+    __syncwarp();
+    if (g < n && lane == leader) cnt[w][dig] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// In-place inclusive scan of `narr` int arrays (stride apart) whose live
+// length is *n_dev.  Three phases: per-block scan, scan of block totals,
+// add-back.
+constexpr int SC_THREADS = 256;
+constexpr int SC_ITEMS = 8;
+constexpr int SC_BLOCK = SC_THREADS * SC_ITEMS;
+
+__device__ __forceinline__ int block_excl_scan_256(int t, int* wsum, int& total) {
+  int x = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane_id() >= (unsigned)o) x += y;
+  }
+  if (lane_id() == 31) wsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int w = threadIdx.x < SC_THREADS / 32 ? wsum[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane_id() >= (unsigned)o) w += y;
+    }
+    if (threadIdx.x < SC_THREADS / 32) wsum[threadIdx.x] = w;
+  }
+  __syncthreads();
+  total = wsum[SC_THREADS / 32 - 1];
+  int r = (x - t) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a, int64_t stride,
+                                                            const int* n_dev, int* __restrict__ partial,
+                                                            int nblk) {
+  __shared__ int wsum[SC_THREADS / 32];
+  const int n = ld_count(n_dev);
+  int* arr = a + blockIdx.y * stride;
+  const int i0 = blockIdx.x * SC_BLOCK + threadIdx.x * SC_ITEMS;
+  if (blockIdx.x * SC_BLOCK >= n) {
+    if (threadIdx.x == 0) partial[blockIdx.y * nblk + blockIdx.x] = 0;
+    return;
+  }
+  int v[SC_ITEMS];
+  int t = 0;
+#pragma unroll
+  for (int j = 0; j < SC_ITEMS; ++j) {
+    v[j] = (i0 + j < n) ? arr[i0 + j] : 0;
+    t += v[j];
+    v[j] = t;
+  }
+  int total;
+  int off = block_excl_scan_256(t, wsum, total);
+#pragma unroll
+  for (int j = 0; j < SC_ITEMS; ++j)
+    if (i0 + j < n) arr[i0 + j] = v[j] + off;
+  if (threadIdx.x == 0) partial[blockIdx.y * nblk + blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(int* __restrict__ partial, int nblk) {
+  // exclusive scan of partial[blockIdx.x * nblk ..]
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  int* p = partial + blockIdx.x * nblk;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nblk; base += 1024) {
+    int i = base + threadIdx.x;
+    int t = i < nblk ? p[i] : 0;
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane_id() >= (unsigned)o) x += y;
+    }
+    if (lane_id() == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = wsum[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane_id() >= (unsigned)o) w += y;
+      }
+      wsum[threadIdx.x] = w;
+    }
+    __syncthreads();
+    int excl = carry + (x - t) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
+    if (i < nblk) p[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + t;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_add(int* __restrict__ a, int64_t stride, const int* n_dev,
+                                                         const int* __restrict__ partial, int nblk) {
+  const int n = ld_count(n_dev);
+  if (blockIdx.x == 0 || blockIdx.x * SC_BLOCK >= n) return;
+  int* arr = a + blockIdx.y * stride;
+  const int off = partial[blockIdx.y * nblk + blockIdx.x];
+  const int i0 = blockIdx.x * SC_BLOCK + threadIdx.x * SC_ITEMS;
+#pragma unroll
+  for (int j = 0; j < SC_ITEMS; ++j)
+    if (i0 + j < n) arr[i0 + j] += off;
+}
+
+// ---------------------------------------------------------------------------
+// unique IDs over the sorted keys
+__global__ void k_unique_flags(const unsigned long long* __restrict__ skey, int B, int* __restrict__ flag,
+                               const DevStatus* st) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B || tt_failed(st)) return;
+  flag[s] = (s == 0 || skey[s] != skey[s - 1]) ? 1 : 0;
+}
+
+// After the inclusive scan: uniq[u] = key, seg[u] = first sorted slot.
+// counts[d-1] = U, seg[U] = B.
+__global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B, const int* __restrict__ scan,
+                              unsigned long long* __restrict__ uniq, int* __restrict__ seg,
+                              int* __restrict__ counts, int d, const DevStatus* st) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B) return;
+  if (tt_failed(st)) {
+    if (s == 0)
+      for (int k = 0; k < d; ++k) counts[k] = 0;
+    return;
+  }
+  int u = scan[s] - 1;
+  if (s == 0 || skey[s] != skey[s - 1]) {
+    uniq[u] = skey[s];
+    seg[u] = s;
+  }
+  if (s == B - 1) {
+    counts[d - 1] = u + 1;
+    seg[u + 1] = B;
+  }
+}
+
+// Level flags: for 0-based level k < d-1, a new prefix (i_1..i_{k+1}) starts
+// at unique u.  flags laid out [k][cap].
+__global__ void k_level_flags(DevCfg c, const unsigned long long* __restrict__ uniq, const int* __restrict__ counts,
+                              int* __restrict__ flags, int64_t cap) {
+  const int U = ld_count(&counts[c.d - 1]);
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= U) return;
+  unsigned long long key = uniq[u], prev = u ? uniq[u - 1] : 0;
+  for (int k = 0; k + 1 < c.d; ++k) {
+    unsigned long long S = (unsigned long long)c.S[k];
+    flags[k * cap + u] = (u == 0 || key / S != prev / S) ? 1 : 0;
+  }
+}
+
+// Node arrays per level (0-based k): digit, parent, first unique.  Level d-1
+// nodes are the unique IDs themselves.
+__global__ void k_level_emit(DevCfg c, const unsigned long long* __restrict__ uniq, int* __restrict__ counts,
+                             const int* __restrict__ scan /*[k][cap] inclusive*/, int64_t cap,
+                             int* __restrict__ digit /*[k][cap]*/, int* __restrict__ parent,
+                             int* __restrict__ first) {
+  const int U = ld_count(&counts[c.d - 1]);
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= U) return;
+  unsigned long long key = uniq[u], prev = u ? uniq[u - 1] : 0;
+  for (int k = 0; k + 1 < c.d; ++k) {
+    unsigned long long S = (unsigned long long)c.S[k];
+    unsigned long long p = key / S;
+    if (u == 0 || p != prev / S) {
+      int node = scan[k * cap + u] - 1;
+      digit[k * cap + node] = (int)(p % (unsigned long long)c.m[k]);
+      first[k * cap + node] = u;
+      parent[k * cap + node] = k ? scan[(k - 1) * cap + u] - 1 : -1;
+    }
+    if (u == U - 1) counts[k] = scan[k * cap + u];
+  }
+  const int k = c.d - 1;
+  digit[k * cap + u] = (int)(key % (unsigned long long)c.m[k]);
+  first[k * cap + u] = u;
+  parent[k * cap + u] = scan[(k - 1) * cap + u] - 1;
+}
+
+// child ranges: level-k node n owns level-(k+1) nodes [cs[n], cs[n+1]).
+__global__ void k_children(DevCfg c, const int* __restrict__ counts, const int* __restrict__ scan, int64_t cap,
+                           const int* __restrict__ first, int* __restrict__ cstart /*[k][cap+1]*/) {
+  const int k = blockIdx.y;  // 0 .. d-2
+  const int cnt = ld_count(&counts[k]);
+  int nd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (nd > cnt) return;
+  int* cs = cstart + k * (cap + 1);
+  if (nd == cnt) {
+    cs[nd] = ld_count(&counts[k + 1]);
+    return;
+  }
+  int u = first[k * cap + nd];
+  cs[nd] = (k + 1 == c.d - 1) ? u : scan[(k + 1) * cap + u] - 1;
+}
+
+// copy node digits into sort keys (values = node index)
+__global__ void k_digits_to_keys(const int* __restrict__ digit, const int* n_dev, unsigned* __restrict__ keys,
+                                 int* __restrict__ vals) {
+  const int n = ld_count(n_dev);
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (unsigned)digit[i];
+  vals[i] = i;
+}
+
+// goff[v] = first slot whose sorted digit >= v, v in [0, m]
+__global__ void k_group_offsets(const unsigned* __restrict__ sdig, const int* n_dev, int m, int* __restrict__ goff) {
+  const int n = ld_count(n_dev);
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > m) return;
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((int)sdig[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  goff[v] = lo;
+}
+
+// level 0 (i_1 nodes): already sorted by digit and unique -> identity order
+__global__ void k_iota(int* __restrict__ a, const int* n_dev) {
+  const int n = ld_count(n_dev);
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+__global__ void k_digits_copy_u32(const int* __restrict__ digit, const int* n_dev, unsigned* __restrict__ out) {
+  const int n = ld_count(n_dev);
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (unsigned)digit[i];
+}
+
+}  // namespace tt
