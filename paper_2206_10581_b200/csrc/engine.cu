@@ -278,6 +278,7 @@ int gen_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   const DevCfg& c = h->dc;
   const int64_t cap = h->cap;
   for (int k = 1; k < c.d; ++k) {
+    if (k == c.d - 1 && !d_out) break;  // backward-only plan: the last level's rows are not needed
     const int64_t total = h->capk[k] * c.rows[k] * c.cols[k];
     LAUNCH(k_gen_fwd_level, grid_for(total), 256, 0, s, c, k, h->params, h->L, h->counts, h->digit + k * cap,
            h->parent + k * cap, h->digit, h->seg, h->spos, d_out, h->st);
@@ -306,6 +307,116 @@ int gen_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   return TT_OK;
 }
 
+int ensure_fused(tt_engine* h) {
+  const DevCfg& c = h->dc;
+  const FusedShape& f = h->fs;
+  FusedBufs& b = h->F;
+  const int64_t nodes = h->capk[f.F], ids = h->capk[c.d - 1];
+  if (b.cap_nodes >= nodes && b.cap_ids >= ids) return TT_OK;
+  free_fused(b);
+  CU(dalloc(&b.Psave, nodes * f.RP * f.NC));
+  CU(dalloc(&b.dPc, nodes * f.ncb * f.RP * f.K));
+  CU(dalloc(&b.W, ids * f.ncb * f.R2 * f.NL));
+  b.cap_nodes = nodes;
+  b.cap_ids = ids;
+  return TT_OK;
+}
+
+FusedArgs fused_args(tt_engine* h, float* d_out, const float* d_up) {
+  const DevCfg& c = h->dc;
+  const FusedShape& f = h->fs;
+  const int64_t cap = h->cap;
+  FusedArgs a{};
+  a.c = c;
+  a.F = f.F; a.ncb = f.ncb; a.RP = f.RP; a.R2 = f.R2; a.NL = f.NL; a.nF = f.nF; a.BNj = f.BNj; a.OUT = f.OUT; a.NC = f.NC;
+  a.params = h->params;
+  a.Aprev = f.F >= 2 ? h->L.P[f.F - 1] : nullptr;
+  a.digitF = h->digit + f.F * cap;
+  a.parentF = h->parent + f.F * cap;
+  a.digit0 = h->digit;
+  a.goffF = h->goff[f.F];
+  a.orderF = h->order[f.F];
+  a.cstartF = h->cstart + f.F * (cap + 1);
+  a.digitL = h->digit + (c.d - 1) * cap;
+  a.seg = h->seg;
+  a.spos = h->spos;
+  a.out = d_out;
+  a.Psave = h->F.Psave;
+  a.up = d_up;
+  a.W = h->F.W;
+  a.dPc = h->F.dPc;
+  a.grads = h->grads;
+  a.st = h->st;
+  return a;
+}
+
+#define FUSED_DISPATCH(KER, K_, BN_, GRID, SMEM, S, ARGS)                                   \
+  do {                                                                                     \
+    auto kfn = KER<K_, BN_>;                                                               \
+    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM))); \
+    kfn<<<(GRID), FB_THREADS, (SMEM), (S)>>>(ARGS);                                        \
+    ++h->launches;                                                                         \
+  } while (0)
+
+#define FUSED_SWITCH(KER, GRID, SMEM, S, ARGS)                                              \
+  do {                                                                                     \
+    const int K_ = h->fs.K, BN_ = h->fs.BN;                                                \
+    if (K_ == 16 && BN_ == 64) FUSED_DISPATCH(KER, 16, 64, GRID, SMEM, S, ARGS);           \
+    else if (K_ == 32 && BN_ == 128) FUSED_DISPATCH(KER, 32, 128, GRID, SMEM, S, ARGS);    \
+    else if (K_ == 64 && BN_ == 256) FUSED_DISPATCH(KER, 64, 256, GRID, SMEM, S, ARGS);    \
+    else if (K_ == 64 && BN_ == 128) FUSED_DISPATCH(KER, 64, 128, GRID, SMEM, S, ARGS);    \
+    else if (K_ == 128 && BN_ == 128) FUSED_DISPATCH(KER, 128, 128, GRID, SMEM, S, ARGS);  \
+    else return fail(TT_ERR_ARG, "fused path: unsupported tile shape");                    \
+  } while (0)
+
+int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
+  const DevCfg& c = h->dc;
+  const FusedShape& f = h->fs;
+  int rc = ensure_fused(h);
+  if (rc) return rc;
+  if (f.F >= 2) {
+    rc = ensure_generic(h);
+    if (rc) return rc;
+    const int64_t cap = h->cap;
+    for (int k = 1; k < f.F; ++k) {
+      const int64_t total = h->capk[k] * c.rows[k] * c.cols[k];
+      LAUNCH(k_gen_fwd_level, grid_for(total), 256, 0, s, c, k, h->params, h->L, h->counts, h->digit + k * cap,
+             h->parent + k * cap, h->digit, h->seg, h->spos, nullptr, h->st);
+    }
+  }
+  FusedArgs a = fused_args(h, d_out, nullptr);
+  FUSED_SWITCH(k_fused_fwd, (int)(c.m[f.F] * f.ncb), f.smem_fwd, s, a);
+  return TT_OK;
+}
+
+int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
+  const DevCfg& c = h->dc;
+  const FusedShape& f = h->fs;
+  const int d = c.d;
+  const int64_t cap = h->cap;
+  FusedArgs a = fused_args(h, nullptr, d_up);
+  FUSED_SWITCH(k_fused_bwd, (int)(c.m[f.F] * f.ncb), f.smem_bwd, s, a);
+  const int WE = f.R2 * f.NL;
+  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], std::min(1024, (WE + 31) / 32 * 32), 0, s, c, f.ncb, WE,
+         h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
+  const int per = f.RP * f.K;
+  float* dst = f.F == 1 ? h->grads : h->L.dP[f.F - 1];
+  LAUNCH(k_fused_reduce_children, grid_for(h->capk[f.F - 1] * per), 256, 0, s, c, f.F, f.ncb, per, h->counts,
+         h->cstart + (f.F - 1) * (cap + 1), h->digit, h->F.dPc, dst, h->st);
+  for (int k = f.F - 1; k >= 1; --k) {
+    LAUNCH(k_gen_bwd_input, grid_for(h->capk[k] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->params, h->L, h->counts,
+           h->digit + k * cap, h->st);
+    LAUNCH(k_gen_bwd_weight, grid_for(c.m[k] * c.R[k] * c.cols[k]), 256, 0, s, c, k, h->params, h->L, h->goff[k],
+           h->order[k], h->parent + k * cap, h->digit, h->grads, h->st);
+    LAUNCH(k_gen_reduce_children, grid_for(h->capk[k - 1] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->L, h->counts,
+           h->cstart + (k - 1) * (cap + 1), h->st);
+  }
+  if (f.F >= 2)
+    LAUNCH(k_gen_bwd_core0, grid_for(h->capk[0] * c.cols[0]), 256, 0, s, c, h->L, h->counts, h->digit, h->grads,
+           h->st);
+  return TT_OK;
+}
+
 void touch_counters(tt_engine* h, cudaStream_t s) {
   const DevCfg& c = h->dc;
   for (int k = 0; k < c.d; ++k)
@@ -319,8 +430,7 @@ int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cuda
   int rc = build_plan(h, d_idx, B, s);
   if (rc) return rc;
   if (use_fused(h)) {
-    rc = fused_forward(h->fs, h->dc, h->F, h->cap, h->capk, h->params, h->counts, h->digit, h->parent, h->goff,
-                       h->order, h->seg, h->spos, write_out ? d_out : nullptr, h->st, s, h->launches);
+    rc = fused_forward(h, write_out ? d_out : nullptr, s);
     h->last_path = 1;
   } else {
     rc = gen_forward(h, write_out ? d_out : nullptr, s);
@@ -337,8 +447,7 @@ int do_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   if (h->dense) CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
   int rc;
   if (h->last_path == 1)
-    rc = fused_backward(h->fs, h->dc, h->F, h->cap, h->capk, h->params, h->grads, h->counts, h->digit, h->parent,
-                        h->cstart, h->goff, h->order, h->seg, h->spos, d_up, h->st, s, h->launches);
+    rc = fused_backward(h, d_up, s);
   else
     rc = gen_backward(h, d_up, s);
   if (rc) return rc;
@@ -515,7 +624,8 @@ int tt_engine_create(const tt_config_c* cfg, int device, tt_engine** out) {
   cudaMemset(h->counts, 0, sizeof(int) * 2 * TT_MAXD);
   DevStatus st0{TT_NO_POS, INT_MAX, 0};
   cudaMemcpy(h->st, &st0, sizeof(st0), cudaMemcpyHostToDevice);
-  h->fused_ok = fused_plan_shape(h->dc, &h->fs);
+  h->fused_ok = fused_plan_shape(h->dc, &h->fs) &&
+                h->fs.smem_bwd <= 227 * 1024 && h->fs.smem_fwd <= 227 * 1024;
   if (cudaGetLastError() != cudaSuccess) return cleanup(fail(TT_ERR_CUDA, "tt_engine_create: CUDA error"));
   *out = h;
   return TT_OK;
