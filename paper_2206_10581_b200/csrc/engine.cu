@@ -18,6 +18,7 @@
 #include "kernels_fused.cuh"
 #include "kernels_generic.cuh"
 #include "kernels_plan.cuh"
+#include "kernels_rows.cuh"
 #include "kernels_update.cuh"
 
 using namespace tt;
@@ -311,27 +312,30 @@ int ensure_fused(tt_engine* h) {
   const DevCfg& c = h->dc;
   const FusedShape& f = h->fs;
   FusedBufs& b = h->F;
-  const int64_t nodes = h->capk[f.F], ids = h->capk[c.d - 1];
-  if (b.cap_nodes >= nodes && b.cap_ids >= ids) return TT_OK;
+  const int64_t nodes = h->capk[f.F], ids = h->capk[c.d - 1], chunks = (h->cap + DY_CHUNK - 1) / DY_CHUNK;
+  if (b.cap_nodes >= nodes && b.cap_ids >= ids && b.cap_chunks >= chunks) return TT_OK;
   free_fused(b);
   CU(dalloc(&b.Psave, nodes * f.RP * f.NC));
   CU(dalloc(&b.dPc, nodes * f.ncb * f.RP * f.K));
-  CU(dalloc(&b.W, ids * f.ncb * f.R2 * f.NL));
+  CU(dalloc(&b.W, ids * f.ncb * f.K * f.NL));
+  CU(dalloc(&b.dY, ids * c.npad));
+  CU(dalloc(&b.Yu, ids * c.npad));
+  CU(dalloc(&b.part, chunks * 2 * c.npad));
   b.cap_nodes = nodes;
   b.cap_ids = ids;
+  b.cap_chunks = chunks;
   return TT_OK;
 }
 
-FusedArgs fused_args(tt_engine* h, float* d_out, const float* d_up) {
+FusedArgs fused_args(tt_engine* h, float* d_out) {
   const DevCfg& c = h->dc;
   const FusedShape& f = h->fs;
   const int64_t cap = h->cap;
   FusedArgs a{};
   a.c = c;
-  a.F = f.F; a.ncb = f.ncb; a.RP = f.RP; a.R2 = f.R2; a.NL = f.NL; a.nF = f.nF; a.BNj = f.BNj; a.OUT = f.OUT; a.NC = f.NC;
+  a.F = f.F; a.ncb = f.ncb; a.RP = f.RP; a.NL = f.NL; a.nF = f.nF; a.BNj = f.BNj; a.OUT = f.OUT; a.NC = f.NC;
   a.params = h->params;
-  a.Aprev = f.F >= 2 ? h->L.P[f.F - 1] : nullptr;
-  a.digitF = h->digit + f.F * cap;
+  a.Abase = f.F >= 2 ? h->L.P[f.F - 1] : h->params;
   a.parentF = h->parent + f.F * cap;
   a.digit0 = h->digit;
   a.goffF = h->goff[f.F];
@@ -341,8 +345,9 @@ FusedArgs fused_args(tt_engine* h, float* d_out, const float* d_up) {
   a.seg = h->seg;
   a.spos = h->spos;
   a.out = d_out;
+  a.Yu = h->F.Yu;
   a.Psave = h->F.Psave;
-  a.up = d_up;
+  a.dY = h->F.dY;
   a.W = h->F.W;
   a.dPc = h->F.dPc;
   a.grads = h->grads;
@@ -384,8 +389,12 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
              h->parent + k * cap, h->digit, h->seg, h->spos, nullptr, h->st);
     }
   }
-  FusedArgs a = fused_args(h, d_out, nullptr);
+  FusedArgs a = fused_args(h, d_out);
+  a.CH = f.CHF;
   FUSED_SWITCH(k_fused_fwd, (int)(c.m[f.F] * f.ncb), f.smem_fwd, s, a);
+  if (d_out)
+    LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
+           h->spos, h->seg, h->F.Yu, d_out, h->st);
   return TT_OK;
 }
 
@@ -394,9 +403,15 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   const FusedShape& f = h->fs;
   const int d = c.d;
   const int64_t cap = h->cap;
-  FusedArgs a = fused_args(h, nullptr, d_up);
+  const int64_t chunks = (h->B + DY_CHUNK - 1) / DY_CHUNK;
+  LAUNCH(k_dy_chunks, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
+         h->seg, h->F.dY, h->F.part, h->st);
+  LAUNCH(k_dy_spans, (int)((h->capk[d - 1] + 7) / 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part, h->F.dY,
+         h->st);
+  FusedArgs a = fused_args(h, nullptr);
+  a.CH = f.CHB;
   FUSED_SWITCH(k_fused_bwd, (int)(c.m[f.F] * f.ncb), f.smem_bwd, s, a);
-  const int WE = f.R2 * f.NL;
+  const int WE = f.K * f.NL;
   LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], std::min(1024, (WE + 31) / 32 * 32), 0, s, c, f.ncb, WE,
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
   const int per = f.RP * f.K;

@@ -6,70 +6,79 @@
 // one GEMM  C (rows x NC) = A (rows x K) . S (K x NC)  with
 //   rows = (#nodes) x RP,  RP = prod_{p<F} n_p,  K = R_F,  NC = n_F R_{F+1},
 // where A stacks the parents' products (the core-0 slices when F = 1).  One
-// CTA owns a (group, column block) unit: the BN-column block of the slice is
-// staged once in shared memory (cp.async) and reused by every row tile of the
-// group; a tile is BM = 64 rows; 256 threads each own a register micro-tile;
-// the contraction is warp-level FFMA (fp32) out of shared memory.
+// CTA owns a (group, column block) unit: the K x BN block of the slice is
+// staged once in shared memory (cp.async) and reused by every 64-row tile of
+// the group; A tiles arrive by cp.async (double-buffered in the forward);
+// 256 threads each own a register micro-tile and contract with warp-level
+// FFMA (fp32) out of shared memory.  Ranks are uniform on this path
+// (R_{F+1} = R_F = K).
 //
-// Forward epilogue: the last level (R_d = 1) is applied straight from the C
-// tile in shared memory -- for every distinct ID under the tile's nodes,
-// out[(a, j_F, j_l)] = sum_r C[a][(j_F, r)] G_{d-1}[r, i_d, j_l] -- and the
-// row is written to every batch position holding that ID.  The C tile is also
-// saved (P_F) for the backward (the autograd pattern; no recompute).
+// Forward epilogue: the last level (R_d = 1) is applied from the C tile in
+// shared memory -- for every distinct ID under the tile's nodes,
+// out[(a, j_F, j_l)] = sum_r C[a][(j_F, r)] G_{d-1}[r, i_d, j_l] (slices staged
+// transposed in shared memory) -- and written to the ID's batch positions
+// (IDs with more than HEAVY_POS positions go through Yu and the balanced
+// k_scatter_heavy).  The C tile is saved (P_F) for the backward.
 //
-// Backward per unit: for each row tile
-//   W_u  (R_{F+1} x n_l)  = P_F[u's prefix]^T . dY_u    (dG_{d-1} partials)
-//   dC   (rows x BN)      = sum_u dY_u . G_{d-1}[i_d(u)]^T   (dP_F)
-//   dG_F block (K x BN)  += A^T . dC                  (registers, whole group)
-//   dA   (rows x K)       = dC . S_block^T              (dP_{F-1} partials)
-// so dG_F needs no atomics (one CTA per slice column block), and the W / dA
-// partials are reduced afterwards by sorted segmented reductions in a fixed
-// order (k_fused_reduce_last, k_fused_reduce_children).
+// Backward per unit, for each row tile (C-tile load overlapped with compute):
+//   dC   (rows x BN)      = sum_u dY_u . G_{d-1}[i_d(u)]^T        (dP_F)
+//   dG_F block (K x BN)  += A^T . dC      (registers across the whole group)
+//   dA   (rows x K)       = dC . S_block^T  -> dP_{F-1} partials
+//   W_u  (K x n_l)        = C_u^T . dY_u    -> dG_{d-1} partials
+// dG_F needs no atomics (one CTA per slice column block); the W / dA partials
+// are reduced by sorted segmented reductions in a fixed order
+// (k_fused_reduce_last, k_fused_reduce_children).
 #pragma once
 #include "common.cuh"
+#include "kernels_rows.cuh"
 
 namespace tt {
 
 constexpr int FB_THREADS = 256;
 constexpr int FB_BM = 64;
-constexpr int FB_CH = 16;  // distinct IDs staged per chunk in the backward
+constexpr int FB_SMEM_MAX = 227 * 1024;
 
 struct FusedShape {
   int ok;
   int F;       // fused level (d-2)
-  int K;       // R_F
+  int K;       // R_F = R_{F+1}
   int BN;      // column block
   int ncb;     // NC / BN
   int NC;      // n_F R_{F+1}
   int RP;      // rows per node at level F
-  int R2;      // R_{F+1}
   int NL;      // n_{d-1}
   int nF;      // n_F
-  int BNj;     // BN / R2
+  int BNj;     // BN / K
   int OUT;     // RP * BNj * NL outputs per ID per column block
+  int CHF, CHB;            // distinct IDs staged per chunk (fwd / bwd)
   size_t smem_fwd, smem_bwd;
 };
 
 struct FusedBufs {
   float* Psave = nullptr;  // [capk[F]][RP][NC]
-  float* W = nullptr;      // [capk[d-1]][ncb][R2*NL]
+  float* W = nullptr;      // [capk[d-1]][ncb][K*NL]
   float* dPc = nullptr;    // [capk[F]][ncb][RP*K]
-  int64_t cap_nodes = 0, cap_ids = 0;
+  float* dY = nullptr;     // [capk[d-1]][npad]   upstream summed per distinct ID
+  float* Yu = nullptr;     // [capk[d-1]][npad]   rows of heavy IDs
+  float* part = nullptr;   // [chunks][2][npad]   k_dy_chunks partials
+  int64_t cap_nodes = 0, cap_ids = 0, cap_chunks = 0;
 };
 
 inline void free_fused(FusedBufs& b) {
   cudaFree(b.Psave);
   cudaFree(b.W);
   cudaFree(b.dPc);
+  cudaFree(b.dY);
+  cudaFree(b.Yu);
+  cudaFree(b.part);
   b = FusedBufs{};
 }
 
 struct FusedArgs {
   DevCfg c;
-  int F, ncb, RP, R2, NL, nF, BNj, OUT, NC;
+  int F, ncb, RP, NL, nF, BNj, OUT, NC, CH;
   const float* params;
-  const float* Aprev;       // P_{F-1} buffer (F >= 2) or nullptr (F == 1: core-0 slices)
-  const int* digitF;        // level-F node digits
+  const float* Abase;       // core-0 parameters (F == 1) or the P_{F-1} buffer
   const int* parentF;       // level-F node parents
   const int* digit0;        // level-0 digits (F == 1)
   const int* goffF;         // group offsets over level-F digits
@@ -79,8 +88,9 @@ struct FusedArgs {
   const int* seg;           // distinct ID -> sorted batch slots
   const int* spos;          // sorted slot -> batch position
   float* out;               // forward rows (nullptr: no row output)
+  float* Yu;
   float* Psave;
-  const float* up;          // backward upstream rows
+  const float* dY;
   float* W;
   float* dPc;
   float* grads;
@@ -91,18 +101,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-
-__device__ __forceinline__ const float* fused_A(const FusedArgs& a, int node) {
-  const int p = a.parentF[node];
-  if (a.F == 1) return a.params + a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0];
-  return a.Aprev + (int64_t)p * a.RP * a.c.R[a.F];
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Stage the (K x BN) column block cb of slice g of core F: Bs[k][n], row stride SB.
-template <int K, int BN>
+template <int K, int BN, int SB>
 __device__ __forceinline__ void load_slice_block(const FusedArgs& a, int g, int cb, float* Bs) {
-  constexpr int SB = BN + 4;
   const float* src = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
   for (int i = threadIdx.x; i < K * BN / 4; i += FB_THREADS) {
     const int k = i / (BN / 4), q = i - k * (BN / 4);
@@ -110,8 +115,10 @@ __device__ __forceinline__ void load_slice_block(const FusedArgs& a, int g, int 
   }
 }
 
-// Per-tile node list and the prefix of their distinct-ID counts.
-__device__ __forceinline__ int tile_nodes(const FusedArgs& a, int t0, int nn, int* s_node, int* s_pref) {
+// Node list of the tile starting at group slot t0: node ids, prefix of their
+// distinct-ID counts, and each node's A-block offset.  Ends with a barrier.
+__device__ __forceinline__ int tile_nodes(const FusedArgs& a, int t0, int nn, int* s_node, int* s_pref,
+                                          int64_t* s_aoff) {
   if (threadIdx.x < 32) {
     int run = 0;
     for (int base = 0; base < nn; base += 32) {
@@ -120,6 +127,9 @@ __device__ __forceinline__ int tile_nodes(const FusedArgs& a, int t0, int nn, in
       if (j < nn) {
         node = a.orderF[t0 + j];
         cnt = a.cstartF[node + 1] - a.cstartF[node];
+        const int p = a.parentF[node];
+        s_aoff[j] = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0]
+                             : (int64_t)p * a.RP * a.c.R[a.F];
       }
       int x = cnt;
 #pragma unroll
@@ -139,7 +149,21 @@ __device__ __forceinline__ int tile_nodes(const FusedArgs& a, int t0, int nn, in
   return s_pref[nn];
 }
 
-// flat ID index f in [0, total) of the tile -> (node_local j, distinct ID u)
+// A tile (BM x K, row-major, stride K) by cp.async; rows past the tile's
+// nodes are zero-filled.
+template <int K>
+__device__ __forceinline__ void load_A_tile(const FusedArgs& a, int nn, const int64_t* s_aoff, float* As) {
+  const int RP = a.RP;
+  for (int i = threadIdx.x; i < FB_BM * K / 4; i += FB_THREADS) {
+    const int m = i / (K / 4), q = i - m * (K / 4);
+    const int j = m / RP;
+    float* dst = As + m * K + q * 4;
+    if (j < nn) cp_async16(dst, a.Abase + s_aoff[j] + (m - j * RP) * K + q * 4);
+    else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// flat distinct-ID index f of the tile -> node_local j (s_pref is ascending)
 __device__ __forceinline__ int find_node(const int* s_pref, int nn, int f) {
   int lo = 0, hi = nn - 1;
   while (lo < hi) {
@@ -149,79 +173,116 @@ __device__ __forceinline__ int find_node(const int* s_pref, int nn, int f) {
   return lo;
 }
 
+// Stage the last-core slices of IDs [c0, c0+nc) of the tile, transposed:
+// Gs[(ci*NL + jl)*(K+1) + r] = G_{d-1}[r, i_d(u), jl]; also s_u/s_j.
+template <int K>
+__device__ __forceinline__ void stage_ids(const FusedArgs& a, int c0, int nc, int nn, const int* s_node,
+                                          const int* s_pref, int* s_u, int* s_j, float* Gs, bool want_g) {
+  for (int ci = threadIdx.x; ci < nc; ci += FB_THREADS) {
+    const int j = find_node(s_pref, nn, c0 + ci);
+    s_j[ci] = j;
+    s_u[ci] = a.cstartF[s_node[j]] + (c0 + ci - s_pref[j]);
+  }
+  __syncthreads();
+  if (!want_g) return;
+  const int NL = a.NL;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  for (int i = threadIdx.x; i < nc * K * NL; i += FB_THREADS) {
+    const int ci = i / (K * NL), e = i - ci * (K * NL);
+    const int r = e / NL, jl = e - r * NL;
+    Gs[(ci * NL + jl) * (K + 1) + r] = __ldg(Gl + (int64_t)a.digitL[s_u[ci]] * sliceL + e);
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 template <int K, int BN>
 __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_fwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, SA = BM + 4, TN = BN / 32;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32;
   extern __shared__ __align__(16) float smem[];
-  float* Bs = smem;             // [K][SB]
-  float* As = Bs + K * SB;      // [K][SA]  (A transposed)
-  float* Cs = As + K * SA;      // [BM][SB]
-  int* s_node = (int*)(Cs + BM * SB);
-  int* s_pref = s_node + BM + 1;
+  float* Bs = smem;                      // [K][SB]
+  float* As0 = Bs + K * SB;              // [2][BM][K]
+  float* Cs = As0 + 2 * BM * K;          // [BM][BN]
+  float* Gs = Cs + BM * BN;              // [CH][NL][K+1]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * a.NL * (K + 1) + ((a.CH * a.NL * (K + 1)) & 1));
+  int* s_node = reinterpret_cast<int*>(s_aoff + 2 * BM);   // [2][BM]
+  int* s_pref = s_node + 2 * BM;                           // [2][BM+1]
+  int* s_u = s_pref + 2 * (BM + 1);                        // [CH]
+  int* s_j = s_u + a.CH;                                   // [CH]
 
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - (blockIdx.x / a.ncb) * a.ncb;
+  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
   if (g0 == g1) return;
-  load_slice_block<K, BN>(a, g, cb, Bs);
-  asm volatile("cp.async.commit_group;\n" ::);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RP = a.RP, npt = BM / RP;
+  const int RP = a.RP, npt = BM / RP, NL = a.NL, BNj = a.BNj, nF = a.nF;
   const int m0 = warp * 8;
-  const int64_t emb = a.c.emb_dim;
-  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
-  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const int64_t emb = a.c.emb_dim, npad = a.c.npad;
 
-  for (int t0 = g0; t0 < g1; t0 += npt) {
-    const int nn = min(npt, g1 - t0);
-    const int total_ids = tile_nodes(a, t0, nn, s_node, s_pref);
-    // A tile, transposed: As[k][j*RP + r]
-    for (int i = threadIdx.x; i < BM * K; i += FB_THREADS) {
-      const int m = i / K, k = i - m * K;
-      const int j = m / RP;
-      float v = 0.f;
-      if (j < nn) v = fused_A(a, s_node[j])[(m - j * RP) * K + k];
-      As[k * SA + m] = v;
+  load_slice_block<K, BN, SB>(a, g, cb, Bs);
+  int nn = min(npt, g1 - g0);
+  tile_nodes(a, g0, nn, s_node, s_pref, s_aoff);
+  load_A_tile<K>(a, nn, s_aoff, As0);
+  cp_async_commit();
+
+  int buf = 0;
+  for (int t0 = g0; t0 < g1; t0 += npt, buf ^= 1) {
+    const int t1 = t0 + npt;
+    const int nn1 = min(npt, g1 - t1);
+    int* nd = s_node + buf * BM;
+    int* pf = s_pref + buf * (BM + 1);
+    if (t1 < g1) {  // prefetch the next tile's nodes and A
+      tile_nodes(a, t1, nn1, s_node + (buf ^ 1) * BM, s_pref + (buf ^ 1) * (BM + 1), s_aoff + (buf ^ 1) * BM);
+      load_A_tile<K>(a, nn1, s_aoff + (buf ^ 1) * BM, As0 + (buf ^ 1) * BM * K);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    cp_async_wait_all();
     __syncthreads();
+    const float* As = As0 + buf * BM * K;
 
     float acc[8][TN];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < K; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(As + k * SA + m0);
-      const float4 a1 = *reinterpret_cast<const float4*>(As + k * SA + m0 + 4);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      float bv[TN];
-      if constexpr (TN >= 4) {
+#pragma unroll 2
+    for (int kk = 0; kk < K; kk += 4) {
+      float4 av[8];
 #pragma unroll
-        for (int q = 0; q < TN / 4; ++q) {
-          const float4 b = *reinterpret_cast<const float4*>(Bs + k * SB + q * 128 + lane * 4);
-          bv[q * 4 + 0] = b.x; bv[q * 4 + 1] = b.y; bv[q * 4 + 2] = b.z; bv[q * 4 + 3] = b.w;
+      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (m0 + i) * K + kk);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float bv[TN];
+        if constexpr (TN >= 4) {
+#pragma unroll
+          for (int q = 0; q < TN / 4; ++q) {
+            const float4 b = *reinterpret_cast<const float4*>(Bs + (kk + t) * SB + q * 128 + lane * 4);
+            bv[q * 4 + 0] = b.x; bv[q * 4 + 1] = b.y; bv[q * 4 + 2] = b.z; bv[q * 4 + 3] = b.w;
+          }
+        } else {
+          const float2 b = *reinterpret_cast<const float2*>(Bs + (kk + t) * SB + lane * 2);
+          bv[0] = b.x; bv[1] = b.y;
         }
-      } else {
-        const float2 b = *reinterpret_cast<const float2*>(Bs + k * SB + lane * 2);
-        bv[0] = b.x; bv[1] = b.y;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
+        }
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
+    const int cur_nn = min(npt, g1 - t0);
     // C -> shared (epilogue) and -> saved P_F (backward)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int m = m0 + i;
       const int j = m / RP;
-      float* crow = Cs + m * SB;
-      float* prow = (a.Psave && j < nn)
-                        ? a.Psave + ((int64_t)s_node[j] * RP + (m - j * RP)) * a.NC + cb * BN : nullptr;
+      float* crow = Cs + m * BN;
+      float* prow = (a.Psave && j < cur_nn)
+                        ? a.Psave + ((int64_t)nd[j] * RP + (m - j * RP)) * a.NC + cb * BN : nullptr;
       if constexpr (TN >= 4) {
 #pragma unroll
         for (int q = 0; q < TN / 4; ++q) {
@@ -238,53 +299,64 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_fwd(FusedArgs a) {
     __syncthreads();
     // last level straight from the C tile
     if (a.out) {
-      const int OUT = a.OUT, R2 = a.R2, NL = a.NL, BNj = a.BNj;
-      for (int f = threadIdx.x; f < total_ids * OUT; f += FB_THREADS) {
-        const int idf = f / OUT, o = f - idf * OUT;
-        const int j = find_node(s_pref, nn, idf);
-        const int u = a.cstartF[s_node[j]] + (idf - s_pref[j]);
-        const int ar = o / (BNj * NL), rem = o - ar * (BNj * NL);
-        const int jf = rem / NL, jl = rem - jf * NL;
-        const float* crow = Cs + (j * RP + ar) * SB + jf * R2;
-        const float* gl = Gl + (int64_t)a.digitL[u] * sliceL + jl;
-        float v = 0.f;
-        for (int r = 0; r < R2; ++r) v = fmaf(crow[r], __ldg(gl + r * NL), v);
-        const int64_t col = ((int64_t)(ar * a.nF + cb * BNj + jf)) * NL + jl;
-        if (col < emb)
-          for (int s = a.seg[u], se = a.seg[u + 1]; s < se; ++s) a.out[(int64_t)a.spos[s] * emb + col] = v;
+      const int total_ids = pf[cur_nn];
+      for (int c0 = 0; c0 < total_ids; c0 += a.CH) {
+        const int nc = min(a.CH, total_ids - c0);
+        stage_ids<K>(a, c0, nc, cur_nn, nd, pf, s_u, s_j, Gs, true);
+        const int per_row = nc * NL;
+        for (int f = threadIdx.x; f < RP * BNj * per_row; f += FB_THREADS) {
+          const int rc = f / per_row, e = f - rc * per_row;  // rc = (ar, jf); e = (ci, jl)
+          const int ci = e / NL, jl = e - ci * NL;
+          const int ar = rc / BNj, jf = rc - ar * BNj;
+          const int u = s_u[ci];
+          const float* crow = Cs + (s_j[ci] * RP + ar) * BN + jf * K;
+          const float* gcol = Gs + (ci * NL + jl) * (K + 1);
+          float v = 0.f;
+#pragma unroll 16
+          for (int r = 0; r < K; ++r) v = fmaf(crow[r], gcol[r], v);
+          const int64_t col = ((int64_t)(ar * nF + cb * BNj + jf)) * NL + jl;
+          const int s0 = a.seg[u], s1 = a.seg[u + 1];
+          if (s1 - s0 > HEAVY_POS) {
+            a.Yu[(int64_t)u * npad + col] = v;
+          } else if (col < emb) {
+            for (int s = s0; s < s1; ++s) a.out[(int64_t)a.spos[s] * emb + col] = v;
+          }
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 template <int K, int BN>
 __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, SA = K + 4, TN = BN / 32, TK = K / 8;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;               // [K][SB]
-  float* As = Bs + K * SB;        // [BM][SA]  (A row-major)
-  float* Cs = As + BM * SA;       // [BM][SB]  C, then dC
-  float* Ys = Cs + BM * SB;       // [FB_CH][OUT] staged dY
-  int* s_node = (int*)(Ys + FB_CH * 256);
-  int* s_pref = s_node + BM + 1;
+  float* As = Bs + K * SB;        // [BM][K]
+  float* Cs = As + BM * K;        // [BM][BN]  saved C (for W)
+  float* Ds = Cs + BM * BN;       // [BM][BN]  dC
+  float* Ys = Ds + BM * BN;       // [CH][OUT]
+  float* Gs = Ys + a.CH * a.OUT;  // [CH][NL][K+1]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * a.NL * (K + 1) + ((a.CH * a.NL * (K + 1) + a.CH * a.OUT) & 1));
+  int* s_node = reinterpret_cast<int*>(s_aoff + BM);
+  int* s_pref = s_node + BM;
+  int* s_u = s_pref + BM + 1;
+  int* s_j = s_u + a.CH;
 
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - (blockIdx.x / a.ncb) * a.ncb;
+  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
   if (g0 == g1) return;
-  load_slice_block<K, BN>(a, g, cb, Bs);
-  asm volatile("cp.async.commit_group;\n" ::);
+  load_slice_block<K, BN, SB>(a, g, cb, Bs);
+  cp_async_commit();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RP = a.RP, npt = BM / RP;
-  const int OUT = a.OUT, R2 = a.R2, NL = a.NL, BNj = a.BNj;
-  const int64_t emb = a.c.emb_dim;
-  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
-  const int64_t sliceL = a.c.slice[a.c.d - 1];
-  const int WE = R2 * NL;
+  const int RP = a.RP, npt = BM / RP, NL = a.NL, BNj = a.BNj, nF = a.nF, OUT = a.OUT, CH = a.CH;
+  const int64_t npad = a.c.npad;
+  const int WE = K * NL;
 
   float gacc[TK][TN];
 #pragma unroll
@@ -294,114 +366,74 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
 
   for (int t0 = g0; t0 < g1; t0 += npt) {
     const int nn = min(npt, g1 - t0);
-    const int total_ids = tile_nodes(a, t0, nn, s_node, s_pref);
-    // A tile row-major; saved C tile
-    for (int i = threadIdx.x; i < BM * K; i += FB_THREADS) {
-      const int m = i / K, k = i - m * K;
-      const int j = m / RP;
-      As[m * SA + k] = j < nn ? fused_A(a, s_node[j])[(m - j * RP) * K + k] : 0.f;
-    }
-    for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
+    const int total_ids = tile_nodes(a, t0, nn, s_node, s_pref, s_aoff);
+    load_A_tile<K>(a, nn, s_aoff, As);
+    cp_async_commit();
+    for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {  // saved C tile (for W, used last)
       const int m = i / (BN / 4), q = i - m * (BN / 4);
       const int j = m / RP;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < nn)
-        v = *reinterpret_cast<const float4*>(a.Psave + ((int64_t)s_node[j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
-      *reinterpret_cast<float4*>(Cs + m * SB + q * 4) = v;
+      float* dst = Cs + m * BN + q * 4;
+      if (j < nn) cp_async16(dst, a.Psave + ((int64_t)s_node[j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
+      else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    cp_async_commit();
+    for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS)
+      reinterpret_cast<float4*>(Ds)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    // pass 1: W_u = C^T dY_u for every distinct ID of the tile
-    for (int c0 = 0; c0 < total_ids; c0 += FB_CH) {
-      const int nc = min(FB_CH, total_ids - c0);
-      for (int f = threadIdx.x; f < nc * OUT; f += FB_THREADS) {
-        const int ci = f / OUT, o = f - ci * OUT;
-        const int j = find_node(s_pref, nn, c0 + ci);
-        const int u = a.cstartF[s_node[j]] + (c0 + ci - s_pref[j]);
-        const int ar = o / (BNj * NL), rem = o - ar * (BNj * NL);
-        const int jf = rem / NL, jl = rem - jf * NL;
-        const int64_t col = ((int64_t)(ar * a.nF + cb * BNj + jf)) * NL + jl;
-        float v = 0.f;
-        if (col < emb)
-          for (int s = a.seg[u], se = a.seg[u + 1]; s < se; ++s) v += a.up[(int64_t)a.spos[s] * emb + col];
-        Ys[ci * OUT + o] = v;
+    // dC = sum over each node's IDs of dY_u G_l(u)^T
+    for (int c0 = 0; c0 < total_ids; c0 += CH) {
+      const int nc = min(CH, total_ids - c0);
+      stage_ids<K>(a, c0, nc, nn, s_node, s_pref, s_u, s_j, Gs, true);
+      for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
+        const int ci = i / (OUT / 4), q = i - ci * (OUT / 4);
+        const int ar = (q * 4) / (BNj * NL), w = q * 4 - ar * (BNj * NL);
+        *reinterpret_cast<float4*>(Ys + ci * OUT + q * 4) = *reinterpret_cast<const float4*>(
+            a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNj) * NL + w);
       }
       __syncthreads();
-      for (int f = threadIdx.x; f < nc * WE; f += FB_THREADS) {
-        const int ci = f / WE, e = f - ci * WE;
-        const int r = e / NL, jl = e - r * NL;
-        const int j = find_node(s_pref, nn, c0 + ci);
-        const int u = a.cstartF[s_node[j]] + (c0 + ci - s_pref[j]);
-        float v = 0.f;
-        for (int ar = 0; ar < RP; ++ar)
-          for (int jf = 0; jf < BNj; ++jf)
-            v = fmaf(Cs[(j * RP + ar) * SB + jf * R2 + r], Ys[ci * OUT + (ar * BNj + jf) * NL + jl], v);
-        a.W[((int64_t)u * a.ncb + cb) * WE + e] = v;
-      }
-      __syncthreads();
-    }
-    // pass 2: dC (overwrites C) = sum over the node's IDs of dY_u G_l(u)^T
-    for (int i = threadIdx.x; i < BM * BN; i += FB_THREADS) Cs[(i / BN) * SB + (i % BN)] = 0.f;
-    __syncthreads();
-    for (int c0 = 0; c0 < total_ids; c0 += FB_CH) {
-      const int nc = min(FB_CH, total_ids - c0);
-      for (int f = threadIdx.x; f < nc * OUT; f += FB_THREADS) {
-        const int ci = f / OUT, o = f - ci * OUT;
-        const int j = find_node(s_pref, nn, c0 + ci);
-        const int u = a.cstartF[s_node[j]] + (c0 + ci - s_pref[j]);
-        const int ar = o / (BNj * NL), rem = o - ar * (BNj * NL);
-        const int jf = rem / NL, jl = rem - jf * NL;
-        const int64_t col = ((int64_t)(ar * a.nF + cb * BNj + jf)) * NL + jl;
-        float v = 0.f;
-        if (col < emb)
-          for (int s = a.seg[u], se = a.seg[u + 1]; s < se; ++s) v += a.up[(int64_t)a.spos[s] * emb + col];
-        Ys[ci * OUT + o] = v;
-      }
-      __syncthreads();
-      const int jlo = find_node(s_pref, nn, c0), jhi = find_node(s_pref, nn, c0 + nc - 1);
+      const int jlo = s_j[0], jhi = s_j[nc - 1];
       const int rows = (jhi - jlo + 1) * RP;
       for (int i = threadIdx.x; i < rows * BN; i += FB_THREADS) {
         const int mm = i / BN, n = i - mm * BN;
         const int m = jlo * RP + mm;
         const int j = m / RP, ar = m - j * RP;
-        const int jf = n / R2, r = n - jf * R2;
-        const int u0 = max(s_pref[j], c0), u1 = min(s_pref[j + 1], c0 + nc);
-        float v = Cs[m * SB + n];
-        for (int f = u0; f < u1; ++f) {
-          const int u = a.cstartF[s_node[j]] + (f - s_pref[j]);
-          const float* gl = Gl + (int64_t)a.digitL[u] * sliceL + r * NL;
-          const float* y = Ys + (f - c0) * OUT + (ar * BNj + jf) * NL;
-          for (int jl = 0; jl < NL; ++jl) v = fmaf(y[jl], __ldg(gl + jl), v);
+        const int jf = n / K, r = n - jf * K;
+        const int f0 = max(s_pref[j], c0) - c0, f1 = min(s_pref[j + 1], c0 + nc) - c0;
+        float v = Ds[m * BN + n];
+        for (int ci = f0; ci < f1; ++ci) {
+          const float* y = Ys + ci * OUT + (ar * BNj + jf) * NL;
+          const float* gc = Gs + ci * NL * (K + 1) + r;
+          for (int jl = 0; jl < NL; ++jl) v = fmaf(y[jl], gc[jl * (K + 1)], v);
         }
-        Cs[m * SB + n] = v;
+        Ds[m * BN + n] = v;
       }
       __syncthreads();
     }
-    // dG_F block += A^T dC  (k rows warp*TK.., columns as in the forward)
+    cp_async_wait<1>();  // slice block + A tile landed (C may still be in flight)
+    __syncthreads();
+    // dG_F block += A^T dC
 #pragma unroll 2
     for (int m = 0; m < BM; ++m) {
       float av[TK];
+      if constexpr (TK >= 4) {
 #pragma unroll
-      for (int q = 0; q < TK; q += 4) {
-        if constexpr (TK >= 4) {
-          const float4 t = *reinterpret_cast<const float4*>(As + m * SA + warp * TK + q);
+        for (int q = 0; q < TK; q += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(As + m * K + warp * TK + q);
           av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
         }
-      }
-      if constexpr (TK < 4) {
+      } else {
 #pragma unroll
-        for (int q = 0; q < TK; ++q) av[q] = As[m * SA + warp * TK + q];
+        for (int q = 0; q < TK; ++q) av[q] = As[m * K + warp * TK + q];
       }
       float bv[TN];
       if constexpr (TN >= 4) {
 #pragma unroll
         for (int q = 0; q < TN / 4; ++q) {
-          const float4 b = *reinterpret_cast<const float4*>(Cs + m * SB + q * 128 + lane * 4);
+          const float4 b = *reinterpret_cast<const float4*>(Ds + m * BN + q * 128 + lane * 4);
           bv[q * 4 + 0] = b.x; bv[q * 4 + 1] = b.y; bv[q * 4 + 2] = b.z; bv[q * 4 + 3] = b.w;
         }
       } else {
-        const float2 b = *reinterpret_cast<const float2*>(Cs + m * SB + lane * 2);
+        const float2 b = *reinterpret_cast<const float2*>(Ds + m * BN + lane * 2);
         bv[0] = b.x; bv[1] = b.y;
       }
 #pragma unroll
@@ -421,7 +453,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       for (int n = 0; n < BN; n += 4) {
         float4 cv[TMA], bv[TKA];
 #pragma unroll
-        for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Cs + (mg + MG * i) * SB + n);
+        for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * BN + n);
 #pragma unroll
         for (int j = 0; j < TKA; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + KG * j) * SB + n);
 #pragma unroll
@@ -444,7 +476,31 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
         for (int jj = 0; jj < TKA; ++jj) dst[kg + KG * jj] = dacc[i][jj];
       }
     }
+    cp_async_wait<0>();  // saved C tile
     __syncthreads();
+    // W_u = C_u^T dY_u  (per distinct ID, this column block's share)
+    for (int c0 = 0; c0 < total_ids; c0 += CH) {
+      const int nc = min(CH, total_ids - c0);
+      stage_ids<K>(a, c0, nc, nn, s_node, s_pref, s_u, s_j, Gs, false);
+      for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
+        const int ci = i / (OUT / 4), q = i - ci * (OUT / 4);
+        const int ar = (q * 4) / (BNj * NL), w = q * 4 - ar * (BNj * NL);
+        *reinterpret_cast<float4*>(Ys + ci * OUT + q * 4) = *reinterpret_cast<const float4*>(
+            a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNj) * NL + w);
+      }
+      __syncthreads();
+      for (int f = threadIdx.x; f < nc * WE; f += FB_THREADS) {
+        const int ci = f / WE, e = f - ci * WE;
+        const int r = e / NL, jl = e - r * NL;
+        const int j = s_j[ci];
+        float v = 0.f;
+        for (int ar = 0; ar < RP; ++ar)
+          for (int jf = 0; jf < BNj; ++jf)
+            v = fmaf(Cs[(j * RP + ar) * BN + jf * K + r], Ys[ci * OUT + (ar * BNj + jf) * NL + jl], v);
+        a.W[((int64_t)s_u[ci] * a.ncb + cb) * WE + e] = v;
+      }
+      __syncthreads();
+    }
   }
   // the group's dG_F column block (one writer per slice block: no atomics)
   float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
@@ -470,11 +526,23 @@ __global__ void k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __rest
   const int v = blockIdx.x;
   const int g0 = goffL[v], g1 = goffL[v + 1];
   if (g0 == g1) return;
+  const int npair = (g1 - g0) * ncb;
   for (int e = threadIdx.x; e < WE; e += blockDim.x) {
     float acc = 0.f;
-    for (int gi = g0; gi < g1; ++gi) {
-      const float* w = W + (int64_t)orderL[gi] * ncb * WE + e;
-      for (int cbi = 0; cbi < ncb; ++cbi) acc += w[cbi * WE];
+    int q = 0;
+    for (; q + 8 <= npair; q += 8) {  // (member, column block) pairs in fixed order
+      float x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int gi = g0 + (q + i) / ncb, cbi = (q + i) - ((q + i) / ncb) * ncb;
+        x[i] = W[((int64_t)orderL[gi] * ncb + cbi) * WE + e];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += x[i];
+    }
+    for (; q < npair; ++q) {
+      const int gi = g0 + q / ncb, cbi = q - (q / ncb) * ncb;
+      acc += W[((int64_t)orderL[gi] * ncb + cbi) * WE + e];
     }
     grads[c.core_off[c.d - 1] + (int64_t)v * c.slice[c.d - 1] + e] = acc;
   }
@@ -491,11 +559,17 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int p = (int)(t / per);
     const int e = (int)(t - (int64_t)p * per);
+    const int n0 = cstart_pm1[p] * ncb, n1 = cstart_pm1[p + 1] * ncb;  // (child, cb) pairs are contiguous
     float acc = 0.f;
-    for (int ch = cstart_pm1[p], ce = cstart_pm1[p + 1]; ch < ce; ++ch) {
-      const float* src = dPc + (int64_t)ch * ncb * per + e;
-      for (int cbi = 0; cbi < ncb; ++cbi) acc += src[cbi * per];
+    int q = n0;
+    for (; q + 8 <= n1; q += 8) {
+      float x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = dPc[(int64_t)(q + i) * per + e];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += x[i];
     }
+    for (; q < n1; ++q) acc += dPc[(int64_t)q * per + e];
     if (F == 1)
       dst[c.core_off[0] + (int64_t)digit0[p] * c.slice[0] + e] = acc;
     else
@@ -509,16 +583,18 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   if (c.d < 3) return false;
   const int F = c.d - 2;
   const int64_t K = c.R[F], NC = c.cols[F], R2 = c.R[F + 1], NL = c.n[c.d - 1], RP = c.rows[F];
+  if (R2 != K) return false;
   int BN = 0;
-  if (K == 16 && NC % 64 == 0 && 64 % R2 == 0) BN = 64;
-  if (K == 32 && NC % 128 == 0 && 128 % R2 == 0) BN = 128;
-  if (K == 64 && NC % 256 == 0 && 256 % R2 == 0) BN = 256;
-  if (K == 64 && !BN && NC % 128 == 0 && 128 % R2 == 0) BN = 128;
-  if (K == 128 && NC % 128 == 0 && 128 % R2 == 0) BN = 128;
+  if (K == 16 && NC % 64 == 0) BN = 64;
+  if (K == 32 && NC % 128 == 0) BN = 128;
+  if (K == 64 && NC % 256 == 0) BN = 256;
+  if (K == 64 && !BN && NC % 128 == 0) BN = 128;
+  if (K == 128 && NC % 128 == 0) BN = 128;
   if (!BN) return false;
   if (RP > FB_BM || FB_BM % RP) return false;
-  const int64_t OUT = RP * (BN / R2) * NL;
-  if (OUT > 256 || R2 * NL > 4096) return false;
+  const int64_t OUT = RP * (BN / K) * NL;
+  if (OUT % 4 || NL > 16) return false;
+  if (c.emb_dim % 4 || c.npad % 4 || c.npad > 512) return false;
   for (int k = 0; k < c.d; ++k)
     if (c.core_off[k] % 4 || c.slice[k] % 4) return false;
   s->ok = 1;
@@ -528,16 +604,21 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->NC = (int)NC;
   s->ncb = (int)(NC / BN);
   s->RP = (int)RP;
-  s->R2 = (int)R2;
   s->NL = (int)NL;
   s->nF = (int)c.n[F];
-  s->BNj = (int)(BN / R2);
+  s->BNj = (int)(BN / K);
   s->OUT = (int)OUT;
-  const int SB = BN + 4;
-  s->smem_fwd = sizeof(float) * ((size_t)K * SB + (size_t)K * (FB_BM + 4) + (size_t)FB_BM * SB) +
-                sizeof(int) * (2 * FB_BM + 4);
-  s->smem_bwd = sizeof(float) * ((size_t)K * SB + (size_t)FB_BM * (K + 4) + (size_t)FB_BM * SB + FB_CH * 256) +
-                sizeof(int) * (2 * FB_BM + 4);
+  const size_t SB = BN + 4;
+  const size_t ints = sizeof(int64_t) * 2 * FB_BM + sizeof(int) * (6 * FB_BM + 8) + 16;
+  const size_t base_f = sizeof(float) * (K * SB + 2 * FB_BM * K + FB_BM * BN) + ints;
+  const size_t base_b = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
+  const size_t per_f = sizeof(float) * NL * (K + 1) + 2 * sizeof(int);
+  const size_t per_b = sizeof(float) * (NL * (K + 1) + OUT) + 2 * sizeof(int);
+  if (base_f + 4 * per_f > (size_t)FB_SMEM_MAX || base_b + 4 * per_b > (size_t)FB_SMEM_MAX) return false;
+  s->CHF = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_f) / per_f);
+  s->CHB = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_b) / per_b);
+  s->smem_fwd = base_f + s->CHF * per_f;
+  s->smem_bwd = base_b + s->CHB * per_b;
   return true;
 }
 

@@ -1,0 +1,114 @@
+// kernels_rows.cuh -- balanced row movement between batch positions and
+// distinct IDs (HBM bound, fully coalesced 16-byte accesses).
+//
+// * k_dy_chunks / k_dy_spans: dY[u] = sum of the upstream rows at the ID's
+//   batch positions, in ascending position order (the stable sort's slot
+//   order) -- the duplicate additivity of backward_lookup
+//   (autodiff.cpp:76-116).  The sorted slots are cut into fixed
+//   32-slot chunks, one warp each, so a Zipf-hot ID with 10^4 positions is
+//   spread over many warps instead of serialising one; segments crossing
+//   chunk boundaries are finished by k_dy_spans in chunk order.  The
+//   summation order depends only on the batch, never on scheduling.
+// * k_scatter_heavy: copies the rows of IDs with many positions (deferred by
+//   the forward epilogue) to every position, one thread per 16 bytes.
+#pragma once
+#include "common.cuh"
+
+namespace tt {
+
+constexpr int DY_CHUNK = 32;
+constexpr int HEAVY_POS = 8;  // IDs with more positions are scattered by k_scatter_heavy
+
+// uid1[s] = (distinct index of sorted slot s) + 1  (the inclusive unique scan)
+__global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up, int B, int64_t emb, int64_t npad,
+                                                   const int* __restrict__ uid1, const int* __restrict__ spos,
+                                                   const int* __restrict__ seg, float* __restrict__ dY,
+                                                   float* __restrict__ part, const DevStatus* st) {
+  if (tt_failed(st)) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int lo = warp * DY_CHUNK;
+  if (lo >= B) return;
+  const int hi = min(lo + DY_CHUNK, B);
+  const int my_s = lo + lane;
+  const int my_u = my_s < hi ? uid1[my_s] - 1 : -1;
+  const int my_p = my_s < hi ? spos[my_s] : 0;
+  const int nv = (int)((npad + 127) / 128);  // float4 column groups per lane (<= 4)
+  float4 acc[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int cur = __shfl_sync(0xffffffffu, my_u, 0);
+  auto flush = [&](int u) {
+    const int s0 = seg[u], s1 = seg[u + 1];
+    float* dst;
+    if (s0 >= lo && s1 <= hi) dst = dY + (int64_t)u * npad;
+    else dst = part + ((int64_t)warp * 2 + (s0 < lo ? 0 : 1)) * npad;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t c = (int64_t)v * 128 + lane * 4;
+      if (v < nv && c < npad) *reinterpret_cast<float4*>(dst + c) = acc[v];
+      acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  for (int i = 0; i < hi - lo; ++i) {
+    const int u = __shfl_sync(0xffffffffu, my_u, i);
+    const int p = __shfl_sync(0xffffffffu, my_p, i);
+    if (u != cur) {
+      flush(cur);
+      cur = u;
+    }
+    const float* row = up + (int64_t)p * emb;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t c = (int64_t)v * 128 + lane * 4;
+      if (v < nv && c < emb) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(row + c));
+        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+      }
+    }
+  }
+  flush(cur);
+}
+
+// finish IDs whose slots span several chunks: first chunk's tail partial,
+// then every following chunk's head partial, in chunk order.
+__global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts, int d, int64_t npad,
+                                                  const int* __restrict__ seg, const float* __restrict__ part,
+                                                  float* __restrict__ dY, const DevStatus* st) {
+  if (tt_failed(st)) return;
+  const int U = ld_count(&counts[d - 1]);
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (u >= U) return;
+  const int s0 = seg[u], s1 = seg[u + 1];
+  const int c0 = s0 / DY_CHUNK, c1 = (s1 - 1) / DY_CHUNK;
+  if (c0 == c1) return;
+  for (int64_t c = lane * 4; c < npad; c += 128) {
+    float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
+    for (int ch = c0 + 1; ch <= c1; ++ch) {
+      const float4 x = *reinterpret_cast<const float4*>(part + ((int64_t)ch * 2) * npad + c);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    *reinterpret_cast<float4*>(dY + (int64_t)u * npad + c) = acc;
+  }
+}
+
+// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS positions)
+__global__ void __launch_bounds__(256) k_scatter_heavy(int B, int64_t emb, int64_t npad, const int* __restrict__ uid1,
+                                                       const int* __restrict__ spos, const int* __restrict__ seg,
+                                                       const float* __restrict__ Yu, float* __restrict__ out,
+                                                       const DevStatus* st) {
+  if (tt_failed(st)) return;
+  const int64_t per = emb / 4;
+  const int64_t total = (int64_t)B * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / per);
+    const int64_t c = (t - (int64_t)s * per) * 4;
+    const int u = uid1[s] - 1;
+    if (seg[u + 1] - seg[u] <= HEAVY_POS) continue;
+    *reinterpret_cast<float4*>(out + (int64_t)spos[s] * emb + c) =
+        *reinterpret_cast<const float4*>(Yu + (int64_t)u * npad + c);
+  }
+}
+
+}  // namespace tt
