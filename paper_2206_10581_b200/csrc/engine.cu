@@ -355,24 +355,27 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
   return a;
 }
 
-#define FUSED_DISPATCH(KER, K_, BN_, GRID, SMEM, S, ARGS)                                   \
-  do {                                                                                     \
-    auto kfn = KER<K_, BN_>;                                                               \
-    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM))); \
-    kfn<<<(GRID), FB_THREADS, (SMEM), (S)>>>(ARGS);                                        \
-    ++h->launches;                                                                         \
+#define FUSED_LAUNCH(KER, SMEM, GRID, S, ARGS)                                               \
+  do {                                                                                       \
+    CU(cudaFuncSetAttribute(KER, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM)));   \
+    KER<<<(GRID), FB_THREADS, (SMEM), (S)>>>(ARGS);                                          \
+    ++h->launches;                                                                           \
   } while (0)
 
-#define FUSED_SWITCH(KER, GRID, SMEM, S, ARGS)                                              \
-  do {                                                                                     \
-    const int K_ = h->fs.K, BN_ = h->fs.BN;                                                \
-    if (K_ == 16 && BN_ == 64) FUSED_DISPATCH(KER, 16, 64, GRID, SMEM, S, ARGS);           \
-    else if (K_ == 32 && BN_ == 128) FUSED_DISPATCH(KER, 32, 128, GRID, SMEM, S, ARGS);    \
-    else if (K_ == 64 && BN_ == 256) FUSED_DISPATCH(KER, 64, 256, GRID, SMEM, S, ARGS);    \
-    else if (K_ == 64 && BN_ == 128) FUSED_DISPATCH(KER, 64, 128, GRID, SMEM, S, ARGS);    \
-    else if (K_ == 128 && BN_ == 128) FUSED_DISPATCH(KER, 128, 128, GRID, SMEM, S, ARGS);  \
-    else return fail(TT_ERR_ARG, "fused path: unsupported tile shape");                    \
-  } while (0)
+#define FUSED_CASE(k_, bn_, rp_, nl_)                                                          \
+  else if (f.K == k_ && f.BN == bn_ && f.RP == rp_ && f.NL == nl_) {                          \
+    if (fwd) FUSED_LAUNCH((k_fused_fwd<k_, bn_, rp_, nl_>), f.smem_fwd, grid, s, a);          \
+    else FUSED_LAUNCH((k_fused_bwd<k_, bn_, rp_, nl_>), f.smem_bwd, grid, s, a);              \
+  }
+
+int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a, int grid, cudaStream_t s) {
+  const FusedShape& f = h->fs;
+  if (false) {
+  }
+  TT_FUSED_SHAPES(FUSED_CASE)
+  else return fail(TT_ERR_ARG, "fused path: shape not compiled");
+  return TT_OK;
+}
 
 int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   const DevCfg& c = h->dc;
@@ -391,7 +394,8 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   }
   FusedArgs a = fused_args(h, d_out);
   a.CH = f.CHF;
-  FUSED_SWITCH(k_fused_fwd, (int)(c.m[f.F] * f.ncb), f.smem_fwd, s, a);
+  rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncb), s);
+  if (rc) return rc;
   if (d_out)
     LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);
@@ -410,7 +414,8 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
          h->st);
   FusedArgs a = fused_args(h, nullptr);
   a.CH = f.CHB;
-  FUSED_SWITCH(k_fused_bwd, (int)(c.m[f.F] * f.ncb), f.smem_bwd, s, a);
+  int rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
+  if (rc) return rc;
   const int WE = f.K * f.NL;
   LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], std::min(1024, (WE + 31) / 32 * 32), 0, s, c, f.ncb, WE,
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);

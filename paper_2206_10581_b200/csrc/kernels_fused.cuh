@@ -115,57 +115,64 @@ __device__ __forceinline__ void load_slice_block(const FusedArgs& a, int g, int 
   }
 }
 
-// Node list of the tile starting at group slot t0: node ids, prefix of their
-// distinct-ID counts, and each node's A-block offset.  Ends with a barrier.
-__device__ __forceinline__ int tile_nodes(const FusedArgs& a, int t0, int nn, int* s_node, int* s_pref,
-                                          int64_t* s_aoff) {
-  if (threadIdx.x < 32) {
-    int run = 0;
-    for (int base = 0; base < nn; base += 32) {
-      const int j = base + threadIdx.x;
-      int node = 0, cnt = 0;
-      if (j < nn) {
-        node = a.orderF[t0 + j];
-        cnt = a.cstartF[node + 1] - a.cstartF[node];
-        const int p = a.parentF[node];
-        s_aoff[j] = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0]
-                             : (int64_t)p * a.RP * a.c.R[a.F];
-      }
-      int x = cnt;
+constexpr int FB_NB = 256;  // nodes whose metadata is staged per batch
+
+// Metadata for nodes [nb0, nb0 + nbn) of the group (one thread per node):
+// node id, first distinct ID, A-block offset, and the exclusive prefix of the
+// nodes' distinct-ID counts (s_pref[nbn] = total).  Ends with a barrier.
+__device__ __forceinline__ void prep_nodes(const FusedArgs& a, int nb0, int nbn, int* s_node, int* s_cs0,
+                                           int* s_pref, int64_t* s_aoff, int* s_wsum) {
+  const int t = threadIdx.x;
+  int cnt = 0;
+  if (t < nbn) {
+    const int node = a.orderF[nb0 + t];
+    const int c0 = a.cstartF[node];
+    cnt = a.cstartF[node + 1] - c0;
+    const int p = a.parentF[node];
+    s_node[t] = node;
+    s_cs0[t] = c0;
+    s_aoff[t] = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0] : (int64_t)p * a.RP * a.c.R[a.F];
+  }
+  int x = cnt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, o);
-        if ((int)lane_id() >= o) x += y;
-      }
-      if (j < nn) {
-        s_node[j] = node;
-        s_pref[j] = run + x - cnt;
-      }
-      run += __shfl_sync(0xffffffffu, x, 31);
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((int)lane_id() >= o) x += y;
+  }
+  if (lane_id() == 31) s_wsum[t >> 5] = x;
+  __syncthreads();
+  if (t < 32) {
+    int w = t < FB_THREADS / 32 ? s_wsum[t] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if ((int)lane_id() >= o) w += y;
     }
-    if (threadIdx.x == 0) s_pref[nn] = run;
+    if (t < FB_THREADS / 32) s_wsum[t] = w;  // inclusive warp totals
   }
   __syncthreads();
-  return s_pref[nn];
+  const int excl = x - cnt + ((t >> 5) ? s_wsum[(t >> 5) - 1] : 0);
+  if (t < nbn) s_pref[t] = excl;
+  if (t == nbn - 1) s_pref[nbn] = excl + cnt;
+  __syncthreads();
 }
 
-// A tile (BM x K, row-major, stride K) by cp.async; rows past the tile's
-// nodes are zero-filled.
-template <int K>
-__device__ __forceinline__ void load_A_tile(const FusedArgs& a, int nn, const int64_t* s_aoff, float* As) {
-  const int RP = a.RP;
+// A tile (BM x K, row-major) of batch-local nodes [tb, tb+nn) by cp.async;
+// rows past the tile's nodes are zero-filled.
+template <int K, int RP>
+__device__ __forceinline__ void load_A_tile(const FusedArgs& a, int tb, int nn, const int64_t* s_aoff, float* As) {
   for (int i = threadIdx.x; i < FB_BM * K / 4; i += FB_THREADS) {
     const int m = i / (K / 4), q = i - m * (K / 4);
     const int j = m / RP;
     float* dst = As + m * K + q * 4;
-    if (j < nn) cp_async16(dst, a.Abase + s_aoff[j] + (m - j * RP) * K + q * 4);
+    if (j < nn) cp_async16(dst, a.Abase + s_aoff[tb + j] + (m - j * RP) * K + q * 4);
     else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
-// flat distinct-ID index f of the tile -> node_local j (s_pref is ascending)
-__device__ __forceinline__ int find_node(const int* s_pref, int nn, int f) {
-  int lo = 0, hi = nn - 1;
+// node (batch-local, in [lo, hi)) owning flat distinct-ID index f
+__device__ __forceinline__ int find_node(const int* s_pref, int lo, int hi, int f) {
+  hi -= 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
@@ -173,153 +180,194 @@ __device__ __forceinline__ int find_node(const int* s_pref, int nn, int f) {
   return lo;
 }
 
-// Stage the last-core slices of IDs [c0, c0+nc) of the tile, transposed:
-// Gs[(ci*NL + jl)*(K+1) + r] = G_{d-1}[r, i_d(u), jl]; also s_u/s_j.
-template <int K>
-__device__ __forceinline__ void stage_ids(const FusedArgs& a, int c0, int nc, int nn, const int* s_node,
-                                          const int* s_pref, int* s_u, int* s_j, float* Gs, bool want_g) {
+// Stage distinct IDs [f0, f0 + nc) of tile nodes [tb, tb+nn): s_u (ID),
+// s_j (tile-local node), s_s0/s_s1 (sorted-slot range) and, if want_g, the
+// last-core slices transposed: Gs[(ci*NL + jl)*(K+4) + r] = G[r, i_d(u), jl].
+template <int K, int NL>
+__device__ __forceinline__ void stage_ids(const FusedArgs& a, int f0, int nc, int tb, int nn, const int* s_cs0,
+                                          const int* s_pref, int* s_u, int* s_j, int* s_s0, int* s_s1, float* Gs,
+                                          bool want_g) {
   for (int ci = threadIdx.x; ci < nc; ci += FB_THREADS) {
-    const int j = find_node(s_pref, nn, c0 + ci);
-    s_j[ci] = j;
-    s_u[ci] = a.cstartF[s_node[j]] + (c0 + ci - s_pref[j]);
+    const int j = find_node(s_pref, tb, tb + nn, f0 + ci);
+    const int u = s_cs0[j] + (f0 + ci - s_pref[j]);
+    s_j[ci] = j - tb;
+    s_u[ci] = u;
+    s_s0[ci] = a.seg[u];
+    s_s1[ci] = a.seg[u + 1];
   }
   __syncthreads();
   if (!want_g) return;
-  const int NL = a.NL;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
-  for (int i = threadIdx.x; i < nc * K * NL; i += FB_THREADS) {
-    const int ci = i / (K * NL), e = i - ci * (K * NL);
-    const int r = e / NL, jl = e - r * NL;
-    Gs[(ci * NL + jl) * (K + 1) + r] = __ldg(Gl + (int64_t)a.digitL[s_u[ci]] * sliceL + e);
+  for (int i = threadIdx.x; i < nc * K * NL / 4; i += FB_THREADS) {
+    const int ci = i / (K * NL / 4), e = (i - ci * (K * NL / 4)) * 4;  // e = r*NL + jl0
+    const int r = e / NL, jl0 = e - r * NL;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(Gl + (int64_t)a.digitL[s_u[ci]] * sliceL + e));
+    float* g = Gs + (ci * NL + jl0) * (K + 4) + r;
+    g[0] = v.x;
+    g[K + 4] = v.y;
+    g[2 * (K + 4)] = v.z;
+    g[3 * (K + 4)] = v.w;
   }
   __syncthreads();
 }
 
+// column n of the thread's micro-tile (GEMM layout): TN >= 4 -> q*128 + lane*4 + t
+template <int BN>
+__device__ __forceinline__ int tile_col(int lane, int jcol) {
+  constexpr int TN = BN / 32;
+  if constexpr (TN >= 4) return (jcol >> 2) * 128 + lane * 4 + (jcol & 3);
+  else return lane * TN + jcol;
+}
+
+template <int BN>
+__device__ __forceinline__ void load_row_frag(const float* row, int lane, float* v) {
+  constexpr int TN = BN / 32;
+  if constexpr (TN >= 4) {
+#pragma unroll
+    for (int q = 0; q < TN / 4; ++q) {
+      const float4 b = *reinterpret_cast<const float4*>(row + q * 128 + lane * 4);
+      v[q * 4 + 0] = b.x; v[q * 4 + 1] = b.y; v[q * 4 + 2] = b.z; v[q * 4 + 3] = b.w;
+    }
+  } else if constexpr (TN == 2) {
+    const float2 b = *reinterpret_cast<const float2*>(row + lane * 2);
+    v[0] = b.x; v[1] = b.y;
+  } else {
+    v[0] = row[lane];
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void store_row_frag(float* row, int lane, const float* v) {
+  constexpr int TN = BN / 32;
+  if constexpr (TN >= 4) {
+#pragma unroll
+    for (int q = 0; q < TN / 4; ++q)
+      *reinterpret_cast<float4*>(row + q * 128 + lane * 4) = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+  } else if constexpr (TN == 2) {
+    *reinterpret_cast<float2*>(row + lane * 2) = make_float2(v[0], v[1]);
+  } else {
+    row[lane] = v[0];
+  }
+}
+
 // ---------------------------------------------------------------------------
-template <int K, int BN>
+template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_fwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP, SG = K + 4;
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
   float* As0 = Bs + K * SB;              // [2][BM][K]
   float* Cs = As0 + 2 * BM * K;          // [BM][BN]
-  float* Gs = Cs + BM * BN;              // [CH][NL][K+1]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * a.NL * (K + 1) + ((a.CH * a.NL * (K + 1)) & 1));
-  int* s_node = reinterpret_cast<int*>(s_aoff + 2 * BM);   // [2][BM]
-  int* s_pref = s_node + 2 * BM;                           // [2][BM+1]
-  int* s_u = s_pref + 2 * (BM + 1);                        // [CH]
-  int* s_j = s_u + a.CH;                                   // [CH]
+  float* Gs = Cs + BM * BN;              // [CH][NL][SG]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * NL * SG);
+  int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
+  int* s_cs0 = s_node + FB_NB;
+  int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
+  int* s_wsum = s_pref + FB_NB + 4;
+  int* s_u = s_wsum + 8;
+  int* s_j = s_u + a.CH;
+  int* s_s0 = s_j + a.CH;
+  int* s_s1 = s_s0 + a.CH;
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
   if (g0 == g1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RP = a.RP, npt = BM / RP, NL = a.NL, BNj = a.BNj, nF = a.nF;
   const int m0 = warp * 8;
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
+  const int nF = a.nF;
 
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
-  int nn = min(npt, g1 - g0);
-  tile_nodes(a, g0, nn, s_node, s_pref, s_aoff);
-  load_A_tile<K>(a, nn, s_aoff, As0);
   cp_async_commit();
-
-  int buf = 0;
-  for (int t0 = g0; t0 < g1; t0 += npt, buf ^= 1) {
-    const int t1 = t0 + npt;
-    const int nn1 = min(npt, g1 - t1);
-    int* nd = s_node + buf * BM;
-    int* pf = s_pref + buf * (BM + 1);
-    if (t1 < g1) {  // prefetch the next tile's nodes and A
-      tile_nodes(a, t1, nn1, s_node + (buf ^ 1) * BM, s_pref + (buf ^ 1) * (BM + 1), s_aoff + (buf ^ 1) * BM);
-      load_A_tile<K>(a, nn1, s_aoff + (buf ^ 1) * BM, As0 + (buf ^ 1) * BM * K);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
+  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
+    const int nbn = min(FB_NB, g1 - nb0);
+    prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    load_A_tile<K, RP>(a, 0, min(NPT, nbn), s_aoff, As0);
+    cp_async_commit();
+    int buf = 0;
+    for (int tb = 0; tb < nbn; tb += NPT, buf ^= 1) {
+      const int nn = min(NPT, nbn - tb);
       cp_async_wait<0>();
-    }
-    __syncthreads();
-    const float* As = As0 + buf * BM * K;
-
-    float acc[8][TN];
+      __syncthreads();
+      if (tb + NPT < nbn) {  // prefetch the next tile's A under this tile's GEMM
+        load_A_tile<K, RP>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
+        cp_async_commit();
+      }
+      const float* As = As0 + buf * BM * K;
+      float acc[8][TN];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 #pragma unroll 2
-    for (int kk = 0; kk < K; kk += 4) {
-      float4 av[8];
+      for (int kk = 0; kk < K; kk += 4) {
+        float4 av[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (m0 + i) * K + kk);
+        for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (m0 + i) * K + kk);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        float bv[TN];
-        if constexpr (TN >= 4) {
+        for (int t = 0; t < 4; ++t) {
+          float bv[TN];
+          load_row_frag<BN>(Bs + (kk + t) * SB, lane, bv);
 #pragma unroll
-          for (int q = 0; q < TN / 4; ++q) {
-            const float4 b = *reinterpret_cast<const float4*>(Bs + (kk + t) * SB + q * 128 + lane * 4);
-            bv[q * 4 + 0] = b.x; bv[q * 4 + 1] = b.y; bv[q * 4 + 2] = b.z; bv[q * 4 + 3] = b.w;
+          for (int i = 0; i < 8; ++i) {
+            const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
           }
-        } else {
-          const float2 b = *reinterpret_cast<const float2*>(Bs + (kk + t) * SB + lane * 2);
-          bv[0] = b.x; bv[1] = b.y;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
         }
       }
-    }
-    const int cur_nn = min(npt, g1 - t0);
-    // C -> shared (epilogue) and -> saved P_F (backward)
+      // C -> shared (epilogue) and -> saved P_F (backward)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m0 + i;
-      const int j = m / RP;
-      float* crow = Cs + m * BN;
-      float* prow = (a.Psave && j < cur_nn)
-                        ? a.Psave + ((int64_t)nd[j] * RP + (m - j * RP)) * a.NC + cb * BN : nullptr;
-      if constexpr (TN >= 4) {
-#pragma unroll
-        for (int q = 0; q < TN / 4; ++q) {
-          const float4 v = make_float4(acc[i][q * 4], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
-          *reinterpret_cast<float4*>(crow + q * 128 + lane * 4) = v;
-          if (prow) *reinterpret_cast<float4*>(prow + q * 128 + lane * 4) = v;
-        }
-      } else {
-        const float2 v = make_float2(acc[i][0], acc[i][1]);
-        *reinterpret_cast<float2*>(crow + lane * 2) = v;
-        if (prow) *reinterpret_cast<float2*>(prow + lane * 2) = v;
+      for (int i = 0; i < 8; ++i) {
+        const int m = m0 + i;
+        const int j = m / RP;
+        store_row_frag<BN>(Cs + m * BN, lane, acc[i]);
+        if (a.Psave && j < nn)
+          store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
       }
-    }
-    __syncthreads();
-    // last level straight from the C tile
-    if (a.out) {
-      const int total_ids = pf[cur_nn];
-      for (int c0 = 0; c0 < total_ids; c0 += a.CH) {
-        const int nc = min(a.CH, total_ids - c0);
-        stage_ids<K>(a, c0, nc, cur_nn, nd, pf, s_u, s_j, Gs, true);
-        const int per_row = nc * NL;
-        for (int f = threadIdx.x; f < RP * BNj * per_row; f += FB_THREADS) {
-          const int rc = f / per_row, e = f - rc * per_row;  // rc = (ar, jf); e = (ci, jl)
-          const int ci = e / NL, jl = e - ci * NL;
-          const int ar = rc / BNj, jf = rc - ar * BNj;
-          const int u = s_u[ci];
-          const float* crow = Cs + (s_j[ci] * RP + ar) * BN + jf * K;
-          const float* gcol = Gs + (ci * NL + jl) * (K + 1);
-          float v = 0.f;
-#pragma unroll 16
-          for (int r = 0; r < K; ++r) v = fmaf(crow[r], gcol[r], v);
-          const int64_t col = ((int64_t)(ar * nF + cb * BNj + jf)) * NL + jl;
-          const int s0 = a.seg[u], s1 = a.seg[u + 1];
+      __syncthreads();
+      if (!a.out) continue;
+      // last level from the C tile: items (ci, jf, jl), each RP outputs (rows ar)
+      const int fA = s_pref[tb], fB = s_pref[tb + nn];
+      for (int f0 = fA; f0 < fB; f0 += a.CH) {
+        const int nc = min(a.CH, fB - f0);
+        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, true);
+        for (int it = threadIdx.x; it < nc * BNJ * NL; it += FB_THREADS) {
+          const int ci = it / (BNJ * NL), rem = it - ci * (BNJ * NL);
+          const int jf = rem / NL, jl = rem - jf * NL;
+          const float* crow = Cs + (s_j[ci] * RP) * BN + jf * K;
+          const float* gcol = Gs + (ci * NL + jl) * SG;
+          float o[RP];
+#pragma unroll
+          for (int ar = 0; ar < RP; ++ar) o[ar] = 0.f;
+#pragma unroll 4
+          for (int r = 0; r < K; r += 4) {
+            const float4 gv = *reinterpret_cast<const float4*>(gcol + r);
+#pragma unroll
+            for (int ar = 0; ar < RP; ++ar) {
+              const float4 cv = *reinterpret_cast<const float4*>(crow + ar * BN + r);
+              o[ar] = fmaf(cv.x, gv.x, o[ar]);
+              o[ar] = fmaf(cv.y, gv.y, o[ar]);
+              o[ar] = fmaf(cv.z, gv.z, o[ar]);
+              o[ar] = fmaf(cv.w, gv.w, o[ar]);
+            }
+          }
+          const int u = s_u[ci], s0 = s_s0[ci], s1 = s_s1[ci];
           if (s1 - s0 > HEAVY_POS) {
-            a.Yu[(int64_t)u * npad + col] = v;
-          } else if (col < emb) {
-            for (int s = s0; s < s1; ++s) a.out[(int64_t)a.spos[s] * emb + col] = v;
+#pragma unroll
+            for (int ar = 0; ar < RP; ++ar)
+              a.Yu[(int64_t)u * npad + ((int64_t)(ar * nF + cb * BNJ + jf)) * NL + jl] = o[ar];
+          } else {
+            for (int s = s0; s < s1; ++s) {
+              float* orow = a.out + (int64_t)a.spos[s] * emb;
+#pragma unroll
+              for (int ar = 0; ar < RP; ++ar) {
+                const int64_t col = ((int64_t)(ar * nF + cb * BNJ + jf)) * NL + jl;
+                if (col < emb) orow[col] = o[ar];
+              }
+            }
           }
         }
         __syncthreads();
@@ -329,9 +377,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_fwd(FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-template <int K, int BN>
+template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP, SG = K + 4;
+  constexpr int OUT = RP * BNJ * NL, WE = K * NL;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;               // [K][SB]
@@ -339,12 +388,16 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
   float* Cs = As + BM * K;        // [BM][BN]  saved C (for W)
   float* Ds = Cs + BM * BN;       // [BM][BN]  dC
   float* Ys = Ds + BM * BN;       // [CH][OUT]
-  float* Gs = Ys + a.CH * a.OUT;  // [CH][NL][K+1]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * a.NL * (K + 1) + ((a.CH * a.NL * (K + 1) + a.CH * a.OUT) & 1));
-  int* s_node = reinterpret_cast<int*>(s_aoff + BM);
-  int* s_pref = s_node + BM;
-  int* s_u = s_pref + BM + 1;
+  float* Gs = Ys + a.CH * OUT;    // [CH][NL][SG]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * NL * SG);
+  int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
+  int* s_cs0 = s_node + FB_NB;
+  int* s_pref = s_cs0 + FB_NB;
+  int* s_wsum = s_pref + FB_NB + 4;
+  int* s_u = s_wsum + 8;
   int* s_j = s_u + a.CH;
+  int* s_s0 = s_j + a.CH;
+  int* s_s1 = s_s0 + a.CH;
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
@@ -354,9 +407,12 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
   cp_async_commit();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RP = a.RP, npt = BM / RP, NL = a.NL, BNj = a.BNj, nF = a.nF, OUT = a.OUT, CH = a.CH;
+  const int m0 = warp * 8;
+  const int nF = a.nF, CH = a.CH;
   const int64_t npad = a.c.npad;
-  const int WE = K * NL;
+  // rows of this warp's micro-tile: node (tile-local) and row within the node
+  constexpr int JLO_DIV = RP;
+  const int wj0 = m0 / JLO_DIV, wj1 = (m0 + 7) / JLO_DIV;
 
   float gacc[TK][TN];
 #pragma unroll
@@ -364,158 +420,159 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
 #pragma unroll
     for (int j = 0; j < TN; ++j) gacc[i][j] = 0.f;
 
-  for (int t0 = g0; t0 < g1; t0 += npt) {
-    const int nn = min(npt, g1 - t0);
-    const int total_ids = tile_nodes(a, t0, nn, s_node, s_pref, s_aoff);
-    load_A_tile<K>(a, nn, s_aoff, As);
-    cp_async_commit();
-    for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {  // saved C tile (for W, used last)
-      const int m = i / (BN / 4), q = i - m * (BN / 4);
-      const int j = m / RP;
-      float* dst = Cs + m * BN + q * 4;
-      if (j < nn) cp_async16(dst, a.Psave + ((int64_t)s_node[j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
-      else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    cp_async_commit();
-    for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS)
-      reinterpret_cast<float4*>(Ds)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
+    const int nbn = min(FB_NB, g1 - nb0);
+    prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    for (int tb = 0; tb < nbn; tb += NPT) {
+      const int nn = min(NPT, nbn - tb);
+      load_A_tile<K, RP>(a, tb, nn, s_aoff, As);
+      cp_async_commit();
+      for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {  // saved C tile (for W, used last)
+        const int m = i / (BN / 4), q = i - m * (BN / 4);
+        const int j = m / RP;
+        float* dst = Cs + m * BN + q * 4;
+        if (j < nn) cp_async16(dst, a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_async_commit();
 
-    // dC = sum over each node's IDs of dY_u G_l(u)^T
-    for (int c0 = 0; c0 < total_ids; c0 += CH) {
-      const int nc = min(CH, total_ids - c0);
-      stage_ids<K>(a, c0, nc, nn, s_node, s_pref, s_u, s_j, Gs, true);
-      for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
-        const int ci = i / (OUT / 4), q = i - ci * (OUT / 4);
-        const int ar = (q * 4) / (BNj * NL), w = q * 4 - ar * (BNj * NL);
-        *reinterpret_cast<float4*>(Ys + ci * OUT + q * 4) = *reinterpret_cast<const float4*>(
-            a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNj) * NL + w);
+      // dC (register-blocked in the GEMM layout) = sum over each node's IDs of dY_u G_l(u)^T
+      float dacc[8][TN];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dacc[i][j] = 0.f;
+      const int fA = s_pref[tb], fB = s_pref[tb + nn];
+      for (int f0 = fA; f0 < fB; f0 += CH) {
+        const int nc = min(CH, fB - f0);
+        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, true);
+        for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
+          const int ci = i / (OUT / 4), q = (i - ci * (OUT / 4)) * 4;
+          const int ar = q / (BNJ * NL), w = q - ar * (BNJ * NL);
+          *reinterpret_cast<float4*>(Ys + ci * OUT + q) = __ldg(reinterpret_cast<const float4*>(
+              a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNJ) * NL + w));
+        }
+        __syncthreads();
+        // this warp's IDs: those of its nodes wj0..wj1 inside the chunk
+        if (wj0 < nn) {
+          const int lo = max(f0, s_pref[tb + wj0]) - f0;
+          const int hi = min(f0 + nc, s_pref[tb + min(wj1, nn - 1) + 1]) - f0;
+          for (int ci = lo; ci < hi; ++ci) {
+            const int j = s_j[ci];
+#pragma unroll
+            for (int jl = 0; jl < NL; ++jl) {
+              float gv[TN];
+              const float* gcol = Gs + (ci * NL + jl) * SG;
+#pragma unroll
+              for (int jc = 0; jc < TN; ++jc) gv[jc] = gcol[tile_col<BN>(lane, jc) % K];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if ((m0 + i) / RP != j) continue;
+                const int ar = (m0 + i) % RP;
+#pragma unroll
+                for (int jc = 0; jc < TN; ++jc) {
+                  const int jf = tile_col<BN>(lane, jc) / K;
+                  dacc[i][jc] = fmaf(Ys[ci * OUT + (ar * BNJ + jf) * NL + jl], gv[jc], dacc[i][jc]);
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
+      cp_async_wait<1>();  // slice block + A tile landed (C may still be in flight)
       __syncthreads();
-      const int jlo = s_j[0], jhi = s_j[nc - 1];
-      const int rows = (jhi - jlo + 1) * RP;
-      for (int i = threadIdx.x; i < rows * BN; i += FB_THREADS) {
-        const int mm = i / BN, n = i - mm * BN;
-        const int m = jlo * RP + mm;
-        const int j = m / RP, ar = m - j * RP;
-        const int jf = n / K, r = n - jf * K;
-        const int f0 = max(s_pref[j], c0) - c0, f1 = min(s_pref[j + 1], c0 + nc) - c0;
-        float v = Ds[m * BN + n];
-        for (int ci = f0; ci < f1; ++ci) {
-          const float* y = Ys + ci * OUT + (ar * BNj + jf) * NL;
-          const float* gc = Gs + ci * NL * (K + 1) + r;
-          for (int jl = 0; jl < NL; ++jl) v = fmaf(y[jl], gc[jl * (K + 1)], v);
-        }
-        Ds[m * BN + n] = v;
-      }
-      __syncthreads();
-    }
-    cp_async_wait<1>();  // slice block + A tile landed (C may still be in flight)
-    __syncthreads();
-    // dG_F block += A^T dC
+      // dG_F block += A^T dC
 #pragma unroll 2
-    for (int m = 0; m < BM; ++m) {
-      float av[TK];
-      if constexpr (TK >= 4) {
+      for (int m = 0; m < BM; ++m) {
+        float av[TK];
+        if constexpr (TK >= 4) {
 #pragma unroll
-        for (int q = 0; q < TK; q += 4) {
-          const float4 t = *reinterpret_cast<const float4*>(As + m * K + warp * TK + q);
-          av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+          for (int q = 0; q < TK; q += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(As + m * K + warp * TK + q);
+            av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < TK; ++q) av[q] = As[m * K + warp * TK + q];
         }
-      } else {
+        float bv[TN];
+        load_row_frag<BN>(Ds + m * BN, lane, bv);
 #pragma unroll
-        for (int q = 0; q < TK; ++q) av[q] = As[m * K + warp * TK + q];
+        for (int i = 0; i < TK; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) gacc[i][j] = fmaf(av[i], bv[j], gacc[i][j]);
       }
-      float bv[TN];
-      if constexpr (TN >= 4) {
-#pragma unroll
-        for (int q = 0; q < TN / 4; ++q) {
-          const float4 b = *reinterpret_cast<const float4*>(Ds + m * BN + q * 128 + lane * 4);
-          bv[q * 4 + 0] = b.x; bv[q * 4 + 1] = b.y; bv[q * 4 + 2] = b.z; bv[q * 4 + 3] = b.w;
-        }
-      } else {
-        const float2 b = *reinterpret_cast<const float2*>(Ds + m * BN + lane * 2);
-        bv[0] = b.x; bv[1] = b.y;
-      }
-#pragma unroll
-      for (int i = 0; i < TK; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) gacc[i][j] = fmaf(av[i], bv[j], gacc[i][j]);
-    }
-    // dA = dC . S_block^T  -> per-(node, column block) partials
-    {
-      const int kg = threadIdx.x % KG, mg = threadIdx.x / KG;
-      float dacc[TMA][TKA];
-#pragma unroll
-      for (int i = 0; i < TMA; ++i)
-#pragma unroll
-        for (int j = 0; j < TKA; ++j) dacc[i][j] = 0.f;
-#pragma unroll 2
-      for (int n = 0; n < BN; n += 4) {
-        float4 cv[TMA], bv[TKA];
-#pragma unroll
-        for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * BN + n);
-#pragma unroll
-        for (int j = 0; j < TKA; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + KG * j) * SB + n);
+      // dA = dC . S_block^T  -> per-(node, column block) partials
+      {
+        const int kg = threadIdx.x % KG, mg = threadIdx.x / KG;
+        float xacc[TMA][TKA];
 #pragma unroll
         for (int i = 0; i < TMA; ++i)
 #pragma unroll
-          for (int j = 0; j < TKA; ++j) {
-            dacc[i][j] = fmaf(cv[i].x, bv[j].x, dacc[i][j]);
-            dacc[i][j] = fmaf(cv[i].y, bv[j].y, dacc[i][j]);
-            dacc[i][j] = fmaf(cv[i].z, bv[j].z, dacc[i][j]);
-            dacc[i][j] = fmaf(cv[i].w, bv[j].w, dacc[i][j]);
-          }
-      }
+          for (int j = 0; j < TKA; ++j) xacc[i][j] = 0.f;
+#pragma unroll 2
+        for (int n = 0; n < BN; n += 4) {
+          float4 cv[TMA], bv[TKA];
 #pragma unroll
-      for (int i = 0; i < TMA; ++i) {
-        const int m = mg + MG * i;
-        const int j = m / RP;
-        if (j >= nn) continue;
-        float* dst = a.dPc + ((int64_t)s_node[j] * a.ncb + cb) * RP * K + (m - j * RP) * K;
+          for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * BN + n);
 #pragma unroll
-        for (int jj = 0; jj < TKA; ++jj) dst[kg + KG * jj] = dacc[i][jj];
+          for (int j = 0; j < TKA; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + KG * j) * SB + n);
+#pragma unroll
+          for (int i = 0; i < TMA; ++i)
+#pragma unroll
+            for (int j = 0; j < TKA; ++j) {
+              xacc[i][j] = fmaf(cv[i].x, bv[j].x, xacc[i][j]);
+              xacc[i][j] = fmaf(cv[i].y, bv[j].y, xacc[i][j]);
+              xacc[i][j] = fmaf(cv[i].z, bv[j].z, xacc[i][j]);
+              xacc[i][j] = fmaf(cv[i].w, bv[j].w, xacc[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < TMA; ++i) {
+          const int m = mg + MG * i;
+          const int j = m / RP;
+          if (j >= nn) continue;
+          float* dst = a.dPc + ((int64_t)s_node[tb + j] * a.ncb + cb) * RP * K + (m - j * RP) * K;
+#pragma unroll
+          for (int jj = 0; jj < TKA; ++jj) dst[kg + KG * jj] = xacc[i][jj];
+        }
       }
-    }
-    cp_async_wait<0>();  // saved C tile
-    __syncthreads();
-    // W_u = C_u^T dY_u  (per distinct ID, this column block's share)
-    for (int c0 = 0; c0 < total_ids; c0 += CH) {
-      const int nc = min(CH, total_ids - c0);
-      stage_ids<K>(a, c0, nc, nn, s_node, s_pref, s_u, s_j, Gs, false);
-      for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
-        const int ci = i / (OUT / 4), q = i - ci * (OUT / 4);
-        const int ar = (q * 4) / (BNj * NL), w = q * 4 - ar * (BNj * NL);
-        *reinterpret_cast<float4*>(Ys + ci * OUT + q * 4) = *reinterpret_cast<const float4*>(
-            a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNj) * NL + w);
-      }
+      cp_async_wait<0>();  // saved C tile
       __syncthreads();
-      for (int f = threadIdx.x; f < nc * WE; f += FB_THREADS) {
-        const int ci = f / WE, e = f - ci * WE;
-        const int r = e / NL, jl = e - r * NL;
-        const int j = s_j[ci];
-        float v = 0.f;
-        for (int ar = 0; ar < RP; ++ar)
-          for (int jf = 0; jf < BNj; ++jf)
-            v = fmaf(Cs[(j * RP + ar) * BN + jf * K + r], Ys[ci * OUT + (ar * BNj + jf) * NL + jl], v);
-        a.W[((int64_t)s_u[ci] * a.ncb + cb) * WE + e] = v;
+      // W_u = C_u^T dY_u  (per distinct ID, this column block's share)
+      for (int f0 = fA; f0 < fB; f0 += CH) {
+        const int nc = min(CH, fB - f0);
+        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, false);
+        for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
+          const int ci = i / (OUT / 4), q = (i - ci * (OUT / 4)) * 4;
+          const int ar = q / (BNJ * NL), w = q - ar * (BNJ * NL);
+          *reinterpret_cast<float4*>(Ys + ci * OUT + q) = __ldg(reinterpret_cast<const float4*>(
+              a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNJ) * NL + w));
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < nc * WE; it += FB_THREADS) {
+          const int ci = it / WE, e = it - ci * WE;
+          const int r = e / NL, jl = e - r * NL;
+          const float* crow = Cs + (s_j[ci] * RP) * BN + r;
+          const float* y = Ys + ci * OUT + jl;
+          float v = 0.f;
+#pragma unroll
+          for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+            for (int jf = 0; jf < BNJ; ++jf) v = fmaf(crow[ar * BN + jf * K], y[(ar * BNJ + jf) * NL], v);
+          a.W[((int64_t)s_u[ci] * a.ncb + cb) * WE + e] = v;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   // the group's dG_F column block (one writer per slice block: no atomics)
   float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
 #pragma unroll
-  for (int i = 0; i < TK; ++i) {
-    float* row = gdst + (int64_t)(warp * TK + i) * a.NC;
-    if constexpr (TN >= 4) {
-#pragma unroll
-      for (int q = 0; q < TN / 4; ++q)
-        *reinterpret_cast<float4*>(row + q * 128 + lane * 4) =
-            make_float4(gacc[i][q * 4], gacc[i][q * 4 + 1], gacc[i][q * 4 + 2], gacc[i][q * 4 + 3]);
-    } else {
-      *reinterpret_cast<float2*>(row + lane * 2) = make_float2(gacc[i][0], gacc[i][1]);
-    }
-  }
+  for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
 
 // dG_{d-1}[v] = sum over the digit-v IDs (group order) and column blocks of W
@@ -577,6 +634,19 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
   }
 }
 
+// The (K, BN, RP, NL) instantiations compiled into the library (engine.cu
+// FUSED_SWITCH): papers, products / sweep32, small, billion, sweep16,
+// sweep64, sweep128.
+#define TT_FUSED_SHAPES(X) \
+  X(64, 256, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 256, 4, 8) X(128, 128, 4, 8)
+
+inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
+#define TT_SHAPE_EQ(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && NL == nl_) return true;
+  TT_FUSED_SHAPES(TT_SHAPE_EQ)
+#undef TT_SHAPE_EQ
+  return false;
+}
+
 // Shape admission for the fused path (host).
 inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   *s = FusedShape{};
@@ -590,10 +660,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   if (K == 64 && NC % 256 == 0) BN = 256;
   if (K == 64 && !BN && NC % 128 == 0) BN = 128;
   if (K == 128 && NC % 128 == 0) BN = 128;
-  if (!BN) return false;
-  if (RP > FB_BM || FB_BM % RP) return false;
-  const int64_t OUT = RP * (BN / K) * NL;
-  if (OUT % 4 || NL > 16) return false;
+  if (!BN || !fused_shape_compiled((int)K, BN, (int)RP, (int)NL)) return false;
   if (c.emb_dim % 4 || c.npad % 4 || c.npad > 512) return false;
   for (int k = 0; k < c.d; ++k)
     if (c.core_off[k] % 4 || c.slice[k] % 4) return false;
@@ -607,13 +674,13 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->NL = (int)NL;
   s->nF = (int)c.n[F];
   s->BNj = (int)(BN / K);
-  s->OUT = (int)OUT;
-  const size_t SB = BN + 4;
-  const size_t ints = sizeof(int64_t) * 2 * FB_BM + sizeof(int) * (6 * FB_BM + 8) + 16;
+  s->OUT = (int)(RP * (BN / K) * NL);
+  const size_t SB = BN + 4, SG = K + 4;
+  const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
   const size_t base_f = sizeof(float) * (K * SB + 2 * FB_BM * K + FB_BM * BN) + ints;
   const size_t base_b = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
-  const size_t per_f = sizeof(float) * NL * (K + 1) + 2 * sizeof(int);
-  const size_t per_b = sizeof(float) * (NL * (K + 1) + OUT) + 2 * sizeof(int);
+  const size_t per_f = sizeof(float) * NL * SG + 4 * sizeof(int);
+  const size_t per_b = sizeof(float) * (NL * SG + s->OUT) + 4 * sizeof(int);
   if (base_f + 4 * per_f > (size_t)FB_SMEM_MAX || base_b + 4 * per_b > (size_t)FB_SMEM_MAX) return false;
   s->CHF = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_f) / per_f);
   s->CHB = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_b) / per_b);

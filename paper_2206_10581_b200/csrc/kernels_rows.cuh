@@ -85,7 +85,17 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
   if (c0 == c1) return;
   for (int64_t c = lane * 4; c < npad; c += 128) {
     float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
-    for (int ch = c0 + 1; ch <= c1; ++ch) {
+    int ch = c0 + 1;
+    for (; ch + 8 <= c1 + 1; ch += 8) {  // 8 loads in flight, added in chunk order
+      float4 x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = *reinterpret_cast<const float4*>(part + ((int64_t)(ch + i) * 2) * npad + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc.x += x[i].x; acc.y += x[i].y; acc.z += x[i].z; acc.w += x[i].w;
+      }
+    }
+    for (; ch <= c1; ++ch) {
       const float4 x = *reinterpret_cast<const float4*>(part + ((int64_t)ch * 2) * npad + c);
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
