@@ -156,7 +156,7 @@ int ensure_plan(tt_engine* h, int64_t B) {
   CU(dalloc(&h->uniq, cap));
   CU(dalloc(&h->pos_a, cap));
   CU(dalloc(&h->pos_b, cap));
-  CU(dalloc(&h->hist, ntiles * RS_BINS));
+  CU(dalloc(&h->hist, ntiles * RS_MAXBINS));
   CU(dalloc(&h->flag, cap));
   CU(dalloc(&h->seg, cap + 1));
   CU(dalloc(&h->lflags, (int64_t)d * cap));
@@ -202,14 +202,17 @@ template <class K>
 K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, const int* n_dev, int n_host,
               int64_t nmax, int nbits, int** vout) {
   const int ntiles = (int)((nmax + RS_TILE - 1) / RS_TILE);
+  const int passes = (nbits + RS_MAXBITS - 1) / RS_MAXBITS;
   K* kin = ka; K* kout = kb;
   int* vin = va; int* vo = vb;
-  for (int shift = 0; shift < nbits; shift += 8) {
-    LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, h->hist, ntiles);
-    LAUNCH(k_scan_excl_single, 1, 1024, 0, s, h->hist, ntiles * RS_BINS);
-    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, 0, s, kin, vin, kout, vo, n_dev, n_host, shift, h->hist, ntiles);
+  int shift = 0;
+  for (int p = 0; p < passes; ++p) {
+    const int bits = (nbits - shift + (passes - p) - 1) / (passes - p);  // split evenly
+    LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, bits, h->hist);
+    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, 0, s, kin, vin, kout, vo, n_dev, n_host, shift, bits, h->hist);
     std::swap(kin, kout);
     std::swap(vin, vo);
+    shift += bits;
   }
   *vout = vin;
   return kin;
@@ -321,6 +324,7 @@ int ensure_fused(tt_engine* h) {
   CU(dalloc(&b.dY, ids * c.npad));
   CU(dalloc(&b.Yu, ids * c.npad));
   CU(dalloc(&b.part, chunks * 2 * c.npad));
+  CU(dalloc(&b.gpart, ((chunks + 31) / 32) * 2 * c.npad));
   b.cap_nodes = nodes;
   b.cap_ids = ids;
   b.cap_chunks = chunks;
@@ -410,14 +414,16 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   const int64_t chunks = (h->B + DY_CHUNK - 1) / DY_CHUNK;
   LAUNCH(k_dy_chunks, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
          h->seg, h->F.dY, h->F.part, h->st);
-  LAUNCH(k_dy_spans, (int)((h->capk[d - 1] + 7) / 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part, h->F.dY,
-         h->st);
+  LAUNCH(k_dy_groups, (int)(((chunks + 31) / 32 + 7) / 8), 256, 0, s, (int)h->B, c.npad, h->flag, h->seg, h->F.part,
+         h->F.gpart, h->F.dY, h->st);
+  LAUNCH(k_dy_spans, (int)((h->capk[d - 1] + 7) / 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part,
+         h->F.gpart, h->F.dY, h->st);
   FusedArgs a = fused_args(h, nullptr);
   a.CH = f.CHB;
   int rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
   if (rc) return rc;
   const int WE = f.K * f.NL;
-  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], std::min(1024, (WE + 31) / 32 * 32), 0, s, c, f.ncb, WE,
+  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], 256, 0, s, c, f.ncb, WE,
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
   const int per = f.RP * f.K;
   float* dst = f.F == 1 ? h->grads : h->L.dP[f.F - 1];
@@ -797,9 +803,20 @@ int tt_step(tt_engine* h, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const DevCfg& c = h->dc;
   LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 2);
-  LAUNCH(k_check_finite, grid_for(c.nparams), 256, 0, s, c, h->grads, h->st);
-  LAUNCH(k_update, grid_for(c.nparams), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, h->opt_kind, (float)h->lr,
-         (float)h->beta1, (float)h->beta2, (float)h->eps, h->d_step, h->st);
+  bool vec4 = true;
+  for (int k = 0; k < c.d; ++k) vec4 = vec4 && c.core_off[k] % 4 == 0 && c.slice[k] % 4 == 0;
+  const int64_t work = vec4 ? c.nparams / 4 : c.nparams;
+  LAUNCH(k_check_finite, grid_for(work), 256, 0, s, c, h->grads, vec4 ? 1 : 0, h->st);
+  const float lr = (float)h->lr, b1 = (float)h->beta1, b2 = (float)h->beta2, ep = (float)h->eps;
+  if (h->opt_kind == TT_OPT_SGD)
+    LAUNCH(k_update<0>, grid_for(work), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, vec4 ? 1 : 0, lr, b1, b2,
+           ep, h->d_step, h->st);
+  else if (h->opt_kind == TT_OPT_ADAM)
+    LAUNCH(k_update<1>, grid_for(work), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, vec4 ? 1 : 0, lr, b1, b2,
+           ep, h->d_step, h->st);
+  else
+    LAUNCH(k_update<2>, grid_for(work), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, vec4 ? 1 : 0, lr, b1, b2,
+           ep, h->d_step, h->st);
   LAUNCH(k_commit_step, 1, 1, 0, s, h->d_step, h->st);
   ++h->cores_version;
   CU(cudaGetLastError());

@@ -61,6 +61,7 @@ struct FusedBufs {
   float* dY = nullptr;     // [capk[d-1]][npad]   upstream summed per distinct ID
   float* Yu = nullptr;     // [capk[d-1]][npad]   rows of heavy IDs
   float* part = nullptr;   // [chunks][2][npad]   k_dy_chunks partials
+  float* gpart = nullptr;  // [groups][2][npad]   k_dy_groups partials
   int64_t cap_nodes = 0, cap_ids = 0, cap_chunks = 0;
 };
 
@@ -71,6 +72,7 @@ inline void free_fused(FusedBufs& b) {
   cudaFree(b.dY);
   cudaFree(b.Yu);
   cudaFree(b.part);
+  cudaFree(b.gpart);
   b = FusedBufs{};
 }
 
@@ -575,33 +577,56 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
 
-// dG_{d-1}[v] = sum over the digit-v IDs (group order) and column blocks of W
-__global__ void k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __restrict__ goffL,
-                                    const int* __restrict__ orderL, const float* __restrict__ W,
-                                    float* __restrict__ grads, const DevStatus* st) {
+// dG_{d-1}[v] = sum over the digit-v IDs (group order) and column blocks of W.
+// 256 threads = S sub-groups x (WE/4) float4 columns; sub-group sg sums the
+// (member, column block) pairs q = sg, sg+S, ... in order, and the S partials
+// are combined in sub-group order (a fixed tree: deterministic).
+__global__ void __launch_bounds__(256) k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __restrict__ goffL,
+                                                           const int* __restrict__ orderL, const float* __restrict__ W,
+                                                           float* __restrict__ grads, const DevStatus* st) {
+  __shared__ float4 red[256];
   if (tt_failed(st)) return;
   const int v = blockIdx.x;
   const int g0 = goffL[v], g1 = goffL[v + 1];
   if (g0 == g1) return;
+  const int cols = WE / 4;
+  const int S = cols >= 256 ? 1 : 256 / cols;
+  float* dst = grads + c.core_off[c.d - 1] + (int64_t)v * c.slice[c.d - 1];
   const int npair = (g1 - g0) * ncb;
-  for (int e = threadIdx.x; e < WE; e += blockDim.x) {
-    float acc = 0.f;
-    int q = 0;
-    for (; q + 8 <= npair; q += 8) {  // (member, column block) pairs in fixed order
-      float x[8];
+  for (int col0 = 0; col0 < cols; col0 += 256) {
+    const int sg = threadIdx.x / min(cols, 256), col = col0 + threadIdx.x % min(cols, 256);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sg < S && col < cols) {
+      int q = sg;
+      for (; q + 3 * S < npair; q += 4 * S) {
+        float4 x[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int gi = g0 + (q + i) / ncb, cbi = (q + i) - ((q + i) / ncb) * ncb;
-        x[i] = W[((int64_t)orderL[gi] * ncb + cbi) * WE + e];
+        for (int i = 0; i < 4; ++i) {
+          const int qq = q + i * S, gi = g0 + qq / ncb, cbi = qq - (qq / ncb) * ncb;
+          x[i] = *reinterpret_cast<const float4*>(W + ((int64_t)orderL[gi] * ncb + cbi) * WE + col * 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc.x += x[i].x; acc.y += x[i].y; acc.z += x[i].z; acc.w += x[i].w;
+        }
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc += x[i];
+      for (; q < npair; q += S) {
+        const int gi = g0 + q / ncb, cbi = q - (q / ncb) * ncb;
+        const float4 x = *reinterpret_cast<const float4*>(W + ((int64_t)orderL[gi] * ncb + cbi) * WE + col * 4);
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
     }
-    for (; q < npair; ++q) {
-      const int gi = g0 + q / ncb, cbi = q - (q / ncb) * ncb;
-      acc += W[((int64_t)orderL[gi] * ncb + cbi) * WE + e];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < min(cols, 256) && col0 + threadIdx.x < cols) {
+      float4 t = red[threadIdx.x];
+      for (int s2 = 1; s2 < S; ++s2) {
+        const float4 y = red[s2 * min(cols, 256) + threadIdx.x];
+        t.x += y.x; t.y += y.y; t.z += y.z; t.w += y.w;
+      }
+      *reinterpret_cast<float4*>(dst + (col0 + threadIdx.x) * 4) = t;
     }
-    grads[c.core_off[c.d - 1] + (int64_t)v * c.slice[c.d - 1] + e] = acc;
+    __syncthreads();
   }
 }
 

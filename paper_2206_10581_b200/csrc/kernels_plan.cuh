@@ -30,130 +30,132 @@ __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B,
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort, 8-bit digits, (key, int value) pairs.
+// Stable LSD radix sort of (key, int value) pairs, up to 10-bit digits per
+// pass, two kernels per pass: per-tile digit histograms, then a scatter whose
+// blocks derive their own global offsets from the histograms (column prefix
+// over earlier tiles + exclusive scan of the digit totals -- redundant per
+// block, L2-resident) and rank keys stably with warp match_any peers.
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_PER_WARP = 512;
 constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;  // 4096 keys per tile
-constexpr int RS_BINS = 256;
+constexpr int RS_MAXBITS = 10;
+constexpr int RS_MAXBINS = 1 << RS_MAXBITS;
 
-template <class K>
-__device__ __forceinline__ int rs_count(const int* n_dev, int n_host) {
-  return n_dev ? ld_count(n_dev) : n_host;
-}
+__device__ __forceinline__ int rs_count(const int* n_dev, int n_host) { return n_dev ? ld_count(n_dev) : n_host; }
 
-// per-tile digit histogram -> hist[digit * ntiles + tile]
+// per-tile digit histogram -> hist[tile * bins + digit]
 template <class K>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, const int* n_dev,
-                                                        int n_host, int shift, int* __restrict__ hist,
-                                                        int ntiles) {
-  __shared__ int cnt[RS_BINS];
-  const int n = rs_count<K>(n_dev, n_host);
-  for (int i = threadIdx.x; i < RS_BINS; i += RS_THREADS) cnt[i] = 0;
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, const int* n_dev, int n_host,
+                                                        int shift, int nbits, int* __restrict__ hist) {
+  __shared__ int cnt[RS_MAXBINS];
+  const int n = rs_count(n_dev, n_host);
+  const int bins = 1 << nbits;
+  const unsigned mask = bins - 1;
+  for (int i = threadIdx.x; i < bins; i += RS_THREADS) cnt[i] = 0;
   __syncthreads();
   const int base = blockIdx.x * RS_TILE;
   if (base < n) {
     for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
-      int g = base + i;
-      if (g < n) atomicAdd(&cnt[(int)((keys[g] >> shift) & 0xFF)], 1);
+      const int g = base + i;
+      if (g < n) atomicAdd(&cnt[(int)((keys[g] >> shift) & mask)], 1);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < RS_BINS; i += RS_THREADS) hist[i * ntiles + blockIdx.x] = cnt[i];
+  for (int i = threadIdx.x; i < bins; i += RS_THREADS) hist[blockIdx.x * bins + i] = cnt[i];
 }
 
-// exclusive scan of an int array of host-known length (single block).
-__global__ void __launch_bounds__(1024) k_scan_excl_single(int* __restrict__ a, int len) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < len; base += 1024 * 8) {
-    int v[8];
-    int t = 0;
-    const int i0 = base + threadIdx.x * 8;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      v[j] = (i0 + j < len) ? a[i0 + j] : 0;
-      t += v[j];
-    }
-    // block exclusive scan of t
-    int x = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane_id() >= (unsigned)o) x += y;
-    }
-    if (lane_id() == 31) wsum[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int w = wsum[threadIdx.x];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane_id() >= (unsigned)o) w += y;
-      }
-      wsum[threadIdx.x] = w;  // inclusive per warp
-    }
-    __syncthreads();
-    int excl = carry + (x - t) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (i0 + j < len) a[i0 + j] = excl;
-      excl += v[j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl;
-    __syncthreads();
-  }
-}
-
-// stable scatter of one tile using per-warp ranks (match_any peers).
 template <class K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const int* __restrict__ vin,
                                                            K* __restrict__ kout, int* __restrict__ vout,
-                                                           const int* n_dev, int n_host, int shift,
-                                                           const int* __restrict__ hist_scanned, int ntiles) {
-  __shared__ int cnt[RS_WARPS][RS_BINS];
-  const int n = rs_count<K>(n_dev, n_host);
+                                                           const int* n_dev, int n_host, int shift, int nbits,
+                                                           const int* __restrict__ hist) {
+  __shared__ int cnt[RS_WARPS][RS_MAXBINS];
+  __shared__ int base[RS_MAXBINS];
+  __shared__ int wsum[RS_WARPS];
+  const int n = rs_count(n_dev, n_host);
   const int tile = blockIdx.x;
   if (tile * RS_TILE >= n) return;
+  const int ntiles = (n + RS_TILE - 1) / RS_TILE;
+  const int bins = 1 << nbits;
+  const unsigned mask = bins - 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+  // global offsets: digit totals (all tiles) and this tile's column prefix
+  constexpr int DPT = RS_MAXBINS / RS_THREADS;  // digits per thread (<= 4)
+  int tot[DPT], pre[DPT];
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    tot[q] = 0;
+    pre[q] = 0;
+    const int dgt = threadIdx.x * DPT + q;
+    if (dgt < bins) {
+      int t = 0;
+      for (; t + 4 <= ntiles; t += 4) {
+        const int h0 = hist[t * bins + dgt], h1 = hist[(t + 1) * bins + dgt];
+        const int h2 = hist[(t + 2) * bins + dgt], h3 = hist[(t + 3) * bins + dgt];
+        pre[q] += (t < tile ? h0 : 0) + (t + 1 < tile ? h1 : 0) + (t + 2 < tile ? h2 : 0) + (t + 3 < tile ? h3 : 0);
+        tot[q] += h0 + h1 + h2 + h3;
+      }
+      for (; t < ntiles; ++t) {
+        const int h = hist[t * bins + dgt];
+        pre[q] += t < tile ? h : 0;
+        tot[q] += h;
+      }
+    }
+  }
+  int my = 0;
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) my += tot[q];
+  int x = my;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  for (int i = threadIdx.x; i < RS_WARPS * RS_MAXBINS; i += RS_THREADS) (&cnt[0][0])[i] = 0;
   __syncthreads();
+  int woff = 0;
+  for (int i = 0; i < w; ++i) woff += wsum[i];
+  int run = woff + x - my;
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int dgt = threadIdx.x * DPT + q;
+    if (dgt < bins) base[dgt] = run + pre[q];
+    run += tot[q];
+  }
+  // per-warp digit counts of this tile
   const int wbase = tile * RS_TILE + w * RS_PER_WARP;
   for (int r = 0; r < RS_PER_WARP / 32; ++r) {
-    int g = wbase + r * 32 + lane;
-    int dig = g < n ? (int)((kin[g] >> shift) & 0xFF) : RS_BINS + lane;
-    unsigned peers = __match_any_sync(0xffffffffu, dig);
-    int leader = 31 - __clz(peers);
-    if (g < n && lane == leader) cnt[w][dig] += __popc(peers);
+    const int g = wbase + r * 32 + lane;
+    const int dig = g < n ? (int)((kin[g] >> shift) & mask) : RS_MAXBINS + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    if (g < n && lane == 31 - __clz(peers)) cnt[w][dig] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  for (int dgt = threadIdx.x; dgt < RS_BINS; dgt += RS_THREADS) {
-    int run = hist_scanned[dgt * ntiles + tile];
+  for (int dgt = threadIdx.x; dgt < bins; dgt += RS_THREADS) {
+    int rr = base[dgt];
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-      int c = cnt[ww][dgt];
-      cnt[ww][dgt] = run;
-      run += c;
+      const int c = cnt[ww][dgt];
+      cnt[ww][dgt] = rr;
+      rr += c;
     }
   }
   __syncthreads();
   for (int r = 0; r < RS_PER_WARP / 32; ++r) {
-    int g = wbase + r * 32 + lane;
-    K key = g < n ? kin[g] : (K)0;
-    int dig = g < n ? (int)((key >> shift) & 0xFF) : RS_BINS + lane;
-    unsigned peers = __match_any_sync(0xffffffffu, dig);
-    int leader = 31 - __clz(peers);
+    const int g = wbase + r * 32 + lane;
+    const K key = g < n ? kin[g] : (K)0;
+    const int dig = g < n ? (int)((key >> shift) & mask) : RS_MAXBINS + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
     if (g < n) {
-      int dst = cnt[w][dig] + __popc(peers & lanemask_lt());
+      const int dst = cnt[w][dig] + __popc(peers & lanemask_lt());
       kout[dst] = key;
       vout[dst] = vin[g];
     }
     __syncwarp();
-    if (g < n && lane == leader) cnt[w][dig] += __popc(peers);
+    if (g < n && lane == 31 - __clz(peers)) cnt[w][dig] += __popc(peers);
     __syncwarp();
   }
 }

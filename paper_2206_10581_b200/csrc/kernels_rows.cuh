@@ -70,33 +70,101 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
   flush(cur);
 }
 
-// finish IDs whose slots span several chunks: first chunk's tail partial,
-// then every following chunk's head partial, in chunk order.
+// Level 1 of the span reduction: warp per group of 32 chunks.  A chunk's
+// head partial part[c][0] continues the ID of its first slot when that ID
+// started in an earlier chunk; runs of equal IDs are summed in chunk order.
+// A run holding all of an ID's continuation chunks completes dY[u] (tail
+// partial of its first chunk + run); otherwise it is kept per group:
+// gpart[G][0] if the ID's continuations began before the group, else
+// gpart[G][1] (it continues after the group).
+__global__ void __launch_bounds__(256) k_dy_groups(int B, int64_t npad, const int* __restrict__ uid1,
+                                                   const int* __restrict__ seg, const float* __restrict__ part,
+                                                   float* __restrict__ gpart, float* __restrict__ dY,
+                                                   const DevStatus* st) {
+  if (tt_failed(st)) return;
+  const int G = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nchunks = (B + DY_CHUNK - 1) / DY_CHUNK;
+  const int cbase = G * 32;
+  if (cbase >= nchunks) return;
+  const int my_c = cbase + lane;
+  int my_u = -1;
+  if (my_c < nchunks) {
+    const int u = uid1[my_c * DY_CHUNK] - 1;
+    if (seg[u] < my_c * DY_CHUNK) my_u = u;  // head partial continues u
+  }
+  const unsigned valid = __ballot_sync(0xffffffffu, my_u >= 0);
+  if (!valid) return;
+  const int nv = (int)((npad + 127) / 128);
+  float4 acc[4];
+  int cur = -1;
+  // a run that holds all of u's continuation chunks is seeded with the tail
+  // partial of u's first chunk (strict chunk order) and completes dY[u]
+  auto complete = [&](int u) {
+    const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
+    return !(c0 + 1 < cbase) && !(c1 > cbase + 31);
+  };
+  auto emit = [&](int u) {
+    const int c0 = seg[u] / DY_CHUNK;
+    const bool before = c0 + 1 < cbase;
+    float* dst = complete(u) ? dY + (int64_t)u * npad : gpart + ((int64_t)G * 2 + (before ? 0 : 1)) * npad;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t c = (int64_t)v * 128 + lane * 4;
+      if (v < nv && c < npad) *reinterpret_cast<float4*>(dst + c) = acc[v];
+    }
+  };
+  for (int i = 0; i < 32; ++i) {
+    const int u = __shfl_sync(0xffffffffu, my_u, i);
+    if (u != cur) {
+      if (cur >= 0) emit(cur);
+      cur = u;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u >= 0 && complete(u)) {
+        const float* head = part + ((int64_t)(seg[u] / DY_CHUNK) * 2 + 1) * npad;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int64_t c = (int64_t)v * 128 + lane * 4;
+          if (v < nv && c < npad) acc[v] = *reinterpret_cast<const float4*>(head + c);
+        }
+      }
+    }
+    if (u < 0) continue;
+    const float* src = part + ((int64_t)(cbase + i) * 2) * npad;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t c = (int64_t)v * 128 + lane * 4;
+      if (v < nv && c < npad) {
+        const float4 x = *reinterpret_cast<const float4*>(src + c);
+        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+      }
+    }
+  }
+  if (cur >= 0) emit(cur);
+}
+
+// Level 2: IDs whose continuation chunks cross group boundaries:
+// dY[u] = tail(c0) + gpart[G0][1] + sum_{G0<G<G1} gpart[G][0] + gpart[G1][0].
 __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts, int d, int64_t npad,
                                                   const int* __restrict__ seg, const float* __restrict__ part,
-                                                  float* __restrict__ dY, const DevStatus* st) {
+                                                  const float* __restrict__ gpart, float* __restrict__ dY,
+                                                  const DevStatus* st) {
   if (tt_failed(st)) return;
   const int U = ld_count(&counts[d - 1]);
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (u >= U) return;
-  const int s0 = seg[u], s1 = seg[u + 1];
-  const int c0 = s0 / DY_CHUNK, c1 = (s1 - 1) / DY_CHUNK;
+  const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
   if (c0 == c1) return;
+  const int G0 = (c0 + 1) / 32, G1 = c1 / 32;
+  if (G0 == G1) return;  // completed by k_dy_groups
   for (int64_t c = lane * 4; c < npad; c += 128) {
     float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
-    int ch = c0 + 1;
-    for (; ch + 8 <= c1 + 1; ch += 8) {  // 8 loads in flight, added in chunk order
-      float4 x[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = *reinterpret_cast<const float4*>(part + ((int64_t)(ch + i) * 2) * npad + c);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        acc.x += x[i].x; acc.y += x[i].y; acc.z += x[i].z; acc.w += x[i].w;
-      }
-    }
-    for (; ch <= c1; ++ch) {
-      const float4 x = *reinterpret_cast<const float4*>(part + ((int64_t)ch * 2) * npad + c);
+    float4 x = *reinterpret_cast<const float4*>(gpart + ((int64_t)G0 * 2 + 1) * npad + c);
+    acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    for (int g = G0 + 1; g <= G1; ++g) {
+      x = *reinterpret_cast<const float4*>(gpart + ((int64_t)g * 2) * npad + c);
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
     *reinterpret_cast<float4*>(dY + (int64_t)u * npad + c) = acc;

@@ -14,59 +14,106 @@
 
 namespace tt {
 
-__device__ __forceinline__ int core_of(const DevCfg& c, int64_t e) {
-  int k = 0;
-#pragma unroll 1
-  while (k + 1 < c.d && e >= c.core_off[k + 1]) ++k;
-  return k;
+// core index and slice of flat parameter e (d <= 8, unrolled compares)
+__device__ __forceinline__ void locate(const DevCfg& c, int64_t e, int& k, int64_t& v) {
+  k = 0;
+#pragma unroll
+  for (int q = 1; q < TT_MAXD; ++q)
+    if (q < c.d && e >= c.core_off[q]) k = q;
+  v = (e - c.core_off[k]) / c.slice[k];
 }
 
-__global__ void k_check_finite(DevCfg c, const float* __restrict__ grads, DevStatus* st) {
+// Vectorised over 4-element groups when every core offset and slice size is a
+// multiple of 4 (then a group never straddles slices); scalar otherwise.
+__global__ void k_check_finite(DevCfg c, const float* __restrict__ grads, int vec4, DevStatus* st) {
   if (tt_failed(st)) return;
   int bad = INT_MAX;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.nparams; e += (int64_t)gridDim.x * blockDim.x) {
-    const float g = grads[e];
-    if (!isfinite(g)) {
-      const int k = core_of(c, e);
-      const int64_t v = (e - c.core_off[k]) / c.slice[k];
-      if (grads[c.tc_off[k] + v] > 0.f && k < bad) bad = k;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  if (vec4) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < c.nparams / 4; q += step) {
+      const float4 g = reinterpret_cast<const float4*>(grads)[q];
+      if (!(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w))) {
+        int k;
+        int64_t v;
+        locate(c, q * 4, k, v);
+        if (grads[c.tc_off[k] + v] > 0.f && k < bad) bad = k;
+      }
+    }
+  } else {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.nparams; e += step) {
+      if (!isfinite(grads[e])) {
+        int k;
+        int64_t v;
+        locate(c, e, k, v);
+        if (grads[c.tc_off[k] + v] > 0.f && k < bad) bad = k;
+      }
     }
   }
   if (bad != INT_MAX) atomicMin(&st->bad_core, bad);
 }
 
-// kind: 0 SGD, 1 Adam, 2 Adagrad.  Vectorised float4 path where a 4-group
-// stays inside one slice (slice sizes are multiples of 4 at every BASELINE
-// config; the scalar tail handles the rest).
-__global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restrict__ grads,
-                         float* __restrict__ s1, float* __restrict__ s2, int kind, float lr, float b1, float b2,
-                         float eps, const long long* __restrict__ step_ptr, const DevStatus* st) {
+template <int KIND>
+__device__ __forceinline__ void upd1(float& p, float g, float& h, float& v2, float lr, float b1, float b2, float eps,
+                                     float bc1, float bc2) {
+  if (KIND == 0) {
+    p = p - lr * g;
+  } else if (KIND == 2) {
+    h = h + g * g;
+    p = p - lr * g / (sqrtf(h) + eps);
+  } else {
+    h = b1 * h + (1.f - b1) * g;
+    v2 = b2 * v2 + (1.f - b2) * g * g;
+    p = p - lr * (h / bc1) / (sqrtf(v2 / bc2) + eps);
+  }
+}
+
+// KIND: 0 SGD, 1 Adam (dense), 2 Adagrad (touched slices only; identical to
+// the dense update since g = 0 leaves p and h bit-identical).
+template <int KIND>
+__global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restrict__ grads, float* __restrict__ s1,
+                         float* __restrict__ s2, int vec4, float lr, float b1, float b2, float eps,
+                         const long long* __restrict__ step_ptr, const DevStatus* st) {
   if (tt_failed(st) || ld_count(&st->bad_core) != INT_MAX) return;
-  const long long step = *step_ptr + 1;
   float bc1 = 1.f, bc2 = 1.f;
-  if (kind == 1) {
+  if (KIND == 1) {
+    const long long step = *step_ptr + 1;
     bc1 = (float)(1.0 - pow((double)b1, (double)step));
     bc2 = (float)(1.0 - pow((double)b2, (double)step));
   }
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.nparams; e += (int64_t)gridDim.x * blockDim.x) {
-    const float g = grads[e];
-    if (kind != 1) {
-      const int k = core_of(c, e);
-      const int64_t v = (e - c.core_off[k]) / c.slice[k];
-      if (!(grads[c.tc_off[k] + v] > 0.f)) continue;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float dummy = 0.f;
+  if (vec4) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < c.nparams / 4; q += stride) {
+      if (KIND != 1) {
+        int k;
+        int64_t v;
+        locate(c, q * 4, k, v);
+        if (!(grads[c.tc_off[k] + v] > 0.f)) continue;
+      }
+      const float4 g = reinterpret_cast<const float4*>(grads)[q];
+      float4 pv = reinterpret_cast<float4*>(p)[q];
+      float4 hv = KIND != 0 ? reinterpret_cast<float4*>(s1)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 vv = KIND == 1 ? reinterpret_cast<float4*>(s2)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      upd1<KIND>(pv.x, g.x, hv.x, vv.x, lr, b1, b2, eps, bc1, bc2);
+      upd1<KIND>(pv.y, g.y, hv.y, vv.y, lr, b1, b2, eps, bc1, bc2);
+      upd1<KIND>(pv.z, g.z, hv.z, vv.z, lr, b1, b2, eps, bc1, bc2);
+      upd1<KIND>(pv.w, g.w, hv.w, vv.w, lr, b1, b2, eps, bc1, bc2);
+      reinterpret_cast<float4*>(p)[q] = pv;
+      if (KIND != 0) reinterpret_cast<float4*>(s1)[q] = hv;
+      if (KIND == 1) reinterpret_cast<float4*>(s2)[q] = vv;
     }
-    if (kind == 0) {
-      p[e] = p[e] - lr * g;
-    } else if (kind == 2) {
-      const float h = s1[e] + g * g;
-      s1[e] = h;
-      p[e] = p[e] - lr * g / (sqrtf(h) + eps);
-    } else {
-      const float m = b1 * s1[e] + (1.f - b1) * g;
-      const float v = b2 * s2[e] + (1.f - b2) * g * g;
-      s1[e] = m;
-      s2[e] = v;
-      p[e] = p[e] - lr * (m / bc1) / (sqrtf(v / bc2) + eps);
+  } else {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.nparams; e += stride) {
+      if (KIND != 1) {
+        int k;
+        int64_t v;
+        locate(c, e, k, v);
+        if (!(grads[c.tc_off[k] + v] > 0.f)) continue;
+      }
+      float h = KIND != 0 ? s1[e] : 0.f, v2 = KIND == 1 ? s2[e] : 0.f;
+      upd1<KIND>(p[e], grads[e], KIND != 0 ? s1[e] : dummy, KIND == 1 ? s2[e] : dummy, lr, b1, b2, eps, bc1, bc2);
+      (void)h;
+      (void)v2;
     }
   }
 }
