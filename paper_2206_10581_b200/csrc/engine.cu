@@ -366,18 +366,24 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
     ++h->launches;                                                                           \
   } while (0)
 
-#define FUSED_CASE(k_, bn_, rp_, nl_)                                                          \
-  else if (f.K == k_ && f.BN == bn_ && f.RP == rp_ && f.NL == nl_) {                          \
-    if (fwd) FUSED_LAUNCH((k_fused_fwd<k_, bn_, rp_, nl_>), f.smem_fwd, grid, s, a);          \
-    else FUSED_LAUNCH((k_fused_bwd<k_, bn_, rp_, nl_>), f.smem_bwd, grid, s, a);              \
-  }
+#define FUSED_CASE_F(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.BNf == bn_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_fused_fwd<k_, bn_, rp_, nl_>), f.smem_fwd, grid, s, a);
+#define FUSED_CASE_B(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.BN == bn_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_fused_bwd<k_, bn_, rp_, nl_>), f.smem_bwd, grid, s, a);
 
 int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a, int grid, cudaStream_t s) {
   const FusedShape& f = h->fs;
-  if (false) {
+  if (fwd) {
+    if (false) {
+    }
+    TT_FUSED_FWD_SHAPES(FUSED_CASE_F)
+    else return fail(TT_ERR_ARG, "fused path: forward shape not compiled");
+  } else {
+    if (false) {
+    }
+    TT_FUSED_SHAPES(FUSED_CASE_B)
+    else return fail(TT_ERR_ARG, "fused path: backward shape not compiled");
   }
-  TT_FUSED_SHAPES(FUSED_CASE)
-  else return fail(TT_ERR_ARG, "fused path: shape not compiled");
   return TT_OK;
 }
 
@@ -398,7 +404,9 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   }
   FusedArgs a = fused_args(h, d_out);
   a.CH = f.CHF;
-  rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncb), s);
+  a.ncb = f.ncbf;
+  a.BNj = f.BNjf;
+  rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
   if (rc) return rc;
   if (d_out)
     LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,

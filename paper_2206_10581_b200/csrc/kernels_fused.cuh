@@ -51,6 +51,7 @@ struct FusedShape {
   int BNj;     // BN / K
   int OUT;     // RP * BNj * NL outputs per ID per column block
   int CHF, CHB;            // distinct IDs staged per chunk (fwd / bwd)
+  int BNf, ncbf, BNjf;     // forward column block (no side traffic: sized for 2 CTAs/SM)
   size_t smem_fwd, smem_bwd;
 };
 
@@ -255,7 +256,7 @@ __device__ __forceinline__ void store_row_frag(float* row, int lane, const float
 
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
-__global__ void __launch_bounds__(FB_THREADS, 1) k_fused_fwd(FusedArgs a) {
+__global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP, SG = K + 4;
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
@@ -664,6 +665,8 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 // sweep64, sweep128.
 #define TT_FUSED_SHAPES(X) \
   X(64, 256, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 256, 4, 8) X(128, 128, 4, 8)
+#define TT_FUSED_FWD_SHAPES(X) \
+  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
 #define TT_SHAPE_EQ(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && NL == nl_) return true;
@@ -700,14 +703,20 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->nF = (int)c.n[F];
   s->BNj = (int)(BN / K);
   s->OUT = (int)(RP * (BN / K) * NL);
-  const size_t SB = BN + 4, SG = K + 4;
+  const int BNf = (int)std::min<int64_t>(BN, 128);
+  s->BNf = BNf;
+  s->ncbf = (int)(NC / BNf);
+  s->BNjf = (int)(BNf / K);
+  const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  const size_t base_f = sizeof(float) * (K * SB + 2 * FB_BM * K + FB_BM * BN) + ints;
+  const size_t base_f = sizeof(float) * (K * SBf + 2 * FB_BM * K + FB_BM * BNf) + ints;
   const size_t base_b = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
   const size_t per_f = sizeof(float) * NL * SG + 4 * sizeof(int);
   const size_t per_b = sizeof(float) * (NL * SG + s->OUT) + 4 * sizeof(int);
   if (base_f + 4 * per_f > (size_t)FB_SMEM_MAX || base_b + 4 * per_b > (size_t)FB_SMEM_MAX) return false;
-  s->CHF = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_f) / per_f);
+  const size_t half = 113 * 1024;  // two forward CTAs per SM when it fits
+  const size_t lim_f = base_f + 4 * per_f <= half ? half : (size_t)FB_SMEM_MAX;
+  s->CHF = (int)std::min<size_t>(32, (lim_f - base_f) / per_f);
   s->CHB = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_b) / per_b);
   s->smem_fwd = base_f + s->CHF * per_f;
   s->smem_bwd = base_b + s->CHB * per_b;
