@@ -255,23 +255,60 @@ __device__ __forceinline__ void store_row_frag(float* row, int lane, const float
 }
 
 // ---------------------------------------------------------------------------
+// Register-level last-core contraction.  A warp's micro-tile holds rows
+// m0..m0+7 and, per lane, NQ column groups of W4 consecutive columns; group q
+// of lane l covers columns q*128 + l*W4 .. (+W4) for BN >= 128 and l*W4.. for
+// BN = 64, i.e. core-F column block jf = col / K and rank index r = col % K.
+// LPJ = K / W4 lanes share one jf, so a contraction over r is W4 FMAs per
+// lane followed by a reduction across those LPJ lanes.  The reduction is a
+// transpose-reduce: V values per lane, log2(LPJ) butterfly levels in which a
+// lane keeps half and ships half, ending with V/LPJ fully reduced values per
+// lane (value index (lane % LPJ) * (V/LPJ) + k).  Fixed tree: deterministic.
+template <int BN>
+struct ColMap {
+  static constexpr int TN = BN / 32;
+  static constexpr int W4 = TN >= 4 ? 4 : TN;
+  static constexpr int NQ = TN / W4;
+  __device__ static int col(int lane, int q) { return TN >= 4 ? q * 128 + lane * 4 : lane * W4; }
+};
+
+template <int V, int LPJ>
+__device__ __forceinline__ void transpose_reduce(float (&v)[V], int lane) {
+  int cnt = V;
+#pragma unroll
+  for (int off = LPJ / 2; off >= 1; off >>= 1) {
+    const bool sel = (lane & off) != 0;
+    const int half = cnt / 2;
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      if (i < half) {
+        const float send = sel ? v[i] : v[i + half];
+        const float keep = sel ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    cnt = half;
+  }
+}
+
+// ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP, SG = K + 4;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
+  using CM = ColMap<BN>;
+  constexpr int W4 = CM::W4, NQ = CM::NQ, LPJ = K / W4;
+  constexpr int NR = RP < 8 ? RP : 8;   // rows of one node inside a warp's 8 rows
+  constexpr int NPW = 8 / NR;           // nodes (or node halves) per warp
+  constexpr int V = NR * NL;            // values per lane per column group before reduction
+  static_assert(V % LPJ == 0 && V >= LPJ, "epilogue reduction shape");
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
   float* As0 = Bs + K * SB;              // [2][BM][K]
-  float* Cs = As0 + 2 * BM * K;          // [BM][BN]
-  float* Gs = Cs + BM * BN;              // [CH][NL][SG]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * NL * SG);
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * K);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
   int* s_wsum = s_pref + FB_NB + 4;
-  int* s_u = s_wsum + 8;
-  int* s_j = s_u + a.CH;
-  int* s_s0 = s_j + a.CH;
-  int* s_s1 = s_s0 + a.CH;
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
@@ -281,6 +318,8 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   const int m0 = warp * 8;
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const int nF = a.nF;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
 
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
   cp_async_commit();
@@ -321,59 +360,63 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
           }
         }
       }
-      // C -> shared (epilogue) and -> saved P_F (backward)
+      // saved P_F for the backward
+      if (a.Psave) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = m0 + i;
-        const int j = m / RP;
-        store_row_frag<BN>(Cs + m * BN, lane, acc[i]);
-        if (a.Psave && j < nn)
-          store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + i, j = m / RP;
+          if (j < nn)
+            store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
+        }
       }
-      __syncthreads();
       if (!a.out) continue;
-      // last level from the C tile: items (ci, jf, jl), each RP outputs (rows ar)
-      const int fA = s_pref[tb], fB = s_pref[tb + nn];
-      for (int f0 = fA; f0 < fB; f0 += a.CH) {
-        const int nc = min(a.CH, fB - f0);
-        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, true);
-        for (int it = threadIdx.x; it < nc * BNJ * NL; it += FB_THREADS) {
-          const int ci = it / (BNJ * NL), rem = it - ci * (BNJ * NL);
-          const int jf = rem / NL, jl = rem - jf * NL;
-          const float* crow = Cs + (s_j[ci] * RP) * BN + jf * K;
-          const float* gcol = Gs + (ci * NL + jl) * SG;
-          float o[RP];
+      // last level from the registers: per node of this warp, per distinct ID
 #pragma unroll
-          for (int ar = 0; ar < RP; ++ar) o[ar] = 0.f;
-#pragma unroll 4
-          for (int r = 0; r < K; r += 4) {
-            const float4 gv = *reinterpret_cast<const float4*>(gcol + r);
+      for (int jw = 0; jw < NPW; ++jw) {
+        const int j = (m0 + jw * NR) / RP;  // tile-local node
+        if (j >= nn) continue;
+        const int ar0 = (m0 + jw * NR) % RP;
+        const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
+        for (int f = fA; f < fB; ++f) {
+          const int u = cs0 + (f - fA);
+          const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
+          const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
 #pragma unroll
-            for (int ar = 0; ar < RP; ++ar) {
-              const float4 cv = *reinterpret_cast<const float4*>(crow + ar * BN + r);
-              o[ar] = fmaf(cv.x, gv.x, o[ar]);
-              o[ar] = fmaf(cv.y, gv.y, o[ar]);
-              o[ar] = fmaf(cv.z, gv.z, o[ar]);
-              o[ar] = fmaf(cv.w, gv.w, o[ar]);
-            }
-          }
-          const int u = s_u[ci], s0 = s_s0[ci], s1 = s_s1[ci];
-          if (s1 - s0 > HEAVY_POS) {
+          for (int q = 0; q < NQ; ++q) {
+            const int colb = CM::col(lane, q);
+            const int r0 = colb % K, jf = colb / K;
+            float gv[W4][NL];
 #pragma unroll
-            for (int ar = 0; ar < RP; ++ar)
-              a.Yu[(int64_t)u * npad + ((int64_t)(ar * nF + cb * BNJ + jf)) * NL + jl] = o[ar];
-          } else {
-            for (int s = s0; s < s1; ++s) {
-              float* orow = a.out + (int64_t)a.spos[s] * emb;
+            for (int t = 0; t < W4; ++t)
 #pragma unroll
-              for (int ar = 0; ar < RP; ++ar) {
-                const int64_t col = ((int64_t)(ar * nF + cb * BNJ + jf)) * NL + jl;
-                if (col < emb) orow[col] = o[ar];
+              for (int l4 = 0; l4 < NL; l4 += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
+                gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
+              }
+            float v[V];
+#pragma unroll
+            for (int ii = 0; ii < NR; ++ii)
+#pragma unroll
+              for (int jl = 0; jl < NL; ++jl) {
+                float s = 0.f;
+#pragma unroll
+                for (int t = 0; t < W4; ++t) s = fmaf(acc[jw * NR + ii][q * W4 + t], gv[t][jl], s);
+                v[ii * NL + jl] = s;
+              }
+            transpose_reduce<V, LPJ>(v, lane);
+#pragma unroll
+            for (int k2 = 0; k2 < V / LPJ; ++k2) {
+              const int idx = (lane % LPJ) * (V / LPJ) + k2;
+              const int ii = idx / NL, jl = idx - ii * NL;
+              const int64_t col = ((int64_t)((ar0 + ii) * nF + cb * BNJ + jf)) * NL + jl;
+              if (s1 - s0 > HEAVY_POS) {
+                a.Yu[(int64_t)u * npad + col] = v[k2];
+              } else if (col < emb) {
+                for (int s = s0; s < s1; ++s) a.out[(int64_t)__ldg(a.spos + s) * emb + col] = v[k2];
               }
             }
           }
         }
-        __syncthreads();
       }
     }
   }
@@ -382,25 +425,24 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP, SG = K + 4;
-  constexpr int OUT = RP * BNJ * NL, WE = K * NL;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP;
+  constexpr int WE = K * NL;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
+  using CM = ColMap<BN>;
+  constexpr int W4 = CM::W4, NQ = CM::NQ;
+  constexpr int NR = RP < 8 ? RP : 8;
+  constexpr int NPW = 8 / NR;
+  constexpr int WPL = WE / 32 > 0 ? WE / 32 : 1;  // W values per lane per ID
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;               // [K][SB]
   float* As = Bs + K * SB;        // [BM][K]
   float* Cs = As + BM * K;        // [BM][BN]  saved C (for W)
   float* Ds = Cs + BM * BN;       // [BM][BN]  dC
-  float* Ys = Ds + BM * BN;       // [CH][OUT]
-  float* Gs = Ys + a.CH * OUT;    // [CH][NL][SG]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Gs + a.CH * NL * SG);
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Ds + BM * BN);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;
   int* s_wsum = s_pref + FB_NB + 4;
-  int* s_u = s_wsum + 8;
-  int* s_j = s_u + a.CH;
-  int* s_s0 = s_j + a.CH;
-  int* s_s1 = s_s0 + a.CH;
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
@@ -411,11 +453,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = warp * 8;
-  const int nF = a.nF, CH = a.CH;
+  const int nF = a.nF;
   const int64_t npad = a.c.npad;
-  // rows of this warp's micro-tile: node (tile-local) and row within the node
-  constexpr int JLO_DIV = RP;
-  const int wj0 = m0 / JLO_DIV, wj1 = (m0 + 7) / JLO_DIV;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
 
   float gacc[TK][TN];
 #pragma unroll
@@ -439,49 +480,54 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       }
       cp_async_commit();
 
-      // dC (register-blocked in the GEMM layout) = sum over each node's IDs of dY_u G_l(u)^T
+      // dC in registers (GEMM layout): dC[row][col] = sum over the node's IDs
+      // and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
       float dacc[8][TN];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) dacc[i][j] = 0.f;
-      const int fA = s_pref[tb], fB = s_pref[tb + nn];
-      for (int f0 = fA; f0 < fB; f0 += CH) {
-        const int nc = min(CH, fB - f0);
-        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, true);
-        for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
-          const int ci = i / (OUT / 4), q = (i - ci * (OUT / 4)) * 4;
-          const int ar = q / (BNJ * NL), w = q - ar * (BNJ * NL);
-          *reinterpret_cast<float4*>(Ys + ci * OUT + q) = __ldg(reinterpret_cast<const float4*>(
-              a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNJ) * NL + w));
-        }
-        __syncthreads();
-        // this warp's IDs: those of its nodes wj0..wj1 inside the chunk
-        if (wj0 < nn) {
-          const int lo = max(f0, s_pref[tb + wj0]) - f0;
-          const int hi = min(f0 + nc, s_pref[tb + min(wj1, nn - 1) + 1]) - f0;
-          for (int ci = lo; ci < hi; ++ci) {
-            const int j = s_j[ci];
 #pragma unroll
-            for (int jl = 0; jl < NL; ++jl) {
-              float gv[TN];
-              const float* gcol = Gs + (ci * NL + jl) * SG;
+      for (int jw = 0; jw < NPW; ++jw) {
+        const int j = (m0 + jw * NR) / RP;
+        if (j >= nn) continue;
+        const int ar0 = (m0 + jw * NR) % RP;
+        const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
+        for (int f = fA; f < fB; ++f) {
+          const int u = cs0 + (f - fA);
+          const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
+          const float* Yp = a.dY + (int64_t)u * npad;
 #pragma unroll
-              for (int jc = 0; jc < TN; ++jc) gv[jc] = gcol[tile_col<BN>(lane, jc) % K];
+          for (int q = 0; q < NQ; ++q) {
+            const int colb = CM::col(lane, q);
+            const int r0 = colb % K, jf = colb / K;
+            float gv[W4][NL];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if ((m0 + i) / RP != j) continue;
-                const int ar = (m0 + i) % RP;
+            for (int t = 0; t < W4; ++t)
 #pragma unroll
-                for (int jc = 0; jc < TN; ++jc) {
-                  const int jf = tile_col<BN>(lane, jc) / K;
-                  dacc[i][jc] = fmaf(Ys[ci * OUT + (ar * BNJ + jf) * NL + jl], gv[jc], dacc[i][jc]);
-                }
+              for (int l4 = 0; l4 < NL; l4 += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
+                gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
+              }
+#pragma unroll
+            for (int ii = 0; ii < NR; ++ii) {
+              float yv[NL];
+              const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + cb * BNJ + jf) * NL;
+#pragma unroll
+              for (int l4 = 0; l4 < NL; l4 += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
+                yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+              }
+#pragma unroll
+              for (int t = 0; t < W4; ++t) {
+                float s = dacc[jw * NR + ii][q * W4 + t];
+#pragma unroll
+                for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[jl], gv[t][jl], s);
+                dacc[jw * NR + ii][q * W4 + t] = s;
               }
             }
           }
         }
-        __syncthreads();
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
@@ -545,31 +591,35 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       }
       cp_async_wait<0>();  // saved C tile
       __syncthreads();
-      // W_u = C_u^T dY_u  (per distinct ID, this column block's share)
-      for (int f0 = fA; f0 < fB; f0 += CH) {
-        const int nc = min(CH, fB - f0);
-        stage_ids<K, NL>(a, f0, nc, tb, nn, s_cs0, s_pref, s_u, s_j, s_s0, s_s1, Gs, false);
-        for (int i = threadIdx.x; i < nc * OUT / 4; i += FB_THREADS) {
-          const int ci = i / (OUT / 4), q = (i - ci * (OUT / 4)) * 4;
-          const int ar = q / (BNJ * NL), w = q - ar * (BNJ * NL);
-          *reinterpret_cast<float4*>(Ys + ci * OUT + q) = __ldg(reinterpret_cast<const float4*>(
-              a.dY + (int64_t)s_u[ci] * npad + ((int64_t)ar * nF + cb * BNJ) * NL + w));
-        }
-        __syncthreads();
-        for (int it = threadIdx.x; it < nc * WE; it += FB_THREADS) {
-          const int ci = it / WE, e = it - ci * WE;
-          const int r = e / NL, jl = e - r * NL;
-          const float* crow = Cs + (s_j[ci] * RP) * BN + r;
-          const float* y = Ys + ci * OUT + jl;
-          float v = 0.f;
+      // W_u = C_u^T dY_u (this column block's share): one warp per ID, lane
+      // owns WPL consecutive (r, jl) entries
+      const int fA = s_pref[tb], fB = s_pref[tb + nn];
+      for (int f = fA + warp; f < fB; f += FB_THREADS / 32) {
+        const int j = find_node(s_pref, tb, tb + nn, f) - tb;
+        const int u = s_cs0[tb + j] + (f - s_pref[tb + j]);
+        const float* Yp = a.dY + (int64_t)u * npad;
+        float wv[WPL];
 #pragma unroll
-          for (int ar = 0; ar < RP; ++ar)
+        for (int e = 0; e < WPL; ++e) wv[e] = 0.f;
+        const int e0 = lane * WPL;
 #pragma unroll
-            for (int jf = 0; jf < BNJ; ++jf) v = fmaf(crow[ar * BN + jf * K], y[(ar * BNJ + jf) * NL], v);
-          a.W[((int64_t)s_u[ci] * a.ncb + cb) * WE + e] = v;
-        }
-        __syncthreads();
+        for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+          for (int jf = 0; jf < BNJ; ++jf) {
+            const float* crow = Cs + (j * RP + ar) * BN + jf * K;
+            const float* yrow = Yp + ((int64_t)ar * nF + cb * BNJ + jf) * NL;
+#pragma unroll
+            for (int e = 0; e < WPL; ++e) {
+              const int ee = e0 + e, r = ee / NL, jl = ee - r * NL;
+              if (ee < WE) wv[e] = fmaf(crow[r], __ldg(yrow + jl), wv[e]);
+            }
+          }
+        float* wdst = a.W + ((int64_t)u * a.ncb + cb) * WE;
+#pragma unroll
+        for (int e = 0; e < WPL; ++e)
+          if (e0 + e < WE) wdst[e0 + e] = wv[e];
       }
+      __syncthreads();
     }
   }
   // the group's dG_F column block (one writer per slice block: no atomics)
@@ -709,17 +759,11 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->BNjf = (int)(BNf / K);
   const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  const size_t base_f = sizeof(float) * (K * SBf + 2 * FB_BM * K + FB_BM * BNf) + ints;
-  const size_t base_b = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
-  const size_t per_f = sizeof(float) * NL * SG + 4 * sizeof(int);
-  const size_t per_b = sizeof(float) * (NL * SG + s->OUT) + 4 * sizeof(int);
-  if (base_f + 4 * per_f > (size_t)FB_SMEM_MAX || base_b + 4 * per_b > (size_t)FB_SMEM_MAX) return false;
-  const size_t half = 113 * 1024;  // two forward CTAs per SM when it fits
-  const size_t lim_f = base_f + 4 * per_f <= half ? half : (size_t)FB_SMEM_MAX;
-  s->CHF = (int)std::min<size_t>(32, (lim_f - base_f) / per_f);
-  s->CHB = (int)std::min<size_t>(32, (FB_SMEM_MAX - base_b) / per_b);
-  s->smem_fwd = base_f + s->CHF * per_f;
-  s->smem_bwd = base_b + s->CHB * per_b;
+  s->smem_fwd = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints;
+  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
+  (void)SG;
+  if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
+  s->CHF = s->CHB = 0;
   return true;
 }
 

@@ -1,0 +1,105 @@
+"""The data-parallel decomposition on CPU (world_size 2, gloo): each rank
+takes a position shard of the batch, computes its core gradients (oracle,
+fp64), packs them with per-slice touch counts into the engine's flat gradient
+buffer layout (paper_2206_10581_b200.dist), and the ranks sum-all-reduce the
+buffer exactly as bench.py / DataParallelTT do over NCCL on GPUs.  The
+reduced buffer must equal the full-batch gradient, its counters the union of
+touched slices, and the touched-only update the reference's dense update."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2206_10581_b200 import config as C
+from paper_2206_10581_b200 import dist as D
+from paper_2206_10581_b200 import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cfg():
+    return C.plan_factorization(2449029, 128, [126, 140, 140], [4, 4, 8], [1, 4, 4, 1])
+
+
+def _worker(rank, world, port, B, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _cfg()
+    cores = [c.astype(np.float64) for c in synth.gaussian_cores(cfg, 5)]
+    idx = synth.zipf_ids(6, B, 1.1, cfg.num_nodes)
+    up = synth.normal(7, 1, B * 128, 1.0, np.float64).reshape(B, 128)
+    lo, hi = D.shard_bounds(B, rank, world)
+    g, bad = oracle.backward_lookup(cfg, cores, idx[lo:hi], up[lo:hi])
+    assert bad == -1
+    buf = torch.from_numpy(D.pack_grad_buffer(cfg, g, D.touch_counts(cfg, idx[lo:hi])))
+    dist.all_reduce(buf)
+    if rank == 0:
+        np.save(out, buf.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_allreduce_equals_full_batch(tmp_path, world):
+    B = 600
+    out = str(tmp_path / "buf.npy")
+    mp.start_processes(_worker, args=(world, _free_port(), B, out), nprocs=world, start_method="spawn")
+    buf = np.load(out)
+    cfg = _cfg()
+    assert buf.size == D.grad_buffer_len(cfg)
+    grads, touched = D.unpack_grad_buffer(cfg, buf)
+    cores = [c.astype(np.float64) for c in synth.gaussian_cores(cfg, 5)]
+    idx = synth.zipf_ids(6, B, 1.1, cfg.num_nodes)
+    up = synth.normal(7, 1, B * 128, 1.0, np.float64).reshape(B, 128)
+    full, _ = oracle.backward_lookup(cfg, cores, idx, up)
+    for k in range(cfg.d):
+        np.testing.assert_allclose(grads[k], full[k], rtol=1e-11, atol=1e-12)
+    # counters: union of touched slices (a slice is touched iff its count > 0)
+    want = D.touch_counts(cfg, idx)
+    for k in range(cfg.d):
+        np.testing.assert_array_equal(touched[k] > 0, want[k] > 0)
+        untouched = ~(touched[k] > 0)
+        assert np.all(grads[k][:, untouched] == 0.0)
+    # touched-only Adagrad on the reduced buffer == the reference's dense update
+    dense = [c.copy() for c in cores]
+    opt = oracle.OptState(cfg, oracle.ADAGRAD, 0.01)
+    assert oracle.apply_update(cfg, dense, full, opt) == -1
+    sparse = [c.copy() for c in cores]
+    for k in range(cfg.d):
+        live = touched[k] > 0
+        gk = grads[k][:, live]
+        h = gk * gk
+        sparse[k][:, live] -= 0.01 * gk / (np.sqrt(h) + 1e-10)
+        np.testing.assert_allclose(sparse[k], dense[k], rtol=1e-12, atol=1e-15)
+
+
+def test_shard_bounds_partition():
+    for B in (0, 1, 7, 4096, 262144):
+        for world in (1, 2, 3, 8):
+            parts = [D.shard_bounds(B, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == B
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            assert max(h - l for l, h in parts) - min(h - l for l, h in parts) <= 1
+
+
+def test_pack_unpack_roundtrip():
+    cfg = C.plan_factorization(1000, 30, [7, 11, 13], [2, 3, 5], [1, 5, 3, 1])
+    g = [synth.normal(1, k, cfg.core_size(k), 1.0, np.float64).reshape(cfg.core_shape(k)) for k in range(3)]
+    t = [np.arange(cfg.m[k], dtype=np.float64) for k in range(3)]
+    g2, t2 = D.unpack_grad_buffer(cfg, D.pack_grad_buffer(cfg, g, t))
+    for a, b in zip(g, g2):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(t, t2):
+        np.testing.assert_array_equal(a, b)
