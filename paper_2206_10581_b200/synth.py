@@ -166,7 +166,7 @@ def gaussian_cores(cfg, seed: int, std: float = 0.1, dtype=np.float32):
 
 def checksum(a: np.ndarray) -> str:
     """Order-sensitive 64-bit checksum of a buffer's bytes (for run records)."""
-    b = np.ascontiguousarray(a).view(np.uint8)
+    b = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
     pad = (-len(b)) % 8
     w = np.concatenate([b, np.zeros(pad, np.uint8)]).view(np.uint64)
     h = splitmix64(w ^ splitmix64(np.arange(len(w), dtype=np.uint64)))
