@@ -100,6 +100,12 @@ int tt_step(tt_engine* h, void* stream);
 /* Waits for `stream`, returns (and clears) the first deferred error. */
 int tt_sync(tt_engine* h, void* stream);
 
+/* Device-side checkpoint of the cores: snapshot copies the parameters to a
+ * handle-owned buffer, restore copies them back (stream-ordered).  Optimizer
+ * state and step are not touched. */
+int tt_cores_snapshot(tt_engine* h, void* stream);
+int tt_cores_restore(tt_engine* h, void* stream);
+
 /* ---- host-buffer entry points (synchronous; the reference call shapes) ---- */
 int tt_lookup_batch(tt_engine* h, const int64_t* h_indices, int64_t batch, float* h_out);
 int tt_backward_lookup(tt_engine* h, const int64_t* h_indices, int64_t batch,

@@ -72,6 +72,7 @@ struct tt_engine {
   int64_t ntc = 0;         // number of touch counters (sum of m_k)
   float* s1 = nullptr;
   float* s2 = nullptr;
+  float* snap = nullptr;  // tt_cores_snapshot
   long long* d_step = nullptr;
   DevStatus* st = nullptr;
   int opt_kind = TT_OPT_SGD;
@@ -387,6 +388,70 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a, int grid, cudaStr
   return TT_OK;
 }
 
+// Wide (materialised) level k < F on the fused kernels: C = P_{k-1} . G_k is
+// written to L.P[k] (forward), dC = L.dP[k] (backward).  Requires a compiled
+// (K, BN, RP, *) instantiation; otherwise the generic kernels run.
+struct WideShape {
+  bool ok = false;
+  FusedShape f{};
+};
+
+WideShape wide_shape(const DevCfg& c, int k) {
+  WideShape w;
+  const int64_t K = c.R[k], NC = c.cols[k], RP = c.rows[k];
+  int BN = 0;
+  if (K == 16 && NC % 64 == 0) BN = 64;
+  if (K == 32 && NC % 128 == 0) BN = 128;
+  if (K == 64 && NC % 128 == 0) BN = 128;
+  if (K == 128 && NC % 128 == 0) BN = 128;
+  if (!BN || RP > FB_BM || FB_BM % RP || c.R[k + 1] != K) return w;
+  int nl = 0;
+  for (int cand : {4, 8})
+    if (fused_shape_compiled((int)K, BN, (int)RP, cand) || fused_shape_compiled((int)K, BN * 2, (int)RP, cand)) nl = cand;
+  if (!nl) return w;
+  FusedShape& f = w.f;
+  f.ok = 1; f.F = k; f.K = (int)K; f.NC = (int)NC; f.RP = (int)RP; f.NL = nl; f.nF = (int)c.n[k];
+  f.BN = BN; f.ncb = (int)(NC / BN); f.BNj = BN / (int)K; f.OUT = 0;
+  f.BNf = BN; f.ncbf = f.ncb; f.BNjf = f.BNj;
+  const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
+  f.smem_fwd = sizeof(float) * (K * (BN + 4) + 2 * FB_BM * K) + ints;
+  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + 2 * FB_BM * BN) + ints;
+  // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
+  bool fwd_ok = false, bwd_ok = false;
+#define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;
+#define TT_CHECK_B(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && nl == nl_) bwd_ok = true;
+  TT_FUSED_FWD_SHAPES(TT_CHECK_F)
+  TT_FUSED_SHAPES(TT_CHECK_B)
+#undef TT_CHECK_F
+#undef TT_CHECK_B
+  w.ok = fwd_ok && bwd_ok;
+  return w;
+}
+
+FusedArgs wide_args(tt_engine* h, int k, const FusedShape& f) {
+  FusedArgs a = fused_args(h, nullptr);
+  const int64_t cap = h->cap;
+  a.F = k; a.ncb = f.ncb; a.RP = f.RP; a.NL = f.NL; a.nF = f.nF; a.BNj = f.BNj; a.OUT = 0; a.NC = f.NC;
+  a.Abase = k >= 2 ? h->L.P[k - 1] : h->params;
+  a.parentF = h->parent + k * cap;
+  a.goffF = h->goff[k];
+  a.orderF = h->order[k];
+  a.cstartF = h->cstart + k * (cap + 1);
+  a.Psave = h->L.P[k];
+  a.out = nullptr;
+  a.mode = 1;
+  a.dPin = h->L.dP[k];
+  return a;
+}
+
+int wide_dispatch(tt_engine* h, const FusedShape& f, bool fwd, const FusedArgs& a, int grid, cudaStream_t s) {
+  FusedShape saved = h->fs;
+  h->fs = f;
+  int rc = fused_dispatch(h, fwd, a, grid, s);
+  h->fs = saved;
+  return rc;
+}
+
 int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   const DevCfg& c = h->dc;
   const FusedShape& f = h->fs;
@@ -397,6 +462,13 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     if (rc) return rc;
     const int64_t cap = h->cap;
     for (int k = 1; k < f.F; ++k) {
+      const WideShape w = wide_shape(c, k);
+      if (w.ok) {
+        FusedArgs wa = wide_args(h, k, w.f);
+        rc = wide_dispatch(h, w.f, true, wa, (int)(c.m[k] * w.f.ncbf), s);
+        if (rc) return rc;
+        continue;
+      }
       const int64_t total = h->capk[k] * c.rows[k] * c.cols[k];
       LAUNCH(k_gen_fwd_level, grid_for(total), 256, 0, s, c, k, h->params, h->L, h->counts, h->digit + k * cap,
              h->parent + k * cap, h->digit, h->seg, h->spos, nullptr, h->st);
@@ -428,6 +500,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
          h->F.gpart, h->F.dY, h->st);
   FusedArgs a = fused_args(h, nullptr);
   a.CH = f.CHB;
+  a.mode = 0;
   int rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
   if (rc) return rc;
   const int WE = f.K * f.NL;
@@ -438,6 +511,23 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   LAUNCH(k_fused_reduce_children, grid_for(h->capk[f.F - 1] * per), 256, 0, s, c, f.F, f.ncb, per, h->counts,
          h->cstart + (f.F - 1) * (cap + 1), h->digit, h->F.dPc, dst, h->st);
   for (int k = f.F - 1; k >= 1; --k) {
+    const WideShape w = wide_shape(c, k);
+    if (w.ok) {
+      if (!h->F.dPcw || h->F.cap_w < h->capk[k] * w.f.ncb * w.f.RP * w.f.K) {
+        cudaFree(h->F.dPcw);
+        h->F.cap_w = h->capk[k] * w.f.ncb * w.f.RP * w.f.K;
+        CU(dalloc(&h->F.dPcw, h->F.cap_w));
+      }
+      FusedArgs wa = wide_args(h, k, w.f);
+      wa.dPc = h->F.dPcw;
+      rc = wide_dispatch(h, w.f, false, wa, (int)(c.m[k] * w.f.ncb), s);
+      if (rc) return rc;
+      const int wper = w.f.RP * w.f.K;
+      float* wdst = k == 1 ? h->grads : h->L.dP[k - 1];
+      LAUNCH(k_fused_reduce_children, grid_for(h->capk[k - 1] * wper), 256, 0, s, c, k, w.f.ncb, wper, h->counts,
+             h->cstart + (k - 1) * (cap + 1), h->digit, h->F.dPcw, wdst, h->st);
+      continue;
+    }
     LAUNCH(k_gen_bwd_input, grid_for(h->capk[k] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->params, h->L, h->counts,
            h->digit + k * cap, h->st);
     LAUNCH(k_gen_bwd_weight, grid_for(c.m[k] * c.R[k] * c.cols[k]), 256, 0, s, c, k, h->params, h->L, h->goff[k],
@@ -445,7 +535,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     LAUNCH(k_gen_reduce_children, grid_for(h->capk[k - 1] * c.rows[k] * c.R[k]), 256, 0, s, c, k, h->L, h->counts,
            h->cstart + (k - 1) * (cap + 1), h->st);
   }
-  if (f.F >= 2)
+  if (f.F >= 2 && !wide_shape(c, 1).ok)
     LAUNCH(k_gen_bwd_core0, grid_for(h->capk[0] * c.cols[0]), 256, 0, s, c, h->L, h->counts, h->digit, h->grads,
            h->st);
   return TT_OK;
@@ -670,7 +760,7 @@ void tt_engine_destroy(tt_engine* h) {
   cudaSetDevice(h->device);
   if (h->own) cudaStreamSynchronize(h->own);
   free_plan(h);
-  void* ptrs[] = {h->params, h->own_grads, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
+  void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
   for (void* p : ptrs) cudaFree(p);
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
@@ -726,6 +816,25 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
   CU(cudaMemcpy(buf.data(), h->grads, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
   from_device_layout(h->dc, buf, grads, buf.data() + h->dc.nparams);
   if (batch_count) *batch_count = h->batch_count;
+  return TT_OK;
+}
+
+int tt_cores_snapshot(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_cores_snapshot: null handle");
+  CU(cudaSetDevice(h->device));
+  if (!h->snap) CU(dalloc(&h->snap, h->dc.nparams));
+  CU(cudaMemcpyAsync(h->snap, h->params, sizeof(float) * (size_t)h->dc.nparams, cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  return TT_OK;
+}
+
+int tt_cores_restore(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_cores_restore: null handle");
+  if (!h->snap) return fail(TT_ERR_STATE, "tt_cores_restore: no snapshot");
+  CU(cudaSetDevice(h->device));
+  CU(cudaMemcpyAsync(h->params, h->snap, sizeof(float) * (size_t)h->dc.nparams, cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  ++h->cores_version;
   return TT_OK;
 }
 

@@ -63,7 +63,8 @@ struct FusedBufs {
   float* Yu = nullptr;     // [capk[d-1]][npad]   rows of heavy IDs
   float* part = nullptr;   // [chunks][2][npad]   k_dy_chunks partials
   float* gpart = nullptr;  // [groups][2][npad]   k_dy_groups partials
-  int64_t cap_nodes = 0, cap_ids = 0, cap_chunks = 0;
+  float* dPcw = nullptr;   // wide-level dA partials
+  int64_t cap_nodes = 0, cap_ids = 0, cap_chunks = 0, cap_w = 0;
 };
 
 inline void free_fused(FusedBufs& b) {
@@ -74,12 +75,15 @@ inline void free_fused(FusedBufs& b) {
   cudaFree(b.Yu);
   cudaFree(b.part);
   cudaFree(b.gpart);
+  cudaFree(b.dPcw);
   b = FusedBufs{};
 }
 
 struct FusedArgs {
   DevCfg c;
   int F, ncb, RP, NL, nF, BNj, OUT, NC, CH;
+  int mode;                 // 0: fused last level; 1: wide level (dC = dPin, no IDs, no W)
+  const float* dPin;        // mode 1: materialised dP_F [nodes][RP][NC]
   const float* params;
   const float* Abase;       // core-0 parameters (F == 1) or the P_{F-1} buffer
   const int* parentF;       // level-F node parents
@@ -471,14 +475,18 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       const int nn = min(NPT, nbn - tb);
       load_A_tile<K, RP>(a, tb, nn, s_aoff, As);
       cp_async_commit();
-      for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {  // saved C tile (for W, used last)
+      // mode 0: saved C tile (for W, used last); mode 1: the materialised dC tile
+      const float* csrc = a.mode == 0 ? a.Psave : a.dPin;
+      float* cdst = a.mode == 0 ? Cs : Ds;
+      for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
         const int m = i / (BN / 4), q = i - m * (BN / 4);
         const int j = m / RP;
-        float* dst = Cs + m * BN + q * 4;
-        if (j < nn) cp_async16(dst, a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
+        float* dst = cdst + m * BN + q * 4;
+        if (j < nn) cp_async16(dst, csrc + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
         else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       cp_async_commit();
+      if (a.mode == 0) {
 
       // dC in registers (GEMM layout): dC[row][col] = sum over the node's IDs
       // and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
@@ -532,6 +540,9 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
       cp_async_wait<1>();  // slice block + A tile landed (C may still be in flight)
+      } else {
+        cp_async_wait<0>();  // slice block + A tile + dC tile
+      }
       __syncthreads();
       // dG_F block += A^T dC
 #pragma unroll 2
@@ -588,6 +599,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
 #pragma unroll
           for (int jj = 0; jj < TKA; ++jj) dst[kg + KG * jj] = xacc[i][jj];
         }
+      }
+      if (a.mode == 1) {
+        __syncthreads();
+        continue;
       }
       cp_async_wait<0>();  // saved C tile
       __syncthreads();

@@ -55,7 +55,7 @@ SYMBOLS = [
     "tt_set_cores_f32", "tt_get_cores_f64", "tt_get_cores_f32", "tt_opt_init", "tt_opt_get_step", "tt_forward",
     "tt_backward", "tt_step", "tt_sync", "tt_lookup_batch", "tt_backward_lookup", "tt_apply_update",
     "tt_train_step_host", "tt_get_core_grads_f64", "tt_set_core_grads_f64", "tt_grad_buffer", "tt_set_dense_grads", "tt_bind_grad_buffer",
-    "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_path", "tt_last_path",
+    "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops",
 ]
 
@@ -85,6 +85,7 @@ def load_library(build_if_missing: bool = True):
         "tt_get_core_grads_f64": (i32, [vp, vp, vp]), "tt_set_core_grads_f64": (i32, [vp, vp, i64]),
         "tt_grad_buffer": (i32, [vp, vp, vp]), "tt_set_dense_grads": (i32, [vp, i32]),
         "tt_bind_grad_buffer": (i32, [vp, vp, i64]),
+        "tt_cores_snapshot": (i32, [vp, vp]), "tt_cores_restore": (i32, [vp, vp]),
         "tt_plan_stats": (i32, [vp, vp]), "tt_plan_digits": (i64, [vp, vp, vp, i64]),
         "tt_plan_sorted": (i64, [vp, vp, vp, i64]), "tt_launch_count": (i64, [vp]),
         "tt_set_path": (i32, [vp, i32]), "tt_last_path": (i32, [vp]),
@@ -279,6 +280,12 @@ class TTEmbedding:
 
     def step(self) -> None:
         _raise(self._lib.tt_step(self._h, self._stream()), "tt_step")
+
+    def snapshot_cores(self) -> None:
+        _raise(self._lib.tt_cores_snapshot(self._h, self._stream()), "tt_cores_snapshot")
+
+    def restore_cores(self) -> None:
+        _raise(self._lib.tt_cores_restore(self._h, self._stream()), "tt_cores_restore")
 
     def sync(self) -> None:
         _raise(self._lib.tt_sync(self._h, self._stream()), "tt_sync")
