@@ -402,7 +402,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   int BN = 0;
   if (K == 16 && NC % 64 == 0) BN = 64;
   if (K == 32 && NC % 128 == 0) BN = 128;
-  if (K == 64 && NC % 128 == 0) BN = 128;
+  if (K == 64 && NC % 256 == 0) BN = 256;
   if (K == 128 && NC % 128 == 0) BN = 128;
   if (!BN || RP > FB_BM || FB_BM % RP || c.R[k + 1] != K) return w;
   int nl = 0;
@@ -414,7 +414,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   f.BN = BN; f.ncb = (int)(NC / BN); f.BNj = BN / (int)K; f.OUT = 0;
   f.BNf = BN; f.ncbf = f.ncb; f.BNjf = f.BNj;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  f.smem_fwd = sizeof(float) * (K * (BN + 4) + 2 * FB_BM * K) + ints;
+  f.smem_fwd = sizeof(float) * (K * (BN + 4) + 2 * K * (FB_BM + 4)) + ints;
   f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + 2 * FB_BM * BN) + ints;
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;

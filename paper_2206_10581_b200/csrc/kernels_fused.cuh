@@ -298,17 +298,19 @@ __device__ __forceinline__ void transpose_reduce(float (&v)[V], int lane) {
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
+  constexpr int BM = FB_BM, SB = BN + 4, SA = BM + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
+  constexpr int AQ = BM * K / 4 / FB_THREADS;  // float4 chunks per thread of an A tile
   using CM = ColMap<BN>;
   constexpr int W4 = CM::W4, NQ = CM::NQ, LPJ = K / W4;
   constexpr int NR = RP < 8 ? RP : 8;   // rows of one node inside a warp's 8 rows
   constexpr int NPW = 8 / NR;           // nodes (or node halves) per warp
   constexpr int V = NR * NL;            // values per lane per column group before reduction
   static_assert(V % LPJ == 0 && V >= LPJ, "epilogue reduction shape");
+  static_assert(AQ >= 1, "A tile too small");
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
-  float* As0 = Bs + K * SB;              // [2][BM][K]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * K);
+  float* As0 = Bs + K * SB;              // [2][K][SA]  A tiles, transposed (k-major rows of m)
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * K * SA);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
@@ -325,45 +327,65 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
 
+  // A tile: global -> registers (prefetch) -> shared, transposed
+  auto lda = [&](int tb, int nn, float4* ra) {
+#pragma unroll
+    for (int q = 0; q < AQ; ++q) {
+      const int idx = threadIdx.x + FB_THREADS * q;
+      const int m = idx % BM, c4 = idx / BM, j = m / RP;
+      ra[q] = j < nn ? __ldg(reinterpret_cast<const float4*>(a.Abase + s_aoff[tb + j] + (m - j * RP) * K + c4 * 4))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto sta = [&](float* At, const float4* ra) {
+#pragma unroll
+    for (int q = 0; q < AQ; ++q) {
+      const int idx = threadIdx.x + FB_THREADS * q;
+      const int m = idx % BM, c4 = idx / BM;
+      At[(c4 * 4 + 0) * SA + m] = ra[q].x;
+      At[(c4 * 4 + 1) * SA + m] = ra[q].y;
+      At[(c4 * 4 + 2) * SA + m] = ra[q].z;
+      At[(c4 * 4 + 3) * SA + m] = ra[q].w;
+    }
+  };
+
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
   cp_async_commit();
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    load_A_tile<K, RP>(a, 0, min(NPT, nbn), s_aoff, As0);
-    cp_async_commit();
+    {
+      float4 ra[AQ];
+      lda(0, min(NPT, nbn), ra);
+      sta(As0, ra);
+    }
+    cp_async_wait<0>();
     int buf = 0;
     for (int tb = 0; tb < nbn; tb += NPT, buf ^= 1) {
       const int nn = min(NPT, nbn - tb);
-      cp_async_wait<0>();
       __syncthreads();
-      if (tb + NPT < nbn) {  // prefetch the next tile's A under this tile's GEMM
-        load_A_tile<K, RP>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
-        cp_async_commit();
-      }
-      const float* As = As0 + buf * BM * K;
+      const bool has_next = tb + NPT < nbn;
+      float4 ra[AQ];
+      if (has_next) lda(tb + NPT, min(NPT, nbn - tb - NPT), ra);  // in flight under the GEMM
+      const float* As = As0 + buf * K * SA;
       float acc[8][TN];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
-      for (int kk = 0; kk < K; kk += 4) {
-        float4 av[8];
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(As + k * SA + m0);
+        const float4 a1 = *reinterpret_cast<const float4*>(As + k * SA + m0 + 4);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float bv[TN];
+        load_row_frag<BN>(Bs + k * SB, lane, bv);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (m0 + i) * K + kk);
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          float bv[TN];
-          load_row_frag<BN>(Bs + (kk + t) * SB, lane, bv);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
-#pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
-          }
-        }
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
       }
+      if (has_next) sta(As0 + (buf ^ 1) * K * SA, ra);
       // saved P_F for the backward
       if (a.Psave) {
 #pragma unroll
@@ -544,26 +566,40 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
         cp_async_wait<0>();  // slice block + A tile + dC tile
       }
       __syncthreads();
-      // dG_F block += A^T dC
-#pragma unroll 2
-      for (int m = 0; m < BM; ++m) {
-        float av[TK];
-        if constexpr (TK >= 4) {
+      // dG_F block += A^T dC  (operands double-buffered in registers)
+      {
+        auto ldA = [&](int m, float* av) {
+          if constexpr (TK >= 4) {
 #pragma unroll
-          for (int q = 0; q < TK; q += 4) {
-            const float4 t = *reinterpret_cast<const float4*>(As + m * K + warp * TK + q);
-            av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+            for (int q = 0; q < TK; q += 4) {
+              const float4 t = *reinterpret_cast<const float4*>(As + m * K + warp * TK + q);
+              av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < TK; ++q) av[q] = As[m * K + warp * TK + q];
           }
-        } else {
+        };
+        auto fma_tile = [&](const float* av, const float* bv) {
 #pragma unroll
-          for (int q = 0; q < TK; ++q) av[q] = As[m * K + warp * TK + q];
+          for (int i = 0; i < TK; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) gacc[i][j] = fmaf(av[i], bv[j], gacc[i][j]);
+        };
+        float a0[TK], b0[TN], a1[TK], b1[TN];
+        ldA(0, a0);
+        load_row_frag<BN>(Ds, lane, b0);
+#pragma unroll 1
+        for (int m = 0; m < BM; m += 2) {
+          ldA(m + 1, a1);
+          load_row_frag<BN>(Ds + (m + 1) * BN, lane, b1);
+          fma_tile(a0, b0);
+          if (m + 2 < BM) {
+            ldA(m + 2, a0);
+            load_row_frag<BN>(Ds + (m + 2) * BN, lane, b0);
+          }
+          fma_tile(a1, b1);
         }
-        float bv[TN];
-        load_row_frag<BN>(Ds + m * BN, lane, bv);
-#pragma unroll
-        for (int i = 0; i < TK; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) gacc[i][j] = fmaf(av[i], bv[j], gacc[i][j]);
       }
       // dA = dC . S_block^T  -> per-(node, column block) partials
       {
@@ -573,13 +609,13 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
         for (int i = 0; i < TMA; ++i)
 #pragma unroll
           for (int j = 0; j < TKA; ++j) xacc[i][j] = 0.f;
-#pragma unroll 2
-        for (int n = 0; n < BN; n += 4) {
-          float4 cv[TMA], bv[TKA];
+        auto ldX = [&](int n, float4* cv, float4* bv) {
 #pragma unroll
           for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * BN + n);
 #pragma unroll
           for (int j = 0; j < TKA; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + KG * j) * SB + n);
+        };
+        auto fmaX = [&](const float4* cv, const float4* bv) {
 #pragma unroll
           for (int i = 0; i < TMA; ++i)
 #pragma unroll
@@ -589,6 +625,15 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
               xacc[i][j] = fmaf(cv[i].z, bv[j].z, xacc[i][j]);
               xacc[i][j] = fmaf(cv[i].w, bv[j].w, xacc[i][j]);
             }
+        };
+        float4 c0[TMA], e0[TKA], c1[TMA], e1[TKA];
+        ldX(0, c0, e0);
+#pragma unroll 1
+        for (int n = 0; n < BN; n += 8) {
+          ldX(n + 4, c1, e1);
+          fmaX(c0, e0);
+          if (n + 8 < BN) ldX(n + 8, c0, e0);
+          fmaX(c1, e1);
         }
 #pragma unroll
         for (int i = 0; i < TMA; ++i) {
@@ -609,30 +654,45 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       // W_u = C_u^T dY_u (this column block's share): one warp per ID, lane
       // owns WPL consecutive (r, jl) entries
       const int fA = s_pref[tb], fB = s_pref[tb + nn];
+      constexpr int RPL = K >= 32 ? K / 32 : 1;  // rank rows per lane
       for (int f = fA + warp; f < fB; f += FB_THREADS / 32) {
         const int j = find_node(s_pref, tb, tb + nn, f) - tb;
         const int u = s_cs0[tb + j] + (f - s_pref[tb + j]);
         const float* Yp = a.dY + (int64_t)u * npad;
-        float wv[WPL];
+        const int r0 = lane * RPL;
+        if (r0 < K) {
+          float wv[RPL][NL];
 #pragma unroll
-        for (int e = 0; e < WPL; ++e) wv[e] = 0.f;
-        const int e0 = lane * WPL;
+          for (int i = 0; i < RPL; ++i)
 #pragma unroll
-        for (int ar = 0; ar < RP; ++ar)
+            for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
 #pragma unroll
-          for (int jf = 0; jf < BNJ; ++jf) {
-            const float* crow = Cs + (j * RP + ar) * BN + jf * K;
-            const float* yrow = Yp + ((int64_t)ar * nF + cb * BNJ + jf) * NL;
+          for (int ar = 0; ar < RP; ++ar)
 #pragma unroll
-            for (int e = 0; e < WPL; ++e) {
-              const int ee = e0 + e, r = ee / NL, jl = ee - r * NL;
-              if (ee < WE) wv[e] = fmaf(crow[r], __ldg(yrow + jl), wv[e]);
+            for (int jf = 0; jf < BNJ; ++jf) {
+              const float* crow = Cs + (j * RP + ar) * BN + jf * K + r0;
+              const float* yrow = Yp + ((int64_t)ar * nF + cb * BNJ + jf) * NL;
+              float yv[NL], cv[RPL];
+#pragma unroll
+              for (int l4 = 0; l4 < NL; l4 += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
+                yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+              }
+#pragma unroll
+              for (int i = 0; i < RPL; ++i) cv[i] = crow[i];
+#pragma unroll
+              for (int i = 0; i < RPL; ++i)
+#pragma unroll
+                for (int jl = 0; jl < NL; ++jl) wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
             }
-          }
-        float* wdst = a.W + ((int64_t)u * a.ncb + cb) * WE;
+          float* wdst = a.W + ((int64_t)u * a.ncb + cb) * WE + r0 * NL;
 #pragma unroll
-        for (int e = 0; e < WPL; ++e)
-          if (e0 + e < WE) wdst[e0 + e] = wv[e];
+          for (int i = 0; i < RPL; ++i)
+#pragma unroll
+            for (int l4 = 0; l4 < NL; l4 += 4)
+              *reinterpret_cast<float4*>(wdst + i * NL + l4) =
+                  make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
+        }
       }
       __syncthreads();
     }
@@ -730,8 +790,7 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 // sweep64, sweep128.
 #define TT_FUSED_SHAPES(X) \
   X(64, 256, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 256, 4, 8) X(128, 128, 4, 8)
-#define TT_FUSED_FWD_SHAPES(X) \
-  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8)
+#define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
 #define TT_SHAPE_EQ(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && NL == nl_) return true;
@@ -768,13 +827,13 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->nF = (int)c.n[F];
   s->BNj = (int)(BN / K);
   s->OUT = (int)(RP * (BN / K) * NL);
-  const int BNf = (int)std::min<int64_t>(BN, 128);
+  const int BNf = BN;
   s->BNf = BNf;
   s->ncbf = (int)(NC / BNf);
   s->BNjf = (int)(BNf / K);
   const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  s->smem_fwd = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints;
+  s->smem_fwd = sizeof(float) * (K * SBf + 2 * K * (FB_BM + 4)) + ints;
   s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
