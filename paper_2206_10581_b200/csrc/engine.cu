@@ -412,13 +412,13 @@ WideShape wide_shape(const DevCfg& c, int k) {
   FusedShape& f = w.f;
   f.ok = 1; f.F = k; f.K = (int)K; f.NC = (int)NC; f.RP = (int)RP; f.NL = nl; f.nF = (int)c.n[k];
   f.BN = BN; f.ncb = (int)(NC / BN); f.BNj = BN / (int)K; f.OUT = 0;
-  f.BNf = BN; f.ncbf = f.ncb; f.BNjf = f.BNj;
+  f.BNf = std::min(BN, 128); f.ncbf = (int)(NC / f.BNf); f.BNjf = f.BNf / (int)K;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  f.smem_fwd = sizeof(float) * (K * (BN + 4) + 2 * K * (FB_BM + 4)) + ints;
+  f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * K * (FB_BM + 4)) + ints;
   f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + 2 * FB_BM * BN) + ints;
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
-#define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;
+#define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && f.BNf == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;
 #define TT_CHECK_B(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && nl == nl_) bwd_ok = true;
   TT_FUSED_FWD_SHAPES(TT_CHECK_F)
   TT_FUSED_SHAPES(TT_CHECK_B)
@@ -465,6 +465,8 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
       const WideShape w = wide_shape(c, k);
       if (w.ok) {
         FusedArgs wa = wide_args(h, k, w.f);
+        wa.ncb = w.f.ncbf;
+        wa.BNj = w.f.BNjf;
         rc = wide_dispatch(h, w.f, true, wa, (int)(c.m[k] * w.f.ncbf), s);
         if (rc) return rc;
         continue;
@@ -481,7 +483,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
   if (rc) return rc;
   if (d_out)
-    LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
+    LAUNCH(k_scatter_heavy, grid_for(h->B * 32, 256, 148 * 16), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);
   return TT_OK;
 }
@@ -496,7 +498,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
          h->seg, h->F.dY, h->F.part, h->st);
   LAUNCH(k_dy_groups, (int)(((chunks + 31) / 32 + 7) / 8), 256, 0, s, (int)h->B, c.npad, h->flag, h->seg, h->F.part,
          h->F.gpart, h->F.dY, h->st);
-  LAUNCH(k_dy_spans, (int)((h->capk[d - 1] + 7) / 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part,
+  LAUNCH(k_dy_spans, grid_for(h->capk[d - 1] * 32, 256, 148 * 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part,
          h->F.gpart, h->F.dY, h->st);
   FusedArgs a = fused_args(h, nullptr);
   a.CH = f.CHB;

@@ -790,7 +790,8 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 // sweep64, sweep128.
 #define TT_FUSED_SHAPES(X) \
   X(64, 256, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 256, 4, 8) X(128, 128, 4, 8)
-#define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
+#define TT_FUSED_FWD_SHAPES(X) \
+  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
 #define TT_SHAPE_EQ(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && NL == nl_) return true;
@@ -827,7 +828,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->nF = (int)c.n[F];
   s->BNj = (int)(BN / K);
   s->OUT = (int)(RP * (BN / K) * NL);
-  const int BNf = BN;
+  const int BNf = (int)std::min<int64_t>(BN, 128);  // 2 CTAs/SM without spills
   s->BNf = BNf;
   s->ncbf = (int)(NC / BNf);
   s->BNjf = (int)(BNf / K);

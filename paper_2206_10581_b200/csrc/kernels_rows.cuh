@@ -50,20 +50,37 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
       acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  for (int i = 0; i < hi - lo; ++i) {
-    const int u = __shfl_sync(0xffffffffu, my_u, i);
+  // rows are loaded PF ahead of their accumulation (memory-level parallelism)
+  constexpr int PF = 4;
+  float4 pre[PF][4];
+  auto load_row = [&](int i, float4* dst) {
     const int p = __shfl_sync(0xffffffffu, my_p, i);
-    if (u != cur) {
-      flush(cur);
-      cur = u;
-    }
     const float* row = up + (int64_t)p * emb;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int64_t c = (int64_t)v * 128 + lane * 4;
-      if (v < nv && c < emb) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(row + c));
-        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+      dst[v] = (v < nv && c < emb) ? __ldg(reinterpret_cast<const float4*>(row + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  const int n = hi - lo;
+#pragma unroll
+  for (int i = 0; i < PF; ++i)
+    if (i < n) load_row(i, pre[i]);
+  for (int i0 = 0; i0 < n; i0 += PF) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int i = i0 + k;
+      if (i < n) {
+        const int u = __shfl_sync(0xffffffffu, my_u, i);
+        if (u != cur) {
+          flush(cur);
+          cur = u;
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          acc[v].x += pre[k][v].x; acc[v].y += pre[k][v].y; acc[v].z += pre[k][v].z; acc[v].w += pre[k][v].w;
+        }
+        if (i + PF < n) load_row(i + PF, pre[k]);
       }
     }
   }
@@ -152,40 +169,42 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
                                                   const DevStatus* st) {
   if (tt_failed(st)) return;
   const int U = ld_count(&counts[d - 1]);
-  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (u >= U) return;
-  const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
-  if (c0 == c1) return;
-  const int G0 = (c0 + 1) / 32, G1 = c1 / 32;
-  if (G0 == G1) return;  // completed by k_dy_groups
-  for (int64_t c = lane * 4; c < npad; c += 128) {
-    float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
-    float4 x = *reinterpret_cast<const float4*>(gpart + ((int64_t)G0 * 2 + 1) * npad + c);
-    acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-    for (int g = G0 + 1; g <= G1; ++g) {
-      x = *reinterpret_cast<const float4*>(gpart + ((int64_t)g * 2) * npad + c);
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
+    if (c0 == c1) continue;
+    const int G0 = (c0 + 1) / 32, G1 = c1 / 32;
+    if (G0 == G1) continue;  // completed by k_dy_groups
+    for (int64_t c = lane * 4; c < npad; c += 128) {
+      float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
+      float4 x = *reinterpret_cast<const float4*>(gpart + ((int64_t)G0 * 2 + 1) * npad + c);
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      for (int g = G0 + 1; g <= G1; ++g) {
+        x = *reinterpret_cast<const float4*>(gpart + ((int64_t)g * 2) * npad + c);
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
+      *reinterpret_cast<float4*>(dY + (int64_t)u * npad + c) = acc;
     }
-    *reinterpret_cast<float4*>(dY + (int64_t)u * npad + c) = acc;
   }
 }
 
-// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS positions)
+// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS
+// positions); one warp per sorted slot (float4 per lane), grid-stride.
 __global__ void __launch_bounds__(256) k_scatter_heavy(int B, int64_t emb, int64_t npad, const int* __restrict__ uid1,
                                                        const int* __restrict__ spos, const int* __restrict__ seg,
                                                        const float* __restrict__ Yu, float* __restrict__ out,
                                                        const DevStatus* st) {
   if (tt_failed(st)) return;
-  const int64_t per = emb / 4;
-  const int64_t total = (int64_t)B * per;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int s = (int)(t / per);
-    const int64_t c = (t - (int64_t)s * per) * 4;
-    const int u = uid1[s] - 1;
-    if (seg[u + 1] - seg[u] <= HEAVY_POS) continue;
-    *reinterpret_cast<float4*>(out + (int64_t)spos[s] * emb + c) =
-        *reinterpret_cast<const float4*>(Yu + (int64_t)u * npad + c);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < B; s += nwarps) {
+    const int u = __ldg(uid1 + s) - 1;
+    if (__ldg(seg + u + 1) - __ldg(seg + u) <= HEAVY_POS) continue;
+    const float* src = Yu + (int64_t)u * npad;
+    float* dst = out + (int64_t)__ldg(spos + s) * emb;
+    for (int64_t c = lane * 4; c < emb; c += 128)
+      *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
   }
 }
 
