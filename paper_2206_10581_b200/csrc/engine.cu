@@ -414,7 +414,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   f.BN = BN; f.ncb = (int)(NC / BN); f.BNj = BN / (int)K; f.OUT = 0;
   f.BNf = std::min(BN, 128); f.ncbf = (int)(NC / f.BNf); f.BNjf = f.BNf / (int)K;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * K * (FB_BM + 4)) + ints;
+  f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints;
   f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + 2 * FB_BM * BN) + ints;
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
@@ -483,7 +483,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
   if (rc) return rc;
   if (d_out)
-    LAUNCH(k_scatter_heavy, grid_for(h->B * 32, 256, 148 * 16), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
+    LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);
   return TT_OK;
 }

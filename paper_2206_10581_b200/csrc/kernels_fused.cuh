@@ -298,19 +298,17 @@ __device__ __forceinline__ void transpose_reduce(float (&v)[V], int lane) {
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
-  constexpr int BM = FB_BM, SB = BN + 4, SA = BM + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
-  constexpr int AQ = BM * K / 4 / FB_THREADS;  // float4 chunks per thread of an A tile
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
   using CM = ColMap<BN>;
   constexpr int W4 = CM::W4, NQ = CM::NQ, LPJ = K / W4;
   constexpr int NR = RP < 8 ? RP : 8;   // rows of one node inside a warp's 8 rows
   constexpr int NPW = 8 / NR;           // nodes (or node halves) per warp
   constexpr int V = NR * NL;            // values per lane per column group before reduction
   static_assert(V % LPJ == 0 && V >= LPJ, "epilogue reduction shape");
-  static_assert(AQ >= 1, "A tile too small");
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
-  float* As0 = Bs + K * SB;              // [2][K][SA]  A tiles, transposed (k-major rows of m)
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * K * SA);
+  float* As0 = Bs + K * SB;              // [2][BM][K]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * K);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
@@ -327,65 +325,45 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
 
-  // A tile: global -> registers (prefetch) -> shared, transposed
-  auto lda = [&](int tb, int nn, float4* ra) {
-#pragma unroll
-    for (int q = 0; q < AQ; ++q) {
-      const int idx = threadIdx.x + FB_THREADS * q;
-      const int m = idx % BM, c4 = idx / BM, j = m / RP;
-      ra[q] = j < nn ? __ldg(reinterpret_cast<const float4*>(a.Abase + s_aoff[tb + j] + (m - j * RP) * K + c4 * 4))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  auto sta = [&](float* At, const float4* ra) {
-#pragma unroll
-    for (int q = 0; q < AQ; ++q) {
-      const int idx = threadIdx.x + FB_THREADS * q;
-      const int m = idx % BM, c4 = idx / BM;
-      At[(c4 * 4 + 0) * SA + m] = ra[q].x;
-      At[(c4 * 4 + 1) * SA + m] = ra[q].y;
-      At[(c4 * 4 + 2) * SA + m] = ra[q].z;
-      At[(c4 * 4 + 3) * SA + m] = ra[q].w;
-    }
-  };
-
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
   cp_async_commit();
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    {
-      float4 ra[AQ];
-      lda(0, min(NPT, nbn), ra);
-      sta(As0, ra);
-    }
-    cp_async_wait<0>();
+    load_A_tile<K, RP>(a, 0, min(NPT, nbn), s_aoff, As0);
+    cp_async_commit();
     int buf = 0;
     for (int tb = 0; tb < nbn; tb += NPT, buf ^= 1) {
       const int nn = min(NPT, nbn - tb);
+      cp_async_wait<0>();
       __syncthreads();
-      const bool has_next = tb + NPT < nbn;
-      float4 ra[AQ];
-      if (has_next) lda(tb + NPT, min(NPT, nbn - tb - NPT), ra);  // in flight under the GEMM
-      const float* As = As0 + buf * K * SA;
+      if (tb + NPT < nbn) {  // prefetch the next tile's A under this tile's GEMM
+        load_A_tile<K, RP>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
+        cp_async_commit();
+      }
+      const float* As = As0 + buf * BM * K;
       float acc[8][TN];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-      for (int k = 0; k < K; ++k) {
-        const float4 a0 = *reinterpret_cast<const float4*>(As + k * SA + m0);
-        const float4 a1 = *reinterpret_cast<const float4*>(As + k * SA + m0 + 4);
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        float bv[TN];
-        load_row_frag<BN>(Bs + k * SB, lane, bv);
+#pragma unroll 2
+      for (int kk = 0; kk < K; kk += 4) {
+        float4 av[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (m0 + i) * K + kk);
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int t = 0; t < 4; ++t) {
+          float bv[TN];
+          load_row_frag<BN>(Bs + (kk + t) * SB, lane, bv);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
+          }
+        }
       }
-      if (has_next) sta(As0 + (buf ^ 1) * K * SA, ra);
       // saved P_F for the backward
       if (a.Psave) {
 #pragma unroll
@@ -834,7 +812,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->BNjf = (int)(BNf / K);
   const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  s->smem_fwd = sizeof(float) * (K * SBf + 2 * K * (FB_BM + 4)) + ints;
+  s->smem_fwd = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints;
   s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;

@@ -50,37 +50,20 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
       acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  // rows are loaded PF ahead of their accumulation (memory-level parallelism)
-  constexpr int PF = 4;
-  float4 pre[PF][4];
-  auto load_row = [&](int i, float4* dst) {
+  for (int i = 0; i < hi - lo; ++i) {
+    const int u = __shfl_sync(0xffffffffu, my_u, i);
     const int p = __shfl_sync(0xffffffffu, my_p, i);
+    if (u != cur) {
+      flush(cur);
+      cur = u;
+    }
     const float* row = up + (int64_t)p * emb;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int64_t c = (int64_t)v * 128 + lane * 4;
-      dst[v] = (v < nv && c < emb) ? __ldg(reinterpret_cast<const float4*>(row + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  const int n = hi - lo;
-#pragma unroll
-  for (int i = 0; i < PF; ++i)
-    if (i < n) load_row(i, pre[i]);
-  for (int i0 = 0; i0 < n; i0 += PF) {
-#pragma unroll
-    for (int k = 0; k < PF; ++k) {
-      const int i = i0 + k;
-      if (i < n) {
-        const int u = __shfl_sync(0xffffffffu, my_u, i);
-        if (u != cur) {
-          flush(cur);
-          cur = u;
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          acc[v].x += pre[k][v].x; acc[v].y += pre[k][v].y; acc[v].z += pre[k][v].z; acc[v].w += pre[k][v].w;
-        }
-        if (i + PF < n) load_row(i + PF, pre[k]);
+      if (v < nv && c < emb) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(row + c));
+        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
       }
     }
   }
@@ -189,22 +172,21 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
   }
 }
 
-// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS
-// positions); one warp per sorted slot (float4 per lane), grid-stride.
+// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS positions)
 __global__ void __launch_bounds__(256) k_scatter_heavy(int B, int64_t emb, int64_t npad, const int* __restrict__ uid1,
                                                        const int* __restrict__ spos, const int* __restrict__ seg,
                                                        const float* __restrict__ Yu, float* __restrict__ out,
                                                        const DevStatus* st) {
   if (tt_failed(st)) return;
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < B; s += nwarps) {
-    const int u = __ldg(uid1 + s) - 1;
-    if (__ldg(seg + u + 1) - __ldg(seg + u) <= HEAVY_POS) continue;
-    const float* src = Yu + (int64_t)u * npad;
-    float* dst = out + (int64_t)__ldg(spos + s) * emb;
-    for (int64_t c = lane * 4; c < emb; c += 128)
-      *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+  const int64_t per = emb / 4;
+  const int64_t total = (int64_t)B * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / per);
+    const int64_t c = (t - (int64_t)s * per) * 4;
+    const int u = uid1[s] - 1;
+    if (seg[u + 1] - seg[u] <= HEAVY_POS) continue;
+    *reinterpret_cast<float4*>(out + (int64_t)spos[s] * emb + c) =
+        *reinterpret_cast<const float4*>(Yu + (int64_t)u * npad + c);
   }
 }
 
