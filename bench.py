@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=0, help="rows per CPU-baseline step (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--graph", type=int, default=1, help="replay the step as one CUDA graph (1) or launch eagerly (0)")
     return p.parse_args()
 
 
@@ -202,12 +203,34 @@ def main():
     out = torch.empty((B, cfg.emb_dim), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
-    def step():
+    def step_eager():
         emb.forward(idx, out)
         emb.backward(up)
         if dp:
             dp.allreduce()
         emb.step()
+
+    step = step_eager
+    graph = None
+    if a.graph and world == 1:
+        # capture forward + backward + update once (after a warm-up that sizes
+        # every buffer) and replay it: one launch per step instead of ~60
+        emb.snapshot_cores()
+        step_eager()
+        torch.cuda.synchronize()
+        emb.sync()
+        emb.restore_cores()
+        s_cap = torch.cuda.Stream(device=dev)
+        s_cap.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_cap):
+            with torch.cuda.graph(graph, stream=s_cap):
+                step_eager()
+        torch.cuda.current_stream(dev).wait_stream(s_cap)
+        torch.cuda.synchronize()
+
+        def step():
+            graph.replay()
 
     # Every timed step starts from the same cores (restored outside the
     # timed events, like the L2 flush): repeated SGD steps on one fixed batch
@@ -229,6 +252,8 @@ def main():
     sampler.start()
     time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    emb.profile_read()  # drop warm-up records
+    emb.set_profiling(True)
     l0 = emb.launch_count()
     for i in range(a.steps):
         emb.restore_cores()
@@ -238,6 +263,8 @@ def main():
         ev[i][1].record()
     torch.cuda.synchronize()
     launches = emb.launch_count() - l0
+    emb.set_profiling(False)
+    prof = emb.profile_read()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -252,16 +279,28 @@ def main():
     value = Bg * a.steps / (t_max / 1e3)
     ms_per_step = t_max / a.steps
 
-    # roofline: algorithmic FLOPs of this rank's step over the device time
+    # roofline of the dominant kernel: its algorithmic FLOPs per launch over its
+    # average launch duration, timed live with CUDA events on its stream
     flops = algorithmic_flops(cfg, U)
     peak = E.ffma_peak_tflops(local, 8192)
-    achieved = flops / (ms_per_step * 1e-3) / 1e12
+    peak_gemm = E.ffma_outer_tflops(local, 4096)
+    costs = level_costs(cfg)
+    fused = emb.last_path() == "fused"
+    last2 = U[-2] * costs[-2] + U[-1] * costs[-1] if len(costs) >= 2 else U[-1] * costs[-1]
+    phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+    if fused:
+        dom = "k_fused_bwd" if phase_ms["bwd_main"] >= phase_ms["fwd_main"] else "k_fused_fwd"
+        dom_flops = (4.0 if dom == "k_fused_bwd" else 2.0) * last2
+        dom_ms = phase_ms["bwd_main" if dom == "k_fused_bwd" else "fwd_main"]
+    else:
+        dom, dom_flops, dom_ms = "whole step (generic path)", flops, ms_per_step
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    prof_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_file):
         try:
-            traffic = json.load(open(prof)).get(name)
-        except (OSError, ValueError):
+            traffic = json.load(open(prof_file)).get(name, {}).get(dom)
+        except (OSError, ValueError, AttributeError):
             traffic = None
 
     # e2e through the C-ABI with pinned host buffers (H2D inputs, D2H output rows)
@@ -317,13 +356,18 @@ def main():
             "config": {"workload": name, "global_batch": Bg, "num_nodes": cfg.num_nodes, "row_factors": cfg.m,
                        "col_factors": cfg.n, "ranks": cfg.R, "optimizer": WORKLOADS[name]["opt"],
                        "parallelism": f"dp{world}", "path": emb.last_path(),
+                       "cuda_graph": graph is not None,
                        "l2": "256 MB buffer written between timed steps (outside the events)",
                        "cores": "restored from a device snapshot before every step (outside the events)",
                        "unique_per_level_rank0": U},
-            "roofline": {"bound": "fp32", "kernel": "whole step", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
-                         "flops_per_step": flops,
-                         "peak_source": "FFMA microbenchmark (tt_ffma_peak_tflops) on this GPU, this run"},
+            "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
+                         "flops_per_launch": dom_flops, "ms_per_launch": dom_ms,
+                         "peak_source": "FFMA microbenchmark (tt_ffma_peak_tflops) on this GPU, this run",
+                         "gemm_shaped_ffma_tflops": peak_gemm,
+                         "step_flops": flops, "step_tflops": flops / (ms_per_step * 1e-3) / 1e12,
+                         "step_frac": flops / (ms_per_step * 1e-3) / 1e12 / peak if peak > 0 else None},
+            "phases_ms_per_step": phase_ms,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "ms_per_step_each": per_step,
         }

@@ -149,6 +149,12 @@ int64_t tt_plan_digits(tt_engine* h, int64_t* ids_out, int32_t* digits_out, int6
 /* The last planned batch's stable sort: keys (IDs) ascending and their batch
  * positions (ties in position order); returns B.  Synchronises. */
 int64_t tt_plan_sorted(tt_engine* h, int64_t* keys_out, int32_t* pos_out, int64_t cap);
+/* Per-phase device timing with CUDA events recorded on the launching stream:
+ * slot 0 plan (K1+K2), 1 forward main kernel(s), 2 backward main kernel(s),
+ * 3 backward auxiliary kernels, 4 update (K5).  tt_profile_read synchronises
+ * and returns total milliseconds and event-pair counts per slot, then resets. */
+int tt_set_profiling(tt_engine* h, int on);
+int tt_profile_read(tt_engine* h, double* ms, int64_t* counts, int nslots);
 /* Kernel launches issued by this handle since creation. */
 int64_t tt_launch_count(tt_engine* h);
 /* Selects the kernel family: 0 = auto (fused fast path where the shapes
@@ -165,6 +171,9 @@ const char* tt_last_error(void);
 /* FP32 FFMA throughput microbenchmark (the roofline denominator): runs
  * `iters` dependent-chain FFMA loops on every SM and returns TFLOP/s. */
 double tt_ffma_peak_tflops(int device, int iters);
+/* The same with GEMM-shaped 3-register FFMAs (8x8 register outer product per
+ * thread): the FFMA rate an SGEMM-style micro-kernel can reach. */
+double tt_ffma_outer_tflops(int device, int iters);
 
 #ifdef __cplusplus
 }

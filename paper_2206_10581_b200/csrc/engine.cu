@@ -109,6 +109,11 @@ struct tt_engine {
   float* st_out = nullptr;
   float* st_up = nullptr;
 
+  // profiling (tt_set_profiling): event pairs per slot
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[8];
+  std::vector<cudaEvent_t> ev_pool;
+
   // bookkeeping
   bool plan_valid = false;
   int64_t cores_version = 0, plan_version = -1;
@@ -121,6 +126,38 @@ struct tt_engine {
 };
 
 namespace {
+
+cudaEvent_t ev_get(tt_engine* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII phase timer: records a start/stop event pair on `s` when profiling
+struct Phase {
+  tt_engine* h;
+  int slot;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  Phase(tt_engine* h_, int slot_, cudaStream_t s_) : h(h_), slot(slot_), s(s_) {
+    if (h->profiling) {
+      a = ev_get(h);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Phase() {
+    if (a) {
+      cudaEvent_t b = ev_get(h);
+      cudaEventRecord(b, s);
+      h->prof_ev[slot].push_back({a, b});
+    }
+  }
+};
 
 void free_plan(tt_engine* h) {
   void* ptrs[] = {h->keys_a, h->keys_b, h->uniq, h->pos_a, h->pos_b, h->hist, h->flag, h->seg,
@@ -236,6 +273,7 @@ __global__ void k_reset_status(DevStatus* st, int which) {
 int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   int rc = ensure_plan(h, B);
   if (rc) return rc;
+  Phase ph(h, 0, s);
   const DevCfg& c = h->dc;
   const int d = c.d;
   const int64_t cap = h->cap;
@@ -480,7 +518,10 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   a.CH = f.CHF;
   a.ncb = f.ncbf;
   a.BNj = f.BNjf;
-  rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
+  {
+    Phase ph(h, 1, s);
+    rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
+  }
   if (rc) return rc;
   if (d_out)
     LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
@@ -503,8 +544,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   FusedArgs a = fused_args(h, nullptr);
   a.CH = f.CHB;
   a.mode = 0;
-  int rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
+  int rc;
+  {
+    Phase ph(h, 2, s);
+    rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
+  }
   if (rc) return rc;
+  Phase ph_aux(h, 3, s);
   const int WE = f.K * f.NL;
   LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], 256, 0, s, c, f.ncb, WE,
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
@@ -762,6 +808,9 @@ void tt_engine_destroy(tt_engine* h) {
   cudaSetDevice(h->device);
   if (h->own) cudaStreamSynchronize(h->own);
   free_plan(h);
+  for (auto& v : h->prof_ev)
+    for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
   for (void* p : ptrs) cudaFree(p);
   if (h->own) cudaStreamDestroy(h->own);
@@ -921,6 +970,7 @@ int tt_step(tt_engine* h, void* stream) {
   CU(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const DevCfg& c = h->dc;
+  Phase ph(h, 4, s);
   LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 2);
   bool vec4 = true;
   for (int k = 0; k < c.d; ++k) vec4 = vec4 && c.core_off[k] % 4 == 0 && c.slice[k] % 4 == 0;
@@ -1088,6 +1138,32 @@ int64_t tt_plan_sorted(tt_engine* h, int64_t* keys, int32_t* pos, int64_t capn) 
 
 int64_t tt_launch_count(tt_engine* h) { return h ? h->launches : -1; }
 
+int tt_set_profiling(tt_engine* h, int on) {
+  if (!h) return fail(TT_ERR_ARG, "tt_set_profiling: null handle");
+  h->profiling = on != 0;
+  return TT_OK;
+}
+
+int tt_profile_read(tt_engine* h, double* ms, int64_t* counts, int nslots) {
+  if (!h || !ms || !counts) return fail(TT_ERR_ARG, "tt_profile_read: null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  for (int k = 0; k < nslots && k < 8; ++k) {
+    double t = 0;
+    for (auto& pr : h->prof_ev[k]) {
+      float x = 0;
+      cudaEventElapsedTime(&x, pr.first, pr.second);
+      t += x;
+      h->ev_pool.push_back(pr.first);
+      h->ev_pool.push_back(pr.second);
+    }
+    ms[k] = t;
+    counts[k] = (int64_t)h->prof_ev[k].size();
+    h->prof_ev[k].clear();
+  }
+  return TT_OK;
+}
+
 int tt_set_path(tt_engine* h, int path) {
   if (!h || path < 0 || path > 1) return fail(TT_ERR_ARG, "tt_set_path: bad argument");
   h->path_pref = path;
@@ -1100,6 +1176,30 @@ int tt_last_path(tt_engine* h) { return h ? h->last_path : -1; }
 int64_t tt_last_error_position(void) { return g_err_pos; }
 int64_t tt_last_error_value(void) { return g_err_val; }
 const char* tt_last_error(void) { return g_err.c_str(); }
+
+double tt_ffma_outer_tflops(int device, int iters) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  cudaMalloc(&out, sizeof(float) * nsm * 8);
+  const int blocks = nsm * 4;
+  k_ffma_outer<<<blocks, 256>>>(out, 16, 1.0f);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_ffma_outer<<<blocks, 256>>>(out, iters, 1.0f);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  const double flops = 2.0 * 64 * (double)iters * 256.0 * blocks;
+  return ms > 0 ? flops / (ms * 1e-3) / 1e12 : -1.0;
+}
 
 double tt_ffma_peak_tflops(int device, int iters) {
   if (cudaSetDevice(device) != cudaSuccess) return -1.0;

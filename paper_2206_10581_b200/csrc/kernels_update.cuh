@@ -142,4 +142,34 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
   if (s == 1234.5f) out[blockIdx.x] = s;
 }
 
+// GEMM-like FFMA microbenchmark: an 8x8 register outer product per thread
+// (3-register FFMAs, operands reused as in an SGEMM micro-kernel).
+__global__ void __launch_bounds__(256) k_ffma_outer(float* out, int iters, float s0) {
+  float a[8], b[8], acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = s0 + threadIdx.x * 0.001f + i;
+    b[i] = s0 - i * 0.5f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a[i] = __int_as_float(__float_as_int(a[i]) ^ 1);
+      b[i] = __int_as_float(__float_as_int(b[i]) ^ 2);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += acc[i][j];
+  if (s == 1234.5f) out[blockIdx.x] = s;
+}
+
 }  // namespace tt

@@ -55,8 +55,8 @@ SYMBOLS = [
     "tt_set_cores_f32", "tt_get_cores_f64", "tt_get_cores_f32", "tt_opt_init", "tt_opt_get_step", "tt_forward",
     "tt_backward", "tt_step", "tt_sync", "tt_lookup_batch", "tt_backward_lookup", "tt_apply_update",
     "tt_train_step_host", "tt_get_core_grads_f64", "tt_set_core_grads_f64", "tt_grad_buffer", "tt_set_dense_grads", "tt_bind_grad_buffer",
-    "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_path", "tt_last_path",
-    "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops",
+    "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
+    "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
 ]
 
 
@@ -88,9 +88,11 @@ def load_library(build_if_missing: bool = True):
         "tt_cores_snapshot": (i32, [vp, vp]), "tt_cores_restore": (i32, [vp, vp]),
         "tt_plan_stats": (i32, [vp, vp]), "tt_plan_digits": (i64, [vp, vp, vp, i64]),
         "tt_plan_sorted": (i64, [vp, vp, vp, i64]), "tt_launch_count": (i64, [vp]),
+        "tt_set_profiling": (i32, [vp, i32]), "tt_profile_read": (i32, [vp, vp, vp, i32]),
         "tt_set_path": (i32, [vp, i32]), "tt_last_path": (i32, [vp]),
         "tt_last_error_position": (i64, []), "tt_last_error_value": (i64, []),
         "tt_last_error": (C.c_char_p, []), "tt_ffma_peak_tflops": (dbl, [i32, i32]),
+        "tt_ffma_outer_tflops": (dbl, [i32, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -358,6 +360,18 @@ class TTEmbedding:
                 return keys[:B], pos[:B]
             cap = int(B)
 
+    PHASES = ("plan", "fwd_main", "bwd_main", "bwd_aux", "update")
+
+    def set_profiling(self, on: bool) -> None:
+        _raise(self._lib.tt_set_profiling(self._h, 1 if on else 0), "tt_set_profiling")
+
+    def profile_read(self):
+        """{phase: (total ms, event pairs)} since the last read (synchronises)."""
+        ms = np.zeros(len(self.PHASES), np.float64)
+        n = np.zeros(len(self.PHASES), np.int64)
+        _raise(self._lib.tt_profile_read(self._h, ms.ctypes.data, n.ctypes.data, len(self.PHASES)), "tt_profile_read")
+        return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(self.PHASES)}
+
     def launch_count(self) -> int:
         return int(self._lib.tt_launch_count(self._h))
 
@@ -419,3 +433,7 @@ def apply_update(emb: TTEmbedding, grads: CoreGradients, opt: OptimizerState) ->
 
 def ffma_peak_tflops(device: int = 0, iters: int = 4096) -> float:
     return float(load_library().tt_ffma_peak_tflops(device, iters))
+
+
+def ffma_outer_tflops(device: int = 0, iters: int = 4096) -> float:
+    return float(load_library().tt_ffma_outer_tflops(device, iters))
