@@ -223,9 +223,11 @@ def main():
         s_cap = torch.cuda.Stream(device=dev)
         s_cap.wait_stream(torch.cuda.current_stream(dev))
         graph = torch.cuda.CUDAGraph()
+        n0 = emb.launch_count()
         with torch.cuda.stream(s_cap):
             with torch.cuda.graph(graph, stream=s_cap):
                 step_eager()
+        graph_kernels = emb.launch_count() - n0
         torch.cuda.current_stream(dev).wait_stream(s_cap)
         torch.cuda.synchronize()
 
@@ -253,7 +255,7 @@ def main():
     time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     emb.profile_read()  # drop warm-up records
-    emb.set_profiling(True)
+    emb.set_profiling(graph is None)
     l0 = emb.launch_count()
     for i in range(a.steps):
         emb.restore_cores()
@@ -263,6 +265,8 @@ def main():
         ev[i][1].record()
     torch.cuda.synchronize()
     launches = emb.launch_count() - l0
+    if graph is not None:
+        launches = graph_kernels * a.steps  # kernels replayed from the captured graph
     emb.set_profiling(False)
     prof = emb.profile_read()
     if world > 1:
@@ -278,6 +282,18 @@ def main():
     t_max = float(tt.item())
     value = Bg * a.steps / (t_max / 1e3)
     ms_per_step = t_max / a.steps
+
+    if graph is not None:
+        # per-phase kernel timing needs the eager launches (events on the
+        # launching stream): the same K steps once more, eagerly
+        emb.set_profiling(True)
+        for i in range(a.steps):
+            emb.restore_cores()
+            flush.zero_()
+            step_eager()
+        torch.cuda.synchronize()
+        emb.set_profiling(False)
+        prof = emb.profile_read()
 
     # roofline of the dominant kernel: its algorithmic FLOPs per launch over its
     # average launch duration, timed live with CUDA events on its stream
