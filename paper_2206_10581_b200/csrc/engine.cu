@@ -359,7 +359,7 @@ int ensure_fused(tt_engine* h) {
   free_fused(b);
   CU(dalloc(&b.Psave, nodes * f.RP * f.NC));
   CU(dalloc(&b.dPc, nodes * f.ncb * f.RP * f.K));
-  CU(dalloc(&b.W, ids * f.ncb * f.K * f.NL));
+  CU(dalloc(&b.W, ids * f.K * f.NL));
   CU(dalloc(&b.dY, ids * c.npad));
   CU(dalloc(&b.Yu, ids * c.npad));
   CU(dalloc(&b.part, chunks * 2 * c.npad));
@@ -440,7 +440,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   int BN = 0;
   if (K == 16 && NC % 64 == 0) BN = 64;
   if (K == 32 && NC % 128 == 0) BN = 128;
-  if (K == 64 && NC % 256 == 0) BN = 256;
+  if (K == 64 && NC % 128 == 0) BN = 128;
   if (K == 128 && NC % 128 == 0) BN = 128;
   if (!BN || RP > FB_BM || FB_BM % RP || c.R[k + 1] != K) return w;
   int nl = 0;
@@ -453,7 +453,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   f.BNf = std::min(BN, 128); f.ncbf = (int)(NC / f.BNf); f.BNjf = f.BNf / (int)K;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
   f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints;
-  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + 2 * FB_BM * BN) + ints;
+  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * BN) + ints;
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
 #define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && f.BNf == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;
@@ -552,7 +552,16 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   if (rc) return rc;
   Phase ph_aux(h, 3, s);
   const int WE = f.K * f.NL;
-  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], 256, 0, s, c, f.ncb, WE,
+#define TT_W_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
+    LAUNCH((k_fused_w<k_, nl_>), grid_for(h->capk[d - 1] * 32, 256, 148 * 16), 256, 0, s, a, h->counts, \
+           h->parent + (d - 1) * cap); \
+  }
+  if (false) {
+  }
+  TT_FUSED_SHAPES(TT_W_CASE)
+#undef TT_W_CASE
+  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], 256, 0, s, c, 1, WE,
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
   const int per = f.RP * f.K;
   float* dst = f.F == 1 ? h->grads : h->L.dP[f.F - 1];

@@ -57,7 +57,7 @@ struct FusedShape {
 
 struct FusedBufs {
   float* Psave = nullptr;  // [capk[F]][RP][NC]
-  float* W = nullptr;      // [capk[d-1]][ncb][K*NL]
+  float* W = nullptr;      // [capk[d-1]][K*NL]
   float* dPc = nullptr;    // [capk[F]][ncb][RP*K]
   float* dY = nullptr;     // [capk[d-1]][npad]   upstream summed per distinct ID
   float* Yu = nullptr;     // [capk[d-1]][npad]   rows of heavy IDs
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
-__global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
+__global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fused_bwd(FusedArgs a) {
   constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP;
   constexpr int WE = K * NL;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
@@ -440,8 +440,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;               // [K][SB]
   float* As = Bs + K * SB;        // [BM][K]
-  float* Cs = As + BM * K;        // [BM][BN]  saved C (for W)
-  float* Ds = Cs + BM * BN;       // [BM][BN]  dC
+  float* Ds = As + BM * K;        // [BM][BN]  dC
   int64_t* s_aoff = reinterpret_cast<int64_t*>(Ds + BM * BN);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
@@ -474,16 +473,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
     for (int tb = 0; tb < nbn; tb += NPT) {
       const int nn = min(NPT, nbn - tb);
       load_A_tile<K, RP>(a, tb, nn, s_aoff, As);
-      cp_async_commit();
-      // mode 0: saved C tile (for W, used last); mode 1: the materialised dC tile
-      const float* csrc = a.mode == 0 ? a.Psave : a.dPin;
-      float* cdst = a.mode == 0 ? Cs : Ds;
-      for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
-        const int m = i / (BN / 4), q = i - m * (BN / 4);
-        const int j = m / RP;
-        float* dst = cdst + m * BN + q * 4;
-        if (j < nn) cp_async16(dst, csrc + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
-        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.mode == 1) {  // the materialised dC tile
+        for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
+          const int m = i / (BN / 4), q = i - m * (BN / 4);
+          const int j = m / RP;
+          float* dst = Ds + m * BN + q * 4;
+          if (j < nn) cp_async16(dst, a.dPin + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
+          else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       cp_async_commit();
       if (a.mode == 0) {
@@ -539,7 +536,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
-      cp_async_wait<1>();  // slice block + A tile landed (C may still be in flight)
+      cp_async_wait<0>();  // slice block + A tile landed
       } else {
         cp_async_wait<0>();  // slice block + A tile + dC tile
       }
@@ -623,55 +620,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
           for (int jj = 0; jj < TKA; ++jj) dst[kg + KG * jj] = xacc[i][jj];
         }
       }
-      if (a.mode == 1) {
-        __syncthreads();
-        continue;
-      }
-      cp_async_wait<0>();  // saved C tile
-      __syncthreads();
-      // W_u = C_u^T dY_u (this column block's share): one warp per ID, lane
-      // owns WPL consecutive (r, jl) entries
-      const int fA = s_pref[tb], fB = s_pref[tb + nn];
-      constexpr int RPL = K >= 32 ? K / 32 : 1;  // rank rows per lane
-      for (int f = fA + warp; f < fB; f += FB_THREADS / 32) {
-        const int j = find_node(s_pref, tb, tb + nn, f) - tb;
-        const int u = s_cs0[tb + j] + (f - s_pref[tb + j]);
-        const float* Yp = a.dY + (int64_t)u * npad;
-        const int r0 = lane * RPL;
-        if (r0 < K) {
-          float wv[RPL][NL];
-#pragma unroll
-          for (int i = 0; i < RPL; ++i)
-#pragma unroll
-            for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
-#pragma unroll
-          for (int ar = 0; ar < RP; ++ar)
-#pragma unroll
-            for (int jf = 0; jf < BNJ; ++jf) {
-              const float* crow = Cs + (j * RP + ar) * BN + jf * K + r0;
-              const float* yrow = Yp + ((int64_t)ar * nF + cb * BNJ + jf) * NL;
-              float yv[NL], cv[RPL];
-#pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
-                yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
-              }
-#pragma unroll
-              for (int i = 0; i < RPL; ++i) cv[i] = crow[i];
-#pragma unroll
-              for (int i = 0; i < RPL; ++i)
-#pragma unroll
-                for (int jl = 0; jl < NL; ++jl) wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
-            }
-          float* wdst = a.W + ((int64_t)u * a.ncb + cb) * WE + r0 * NL;
-#pragma unroll
-          for (int i = 0; i < RPL; ++i)
-#pragma unroll
-            for (int l4 = 0; l4 < NL; l4 += 4)
-              *reinterpret_cast<float4*>(wdst + i * NL + l4) =
-                  make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
-        }
-      }
       __syncthreads();
     }
   }
@@ -679,6 +627,65 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_fused_bwd(FusedArgs a) {
   float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
 #pragma unroll
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
+}
+
+// W_u = P_F[prefix(u)]^T dY_u over all NC columns (K x n_d per distinct ID):
+// the last core's gradient contributions, streamed from the saved P_F.  One
+// warp per ID (grid-stride), lane owns RPL rank rows x NL columns.
+template <int K, int NL>
+__global__ void __launch_bounds__(256) k_fused_w(FusedArgs a, const int* __restrict__ counts,
+                                                 const int* __restrict__ parentL) {
+  if (tt_failed(a.st)) return;
+  constexpr int RPL = K >= 32 ? K / 32 : 1;
+  const int U = ld_count(&counts[a.c.d - 1]);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int r0 = lane * RPL;
+  const int RP = a.RP, nF = a.nF;
+  const int64_t npad = a.c.npad;
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    const int p = __ldg(parentL + u);
+    const float* Cp = a.Psave + (int64_t)p * RP * a.NC;
+    const float* Yp = a.dY + (int64_t)u * npad;
+    float wv[RPL][NL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i)
+#pragma unroll
+      for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
+    if (r0 < K) {
+#pragma unroll 4
+      for (int q = 0; q < RP * nF; ++q) {  // q = (ar, jf) = row block of the output
+        const int ar = q / nF, jf = q - ar * nF;
+        const float* crow = Cp + (int64_t)ar * a.NC + jf * K + r0;
+        const float* yrow = Yp + (int64_t)q * NL;
+        float cv[RPL], yv[NL];
+        if constexpr (RPL == 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(crow));
+          cv[0] = x.x; cv[1] = x.y; cv[2] = x.z; cv[3] = x.w;
+        } else if constexpr (RPL == 2) {
+          const float2 x = __ldg(reinterpret_cast<const float2*>(crow));
+          cv[0] = x.x; cv[1] = x.y;
+        } else {
+          cv[0] = __ldg(crow);
+        }
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
+          yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+        }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
+      }
+      float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4)
+          *reinterpret_cast<float4*>(wdst + i * NL + l4) = make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
+    }
+  }
 }
 
 // dG_{d-1}[v] = sum over the digit-v IDs (group order) and column blocks of W.
@@ -767,9 +774,8 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 // FUSED_SWITCH): papers, products / sweep32, small, billion, sweep16,
 // sweep64, sweep128.
 #define TT_FUSED_SHAPES(X) \
-  X(64, 256, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 256, 4, 8) X(128, 128, 4, 8)
-#define TT_FUSED_FWD_SHAPES(X) \
   X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8)
+#define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
 #define TT_SHAPE_EQ(k_, bn_, rp_, nl_) if (K == k_ && BN == bn_ && RP == rp_ && NL == nl_) return true;
@@ -788,8 +794,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   int BN = 0;
   if (K == 16 && NC % 64 == 0) BN = 64;
   if (K == 32 && NC % 128 == 0) BN = 128;
-  if (K == 64 && NC % 256 == 0) BN = 256;
-  if (K == 64 && !BN && NC % 128 == 0) BN = 128;
+  if (K == 64 && NC % 128 == 0) BN = 128;
   if (K == 128 && NC % 128 == 0) BN = 128;
   if (!BN || !fused_shape_compiled((int)K, BN, (int)RP, (int)NL)) return false;
   if (c.emb_dim % 4 || c.npad % 4 || c.npad > 512) return false;
@@ -813,7 +818,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
   s->smem_fwd = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints;
-  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + 2 * FB_BM * BN) + ints;
+  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * BN) + ints;
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
   s->CHF = s->CHB = 0;
