@@ -194,7 +194,7 @@ int ensure_plan(tt_engine* h, int64_t B) {
   CU(dalloc(&h->uniq, cap));
   CU(dalloc(&h->pos_a, cap));
   CU(dalloc(&h->pos_b, cap));
-  CU(dalloc(&h->hist, ntiles * RS_MAXBINS));
+  CU(dalloc(&h->hist, ntiles * RS_MAXBINS + RS_MAXBINS));
   CU(dalloc(&h->flag, cap));
   CU(dalloc(&h->seg, cap + 1));
   CU(dalloc(&h->lflags, (int64_t)d * cap));
@@ -243,11 +243,23 @@ K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, cons
   const int passes = (nbits + RS_MAXBITS - 1) / RS_MAXBITS;
   K* kin = ka; K* kout = kb;
   int* vin = va; int* vo = vb;
+  int* tot = h->hist + (int64_t)ntiles * RS_MAXBINS;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rs_scatter<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)RS_SCATTER_SMEM);
+    cudaFuncSetAttribute(k_rs_scatter<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SCATTER_SMEM);
+    attr_set = true;
+  }
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (nbits - shift + (passes - p) - 1) / (passes - p);  // split evenly
+    const int bins = 1 << bits;
     LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, bits, h->hist);
-    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, 0, s, kin, vin, kout, vo, n_dev, n_host, shift, bits, h->hist);
+    LAUNCH(k_rs_colscan, (bins + 255) / 256, 256, 0, s, h->hist, tot, n_dev, n_host, bits);
+    const size_t smem = sizeof(int) * ((size_t)RS_WARPS * bins + bins + 64);
+    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, smem, s, kin, vin, kout, vo, n_dev, n_host, shift, bits, h->hist,
+           tot);
     std::swap(kin, kout);
     std::swap(vin, vo);
     shift += bits;
@@ -301,17 +313,24 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   LAUNCH(k_digits_copy_u32, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit, h->counts, h->gk[0][0]);
   h->order[0] = h->gv[0][0];
   h->sdig[0] = h->gk[0][0];
-  LAUNCH(k_group_offsets, grid_for(c.m[0] + 1, 256, INT_MAX), 256, 0, s, h->gk[0][0], h->counts, (int)c.m[0],
-         h->goff[0]);
+
   for (int k = 1; k < d; ++k) {
     LAUNCH(k_digits_to_keys, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit + k * cap, h->counts + k, h->gk[k][0],
            h->gv[k][0]);
     const int nb = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.m[k] - 1)));
     h->sdig[k] = radix_sort<unsigned>(h, s, h->gk[k][0], h->gv[k][0], h->gk[k][1], h->gv[k][1], h->counts + k, 0,
                                       h->capk[k], nb, &h->order[k]);
-    LAUNCH(k_group_offsets, grid_for(c.m[k] + 1, 256, INT_MAX), 256, 0, s, h->sdig[k], h->counts + k, (int)c.m[k],
-           h->goff[k]);
+
   }
+  GroupOffArgs ga{};
+  int64_t mmax = 0;
+  for (int k = 0; k < d; ++k) {
+    ga.sdig[k] = h->sdig[k];
+    ga.goff[k] = h->goff[k];
+    ga.m[k] = (int)c.m[k];
+    mmax = std::max<int64_t>(mmax, c.m[k]);
+  }
+  LAUNCH(k_group_offsets_all, dim3(grid_for(mmax + 1, 256, INT_MAX), d), 256, 0, s, ga, h->counts);
   return TT_OK;
 }
 

@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(256) k_fused_w(FusedArgs a, const int* __restr
 #pragma unroll
       for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
     if (r0 < K) {
-#pragma unroll 4
+#pragma unroll 8
       for (int q = 0; q < RP * nF; ++q) {  // q = (ar, jf) = row block of the output
         const int ar = q / nF, jf = q - ar * nF;
         const float* crow = Cp + (int64_t)ar * a.NC + jf * K + r0;

@@ -30,17 +30,18 @@ __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B,
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of (key, int value) pairs, up to 10-bit digits per
-// pass, two kernels per pass: per-tile digit histograms, then a scatter whose
-// blocks derive their own global offsets from the histograms (column prefix
-// over earlier tiles + exclusive scan of the digit totals -- redundant per
-// block, L2-resident) and rank keys stably with warp match_any peers.
+// Stable LSD radix sort of (key, int value) pairs, up to 11-bit digits per
+// pass and three kernels per pass: per-tile digit histograms; a column scan
+// (one thread per digit) turning them into per-tile exclusive offsets plus
+// digit totals; a scatter whose blocks scan the digit totals, rank their keys
+// stably with warp match_any peers and write.  Counts stay on the device.
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_PER_WARP = 512;
 constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;  // 4096 keys per tile
-constexpr int RS_MAXBITS = 10;
+constexpr int RS_MAXBITS = 11;
 constexpr int RS_MAXBINS = 1 << RS_MAXBITS;
+constexpr size_t RS_SCATTER_SMEM = sizeof(int) * ((size_t)RS_WARPS * RS_MAXBINS + RS_MAXBINS + 64);
 
 __device__ __forceinline__ int rs_count(const int* n_dev, int n_host) { return n_dev ? ld_count(n_dev) : n_host; }
 
@@ -50,62 +51,72 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
                                                         int shift, int nbits, int* __restrict__ hist) {
   __shared__ int cnt[RS_MAXBINS];
   const int n = rs_count(n_dev, n_host);
+  const int base = blockIdx.x * RS_TILE;
+  if (base >= n) return;
   const int bins = 1 << nbits;
   const unsigned mask = bins - 1;
   for (int i = threadIdx.x; i < bins; i += RS_THREADS) cnt[i] = 0;
   __syncthreads();
-  const int base = blockIdx.x * RS_TILE;
-  if (base < n) {
-    for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
-      const int g = base + i;
-      if (g < n) atomicAdd(&cnt[(int)((keys[g] >> shift) & mask)], 1);
-    }
+  for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
+    const int g = base + i;
+    if (g < n) atomicAdd(&cnt[(int)((keys[g] >> shift) & mask)], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < bins; i += RS_THREADS) hist[blockIdx.x * bins + i] = cnt[i];
+}
+
+// hist[t][d] <- sum_{t' < t} hist[t'][d];  tot[d] = sum_t hist[t][d]
+__global__ void __launch_bounds__(256) k_rs_colscan(int* __restrict__ hist, int* __restrict__ tot, const int* n_dev,
+                                                    int n_host, int nbits) {
+  const int bins = 1 << nbits;
+  const int dgt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (dgt >= bins) return;
+  const int n = rs_count(n_dev, n_host);
+  const int ntiles = (n + RS_TILE - 1) / RS_TILE;
+  int run = 0, t = 0;
+  for (; t + 8 <= ntiles; t += 8) {
+    int h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = hist[(t + i) * bins + dgt];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hist[(t + i) * bins + dgt] = run;
+      run += h[i];
+    }
+  }
+  for (; t < ntiles; ++t) {
+    const int h = hist[t * bins + dgt];
+    hist[t * bins + dgt] = run;
+    run += h;
+  }
+  tot[dgt] = run;
 }
 
 template <class K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const int* __restrict__ vin,
                                                            K* __restrict__ kout, int* __restrict__ vout,
                                                            const int* n_dev, int n_host, int shift, int nbits,
-                                                           const int* __restrict__ hist) {
-  __shared__ int cnt[RS_WARPS][RS_MAXBINS];
-  __shared__ int base[RS_MAXBINS];
-  __shared__ int wsum[RS_WARPS];
+                                                           const int* __restrict__ colpre, const int* __restrict__ tot) {
+  extern __shared__ int rs_smem[];
+  int* cnt = rs_smem;                            // [RS_WARPS][bins]
+  const int bins = 1 << nbits;
+  int* base = cnt + RS_WARPS * bins;             // [bins]
+  int* wsum = base + bins;                       // [RS_WARPS]
   const int n = rs_count(n_dev, n_host);
   const int tile = blockIdx.x;
   if (tile * RS_TILE >= n) return;
-  const int ntiles = (n + RS_TILE - 1) / RS_TILE;
-  const int bins = 1 << nbits;
   const unsigned mask = bins - 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // global offsets: digit totals (all tiles) and this tile's column prefix
-  constexpr int DPT = RS_MAXBINS / RS_THREADS;  // digits per thread (<= 4)
-  int tot[DPT], pre[DPT];
-#pragma unroll
-  for (int q = 0; q < DPT; ++q) {
-    tot[q] = 0;
-    pre[q] = 0;
-    const int dgt = threadIdx.x * DPT + q;
-    if (dgt < bins) {
-      int t = 0;
-      for (; t + 4 <= ntiles; t += 4) {
-        const int h0 = hist[t * bins + dgt], h1 = hist[(t + 1) * bins + dgt];
-        const int h2 = hist[(t + 2) * bins + dgt], h3 = hist[(t + 3) * bins + dgt];
-        pre[q] += (t < tile ? h0 : 0) + (t + 1 < tile ? h1 : 0) + (t + 2 < tile ? h2 : 0) + (t + 3 < tile ? h3 : 0);
-        tot[q] += h0 + h1 + h2 + h3;
-      }
-      for (; t < ntiles; ++t) {
-        const int h = hist[t * bins + dgt];
-        pre[q] += t < tile ? h : 0;
-        tot[q] += h;
-      }
-    }
-  }
+  // exclusive scan of the digit totals, plus this tile's column prefix
+  constexpr int DPT = RS_MAXBINS / RS_THREADS;  // digits per thread (<= 8)
+  int tv[DPT];
   int my = 0;
 #pragma unroll
-  for (int q = 0; q < DPT; ++q) my += tot[q];
+  for (int q = 0; q < DPT; ++q) {
+    const int dgt = threadIdx.x * DPT + q;
+    tv[q] = dgt < bins ? tot[dgt] : 0;
+    my += tv[q];
+  }
   int x = my;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -113,16 +124,15 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     if (lane >= o) x += y;
   }
   if (lane == 31) wsum[w] = x;
-  for (int i = threadIdx.x; i < RS_WARPS * RS_MAXBINS; i += RS_THREADS) (&cnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < RS_WARPS * bins; i += RS_THREADS) cnt[i] = 0;
   __syncthreads();
-  int woff = 0;
-  for (int i = 0; i < w; ++i) woff += wsum[i];
-  int run = woff + x - my;
+  int run = x - my;
+  for (int i = 0; i < w; ++i) run += wsum[i];
 #pragma unroll
   for (int q = 0; q < DPT; ++q) {
     const int dgt = threadIdx.x * DPT + q;
-    if (dgt < bins) base[dgt] = run + pre[q];
-    run += tot[q];
+    if (dgt < bins) base[dgt] = run + colpre[tile * bins + dgt];
+    run += tv[q];
   }
   // per-warp digit counts of this tile
   const int wbase = tile * RS_TILE + w * RS_PER_WARP;
@@ -130,7 +140,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     const int g = wbase + r * 32 + lane;
     const int dig = g < n ? (int)((kin[g] >> shift) & mask) : RS_MAXBINS + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
-    if (g < n && lane == 31 - __clz(peers)) cnt[w][dig] += __popc(peers);
+    if (g < n && lane == 31 - __clz(peers)) cnt[w * bins + dig] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
@@ -138,8 +148,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     int rr = base[dgt];
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-      const int c = cnt[ww][dgt];
-      cnt[ww][dgt] = rr;
+      const int c = cnt[ww * bins + dgt];
+      cnt[ww * bins + dgt] = rr;
       rr += c;
     }
   }
@@ -150,12 +160,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     const int dig = g < n ? (int)((key >> shift) & mask) : RS_MAXBINS + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
     if (g < n) {
-      const int dst = cnt[w][dig] + __popc(peers & lanemask_lt());
+      const int dst = cnt[w * bins + dig] + __popc(peers & lanemask_lt());
       kout[dst] = key;
       vout[dst] = vin[g];
     }
     __syncwarp();
-    if (g < n && lane == 31 - __clz(peers)) cnt[w][dig] += __popc(peers);
+    if (g < n && lane == 31 - __clz(peers)) cnt[w * bins + dig] += __popc(peers);
     __syncwarp();
   }
 }
@@ -365,6 +375,27 @@ __global__ void k_digits_to_keys(const int* __restrict__ digit, const int* n_dev
   if (i >= n) return;
   keys[i] = (unsigned)digit[i];
   vals[i] = i;
+}
+
+struct GroupOffArgs {
+  const unsigned* sdig[TT_MAXD];
+  int* goff[TT_MAXD];
+  int m[TT_MAXD];
+};
+
+// all levels at once: blockIdx.y = level
+__global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ counts) {
+  const int k = blockIdx.y;
+  const int n = ld_count(&counts[k]);
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > ga.m[k]) return;
+  const unsigned* sd = ga.sdig[k];
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)sd[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  ga.goff[k][v] = lo;
 }
 
 // goff[v] = first slot whose sorted digit >= v, v in [0, m]
