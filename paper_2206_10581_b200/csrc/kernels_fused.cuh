@@ -631,56 +631,64 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
 
 // W_u = P_F[prefix(u)]^T dY_u over all NC columns (K x n_d per distinct ID):
 // the last core's gradient contributions, streamed from the saved P_F.  One
-// warp per ID (grid-stride), lane owns RPL rank rows x NL columns.
+// warp per ID (grid-stride); each load instruction moves 512 B of a C row:
+// lane l covers rank rows r0..r0+3 of column block jf = jg*JPL + l/(K/4), and
+// the JPL lane groups are combined with a fixed butterfly at the end.
 template <int K, int NL>
 __global__ void __launch_bounds__(256) k_fused_w(FusedArgs a, const int* __restrict__ counts,
                                                  const int* __restrict__ parentL) {
   if (tt_failed(a.st)) return;
-  constexpr int RPL = K >= 32 ? K / 32 : 1;
+  constexpr int LPB = K / 4;        // lanes per column block
+  constexpr int JPL = 32 / LPB;     // column blocks per warp-wide load
+  static_assert(LPB >= 1 && LPB <= 32, "rank shape");
   const int U = ld_count(&counts[a.c.d - 1]);
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int r0 = lane * RPL;
+  const int jfo = lane / LPB, r0 = (lane % LPB) * 4;
   const int RP = a.RP, nF = a.nF;
+  const int ngroups = (nF + JPL - 1) / JPL;
   const int64_t npad = a.c.npad;
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
     const int p = __ldg(parentL + u);
     const float* Cp = a.Psave + (int64_t)p * RP * a.NC;
     const float* Yp = a.dY + (int64_t)u * npad;
-    float wv[RPL][NL];
+    float wv[4][NL];
 #pragma unroll
-    for (int i = 0; i < RPL; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
-    if (r0 < K) {
+    const int nq = RP * ngroups;
 #pragma unroll 8
-      for (int q = 0; q < RP * nF; ++q) {  // q = (ar, jf) = row block of the output
-        const int ar = q / nF, jf = q - ar * nF;
-        const float* crow = Cp + (int64_t)ar * a.NC + jf * K + r0;
-        const float* yrow = Yp + (int64_t)q * NL;
-        float cv[RPL], yv[NL];
-        if constexpr (RPL == 4) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(crow));
-          cv[0] = x.x; cv[1] = x.y; cv[2] = x.z; cv[3] = x.w;
-        } else if constexpr (RPL == 2) {
-          const float2 x = __ldg(reinterpret_cast<const float2*>(crow));
-          cv[0] = x.x; cv[1] = x.y;
-        } else {
-          cv[0] = __ldg(crow);
-        }
+    for (int q = 0; q < nq; ++q) {
+      const int ar = q / ngroups, jf = (q - ar * ngroups) * JPL + jfo;
+      if (jf < nF) {
+        const float4 cv = __ldg(reinterpret_cast<const float4*>(Cp + (int64_t)ar * a.NC + jf * K + r0));
+        const float* yrow = Yp + ((int64_t)ar * nF + jf) * NL;
+        float yv[NL];
 #pragma unroll
         for (int l4 = 0; l4 < NL; l4 += 4) {
           const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
           yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
         }
 #pragma unroll
-        for (int i = 0; i < RPL; ++i)
-#pragma unroll
-          for (int jl = 0; jl < NL; ++jl) wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
+        for (int jl = 0; jl < NL; ++jl) {
+          wv[0][jl] = fmaf(cv.x, yv[jl], wv[0][jl]);
+          wv[1][jl] = fmaf(cv.y, yv[jl], wv[1][jl]);
+          wv[2][jl] = fmaf(cv.z, yv[jl], wv[2][jl]);
+          wv[3][jl] = fmaf(cv.w, yv[jl], wv[3][jl]);
+        }
       }
+    }
+#pragma unroll
+    for (int off = LPB; off < 32; off <<= 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jl = 0; jl < NL; ++jl) wv[i][jl] += __shfl_xor_sync(0xffffffffu, wv[i][jl], off);
+    if (jfo == 0) {
       float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
 #pragma unroll
-      for (int i = 0; i < RPL; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int l4 = 0; l4 < NL; l4 += 4)
           *reinterpret_cast<float4*>(wdst + i * NL + l4) = make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
