@@ -157,10 +157,11 @@ int tt_set_profiling(tt_engine* h, int on);
 int tt_profile_read(tt_engine* h, double* ms, int64_t* counts, int nslots);
 /* Kernel launches issued by this handle since creation. */
 int64_t tt_launch_count(tt_engine* h);
-/* Selects the kernel family: 0 = auto (fused fast path where the shapes
- * allow), 1 = generic path only. */
+/* Selects the kernel family: 0 = auto (fused FFMA fast path where the shapes
+ * allow), 1 = generic path only, 2 = fused with the optional tensor-core
+ * 3xTF32 contraction where compiled for the shape (reported separately). */
 int tt_set_path(tt_engine* h, int path);
-/* Which path the last forward used (0 generic, 1 fused). */
+/* Which path the last forward used (0 generic, 1 fused FFMA, 2 fused 3xTF32). */
 int tt_last_path(tt_engine* h);
 /* Batch position (TT_ERR_INDEX) or core (TT_ERR_NONFINITE) of the last error. */
 int64_t tt_last_error_position(void);

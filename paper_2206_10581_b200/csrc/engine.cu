@@ -19,6 +19,7 @@
 #include "kernels_generic.cuh"
 #include "kernels_plan.cuh"
 #include "kernels_rows.cuh"
+#include "kernels_tc.cuh"
 #include "kernels_update.cuh"
 
 using namespace tt;
@@ -539,7 +540,14 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   a.BNj = f.BNjf;
   {
     Phase ph(h, 1, s);
-    rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
+    if (h->path_pref == 2 && f.K == 64 && f.BNf == 128 && f.RP == 4 && f.NL == 4) {
+      const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
+      const size_t smem = sizeof(float) * (2 * 64 * (128 + 4) + 2 * FB_BM * (64 + 4)) + ints;
+      FUSED_LAUNCH((k_fused_fwd_tc<64, 128, 4, 4>), smem, (int)(c.m[f.F] * f.ncbf), s, a);
+      h->last_path = 2;
+    } else {
+      rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
+    }
   }
   if (rc) return rc;
   if (d_out)
@@ -623,15 +631,15 @@ void touch_counters(tt_engine* h, cudaStream_t s) {
     LAUNCH(k_touch_counters, grid_for(c.m[k], 256, INT_MAX), 256, 0, s, c, k, h->goff[k], h->grads, 0, h->st);
 }
 
-bool use_fused(tt_engine* h) { return h->path_pref == 0 && h->fused_ok; }
+bool use_fused(tt_engine* h) { return h->path_pref != 1 && h->fused_ok; }
 
 int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cudaStream_t s, bool write_out) {
   LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 1);
   int rc = build_plan(h, d_idx, B, s);
   if (rc) return rc;
   if (use_fused(h)) {
-    rc = fused_forward(h, write_out ? d_out : nullptr, s);
     h->last_path = 1;
+    rc = fused_forward(h, write_out ? d_out : nullptr, s);
   } else {
     rc = gen_forward(h, write_out ? d_out : nullptr, s);
     h->last_path = 0;
@@ -646,7 +654,7 @@ int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cuda
 int do_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   if (h->dense) CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
   int rc;
-  if (h->last_path == 1)
+  if (h->last_path >= 1)
     rc = fused_backward(h, d_up, s);
   else
     rc = gen_backward(h, d_up, s);
@@ -1193,7 +1201,7 @@ int tt_profile_read(tt_engine* h, double* ms, int64_t* counts, int nslots) {
 }
 
 int tt_set_path(tt_engine* h, int path) {
-  if (!h || path < 0 || path > 1) return fail(TT_ERR_ARG, "tt_set_path: bad argument");
+  if (!h || path < 0 || path > 2) return fail(TT_ERR_ARG, "tt_set_path: bad argument");
   h->path_pref = path;
   h->plan_valid = false;
   return TT_OK;

@@ -91,7 +91,7 @@ def test_plan_bit_exact(name):
     assert emb.plan_stats() == oracle.prefix_counts(cfg, idx)
 
 
-@pytest.mark.parametrize("path", ["generic", "auto"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tf32x3"])
 @pytest.mark.parametrize("name", list(SHAPES))
 def test_forward_parity(name, path):
     import torch
@@ -113,7 +113,7 @@ def test_forward_parity(name, path):
     np.testing.assert_array_equal(one, out[:3])
 
 
-@pytest.mark.parametrize("path", ["generic", "auto"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tf32x3"])
 @pytest.mark.parametrize("name", list(SHAPES))
 def test_backward_parity(name, path):
     import torch
