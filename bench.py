@@ -301,7 +301,7 @@ def main():
     peak = E.ffma_peak_tflops(local, 8192)
     peak_gemm = E.ffma_outer_tflops(local, 4096)
     costs = level_costs(cfg)
-    fused = emb.last_path() == "fused"
+    fused = emb.last_path().startswith("fused")
     last2 = U[-2] * costs[-2] + U[-1] * costs[-1] if len(costs) >= 2 else U[-1] * costs[-1]
     phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
     if fused:

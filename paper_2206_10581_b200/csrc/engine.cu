@@ -472,7 +472,8 @@ WideShape wide_shape(const DevCfg& c, int k) {
   f.BN = BN; f.ncb = (int)(NC / BN); f.BNj = BN / (int)K; f.OUT = 0;
   f.BNf = std::min(BN, 128); f.ncbf = (int)(NC / f.BNf); f.BNjf = f.BNf / (int)K;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints;
+  f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints + sizeof(int) * (3 * FB_IDS + 8) + 16;
+  f.CHF = 0;
   f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * BN) + ints;
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
@@ -523,6 +524,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
       const WideShape w = wide_shape(c, k);
       if (w.ok) {
         FusedArgs wa = wide_args(h, k, w.f);
+        wa.CH = 0;
         wa.ncb = w.f.ncbf;
         wa.BNj = w.f.BNjf;
         rc = wide_dispatch(h, w.f, true, wa, (int)(c.m[k] * w.f.ncbf), s);

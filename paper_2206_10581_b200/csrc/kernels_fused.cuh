@@ -164,6 +164,27 @@ __device__ __forceinline__ void prep_nodes(const FusedArgs& a, int nb0, int nbn,
   __syncthreads();
 }
 
+constexpr int FB_IDS = 512;  // per-batch distinct IDs whose metadata is staged
+
+// digit i_d and slot range of the batch's first FB_IDS distinct IDs (flat
+// index f = position in the batch's ID prefix s_pref).  Ends with a barrier.
+__device__ __forceinline__ void prep_ids(const FusedArgs& a, int nbn, const int* s_cs0, const int* s_pref, int* s_bd,
+                                         int* s_bs0, int* s_bs1) {
+  const int tot = min(s_pref[nbn], FB_IDS);
+  for (int f = threadIdx.x; f < tot; f += FB_THREADS) {
+    int lo = 0, hi = nbn - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
+    }
+    const int u = s_cs0[lo] + (f - s_pref[lo]);
+    s_bd[f] = __ldg(a.digitL + u);
+    s_bs0[f] = __ldg(a.seg + u);
+    s_bs1[f] = __ldg(a.seg + u + 1);
+  }
+  __syncthreads();
+}
+
 // A tile (BM x K, row-major) of batch-local nodes [tb, tb+nn) by cp.async;
 // rows past the tile's nodes are zero-filled.
 template <int K, int RP>
@@ -313,6 +334,11 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
   int* s_wsum = s_pref + FB_NB + 4;
+  // per-ID metadata of the batch (first FB_IDS IDs) and the tile's staged slices
+  int* s_bd = s_wsum + 8;                 // digit i_d
+  int* s_bs0 = s_bd + FB_IDS;             // seg[u]
+  int* s_bs1 = s_bs0 + FB_IDS;            // seg[u+1]
+  float* Gst = reinterpret_cast<float*>(s_bs1 + FB_IDS);  // [CH][K*NL], 16-byte aligned
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
@@ -330,6 +356,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    if (a.out) prep_ids(a, nbn, s_cs0, s_pref, s_bd, s_bs0, s_bs1);
     load_A_tile<K, RP>(a, 0, min(NPT, nbn), s_aoff, As0);
     cp_async_commit();
     int buf = 0;
@@ -339,8 +366,15 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
       __syncthreads();
       if (tb + NPT < nbn) {  // prefetch the next tile's A under this tile's GEMM
         load_A_tile<K, RP>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
-        cp_async_commit();
       }
+      // the tile's last-core slices (first CH IDs) land under the GEMM too
+      const int tfA = s_pref[tb];
+      const int nstage = a.out ? max(0, min(a.CH, min(s_pref[tb + nn], FB_IDS) - tfA)) : 0;
+      for (int i = threadIdx.x; i < nstage * (K * NL / 4); i += FB_THREADS) {
+        const int ci = i / (K * NL / 4), q = i - ci * (K * NL / 4);
+        cp_async16(Gst + ci * K * NL + q * 4, Gl + (int64_t)s_bd[tfA + ci] * sliceL + q * 4);
+      }
+      cp_async_commit();
       const float* As = As0 + buf * BM * K;
       float acc[8][TN];
 #pragma unroll
@@ -374,6 +408,8 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
         }
       }
       if (!a.out) continue;
+      cp_async_wait<0>();  // staged slices (and the next A tile)
+      __syncthreads();
       // last level from the registers: per node of this warp, per distinct ID
 #pragma unroll
       for (int jw = 0; jw < NPW; ++jw) {
@@ -383,8 +419,11 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
         const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
         for (int f = fA; f < fB; ++f) {
           const int u = cs0 + (f - fA);
-          const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
-          const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+          const bool staged = f - tfA < nstage;
+          const bool known = f < FB_IDS;
+          const float* Gp = staged ? Gst + (f - tfA) * K * NL
+                                   : Gl + (int64_t)(known ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
+          const int s0 = known ? s_bs0[f] : __ldg(a.seg + u), s1 = known ? s_bs1[f] : __ldg(a.seg + u + 1);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
             const int colb = CM::col(lane, q);
@@ -394,7 +433,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
             for (int t = 0; t < W4; ++t)
 #pragma unroll
               for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
+                const float4 x = *reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4);
                 gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
               }
             float v[V];
@@ -825,11 +864,16 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->BNjf = (int)(BNf / K);
   const size_t SB = BN + 4, SG = K + 4, SBf = BNf + 4;
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-  s->smem_fwd = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints;
+  const size_t base_f = sizeof(float) * (K * SBf + 2 * FB_BM * K) + ints + sizeof(int) * (3 * FB_IDS + 8) + 16;
+  const size_t half = 113 * 1024;  // keep two forward CTAs per SM
+  const size_t per_id = sizeof(float) * K * NL;
+  s->CHF = (int)std::min<size_t>(32, base_f < half ? (half - base_f) / per_id : 0);
+  if (s->CHF < 1) s->CHF = (int)std::min<size_t>(8, ((size_t)FB_SMEM_MAX - base_f) / per_id);
+  s->smem_fwd = base_f + s->CHF * per_id;
   s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * BN) + ints;
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
-  s->CHF = s->CHB = 0;
+  s->CHB = 0;
   return true;
 }
 
