@@ -536,15 +536,17 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
              h->parent + k * cap, h->digit, h->seg, h->spos, nullptr, h->st);
     }
   }
-  FusedArgs a = fused_args(h, d_out);
-  a.CH = f.CHF;
+  // the fused kernel computes P_F (saved); the last level runs as a streaming
+  // kernel over it (k_last_level), then heavy rows are scattered
+  FusedArgs a = fused_args(h, nullptr);
+  a.CH = 0;
   a.ncb = f.ncbf;
   a.BNj = f.BNjf;
   {
     Phase ph(h, 1, s);
     if (h->path_pref == 2 && f.K == 64 && f.BNf == 128 && f.RP == 4 && f.NL == 4) {
       const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-      const size_t smem = sizeof(float) * (2 * 64 * (128 + 4) + 2 * FB_BM * (64 + 4)) + ints;
+      const size_t smem = sizeof(float) * (2 * 64 * (128 + 4) + 2 * FB_BM * (64 + 4)) + ints;  // Bhl + As
       FUSED_LAUNCH((k_fused_fwd_tc<64, 128, 4, 4>), smem, (int)(c.m[f.F] * f.ncbf), s, a);
       h->last_path = 2;
     } else {
@@ -552,6 +554,20 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     }
   }
   if (rc) return rc;
+  if (d_out) {
+    FusedArgs o = fused_args(h, d_out);
+    const int d = c.d;
+    const int64_t cap = h->cap;
+#define TT_LL_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
+    LAUNCH((k_last_level<k_, nl_>), grid_for(h->capk[d - 1] * 32, 256, 148 * 16), 256, 0, s, o, h->counts, \
+           h->parent + (d - 1) * cap); \
+  }
+    if (false) {
+    }
+    TT_FUSED_SHAPES(TT_LL_CASE)
+#undef TT_LL_CASE
+  }
   if (d_out)
     LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);

@@ -668,6 +668,66 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
 
+// The last level from the saved P_F (forward rows): one warp per distinct ID
+// (grid-stride), lane q owns output row block (ar, jf) = q: out[(q, jl)] =
+// sum_r P_F[prefix][ar][(jf, r)] G_{d-1}[r, i_d, jl] -- K x NL FMAs per lane,
+// no cross-lane reduction, and a row's NL outputs are contiguous so a warp
+// writes 32 x NL x 4 contiguous bytes per batch position.  IDs with more
+// than HEAVY_POS positions go to Yu for k_scatter_heavy.
+template <int K, int NL>
+__global__ void __launch_bounds__(256) k_last_level(FusedArgs a, const int* __restrict__ counts,
+                                                    const int* __restrict__ parentL) {
+  if (tt_failed(a.st)) return;
+  const int U = ld_count(&counts[a.c.d - 1]);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  const int64_t emb = a.c.emb_dim, npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    const int p = __ldg(parentL + u);
+    const float* Cp = a.Psave + (int64_t)p * RP * a.NC;
+    const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
+    const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+    for (int q = lane; q < nrow; q += 32) {
+      const int ar = q / nF, jf = q - ar * nF;
+      const float* crow = Cp + (int64_t)ar * a.NC + jf * K;
+      float o[NL];
+#pragma unroll
+      for (int jl = 0; jl < NL; ++jl) o[jl] = 0.f;
+#pragma unroll 4
+      for (int r = 0; r < K; r += 4) {
+        const float4 c = __ldg(reinterpret_cast<const float4*>(crow + r));
+        const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int l4 = 0; l4 < NL; l4 += 4) {
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(Gp + (r + t) * NL + l4));
+            o[l4] = fmaf(cv[t], gv.x, o[l4]);
+            o[l4 + 1] = fmaf(cv[t], gv.y, o[l4 + 1]);
+            o[l4 + 2] = fmaf(cv[t], gv.z, o[l4 + 2]);
+            o[l4 + 3] = fmaf(cv[t], gv.w, o[l4 + 3]);
+          }
+      }
+      const int64_t col = (int64_t)q * NL;
+      if (s1 - s0 > HEAVY_POS) {
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4)
+          *reinterpret_cast<float4*>(a.Yu + (int64_t)u * npad + col + l4) = make_float4(o[l4], o[l4 + 1], o[l4 + 2], o[l4 + 3]);
+      } else if (col < emb) {
+        for (int s = s0; s < s1; ++s) {
+          float* orow = a.out + (int64_t)__ldg(a.spos + s) * emb + col;
+#pragma unroll
+          for (int l4 = 0; l4 < NL; l4 += 4)
+            *reinterpret_cast<float4*>(orow + l4) = make_float4(o[l4], o[l4 + 1], o[l4 + 2], o[l4 + 3]);
+        }
+      }
+    }
+  }
+}
+
 // W_u = P_F[prefix(u)]^T dY_u over all NC columns (K x n_d per distinct ID):
 // the last core's gradient contributions, streamed from the saved P_F.  One
 // warp per ID (grid-stride); each load instruction moves 512 B of a C row:

@@ -53,12 +53,11 @@ __device__ __forceinline__ void load_A_tile_pad(const FusedArgs& a, int tb, int 
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd_tc(FusedArgs a) {
   static_assert(BN == 2 * K && K % 8 == 0 && RP == 4 && NL == 4, "tensor-core forward: papers-type shape only");
-  constexpr int BM = FB_BM, SB = BN + 4, SA = K + 4, NPT = BM / RP, BNJ = BN / K;
+  constexpr int BM = FB_BM, SB2 = BN + 4, SA = K + 4, NPT = BM / RP, BNJ = BN / K;
   constexpr int NT = K / 8;  // n8 tiles per warp (its K columns)
   extern __shared__ __align__(16) float smem[];
-  float* Bh = smem;                      // [K][SB] hi plane (raw slice block first)
-  float* Bl = Bh + K * SB;               // [K][SB] lo plane
-  float* As0 = Bl + K * SB;              // [2][BM][SA]
+  float2* Bhl = reinterpret_cast<float2*>(smem);   // [K][SB2] (hi, lo) pairs: one LDS.64 per element
+  float* As0 = smem + 2 * K * SB2;                 // [2][BM][SA]
   int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * SA);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
@@ -78,17 +77,18 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd_tc(FusedArgs a) {
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
 
-  load_slice_block<K, BN, SB>(a, g, cb, Bh);
+  // raw slice block -> (A staging area) -> split once into interleaved hi/lo pairs
+  load_slice_block<K, BN, BN>(a, g, cb, As0);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  for (int i = threadIdx.x; i < K * BN; i += FB_THREADS) {  // split the slice block once
+  for (int i = threadIdx.x; i < K * BN; i += FB_THREADS) {
     const int k = i / BN, n = i - k * BN;
     uint32_t hi, lo;
-    split3(Bh[k * SB + n], hi, lo);
-    Bh[k * SB + n] = __uint_as_float(hi);
-    Bl[k * SB + n] = __uint_as_float(lo);
+    split3(As0[i], hi, lo);
+    Bhl[k * SB2 + n] = make_float2(__uint_as_float(hi), __uint_as_float(lo));
   }
+  __syncthreads();
 
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
@@ -120,8 +120,9 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd_tc(FusedArgs a) {
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int n = cn0 + j * 8 + gq;
-          const uint32_t bh0 = __float_as_uint(Bh[(kk + tq) * SB + n]), bh1 = __float_as_uint(Bh[(kk + tq + 4) * SB + n]);
-          const uint32_t bl0 = __float_as_uint(Bl[(kk + tq) * SB + n]), bl1 = __float_as_uint(Bl[(kk + tq + 4) * SB + n]);
+          const float2 p0 = Bhl[(kk + tq) * SB2 + n], p1 = Bhl[(kk + tq + 4) * SB2 + n];
+          const uint32_t bh0 = __float_as_uint(p0.x), bh1 = __float_as_uint(p1.x);
+          const uint32_t bl0 = __float_as_uint(p0.y), bl1 = __float_as_uint(p1.y);
           mma_tf32(acc[j], al, bh0, bh1);
           mma_tf32(acc[j], ah, bl0, bl1);
           mma_tf32(acc[j], ah, bh0, bh1);
