@@ -668,37 +668,53 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
 
-// The last level from the saved P_F (forward rows): one warp per distinct ID
-// (grid-stride), lane q owns output row block (ar, jf) = q: out[(q, jl)] =
-// sum_r P_F[prefix][ar][(jf, r)] G_{d-1}[r, i_d, jl] -- K x NL FMAs per lane,
-// no cross-lane reduction, and a row's NL outputs are contiguous so a warp
-// writes 32 x NL x 4 contiguous bytes per batch position.  IDs with more
-// than HEAVY_POS positions go to Yu for k_scatter_heavy.
+// Streaming kernels over the saved P_F, one warp per distinct ID
+// (grid-stride).  The ID's prefix block P_F[p] (RP x NC floats, contiguous)
+// is staged into the warp's shared buffer with coalesced 16-byte loads (all
+// independent: the whole block is in flight at once), rows padded to K + 4.
+constexpr int SK_WARPS = 8;
+
+template <int K>
+__device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp, int nrow, float* buf, int lane) {
+  const int n4 = nrow * (K / 4);
+#pragma unroll 4
+  for (int i = lane; i < n4; i += 32) {
+    const int row = i / (K / 4), c4 = i - row * (K / 4);
+    *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = __ldg(reinterpret_cast<const float4*>(Cp) + i);
+  }
+  __syncwarp();
+}
+
+// The last level (forward rows): lane q owns output row block (ar, jf) = q:
+// out[(q, jl)] = sum_r P_F[prefix][q][r] G_{d-1}[r, i_d, jl]; a row's NL
+// outputs are contiguous, so a warp writes one contiguous output row per batch
+// position.  IDs with more than HEAVY_POS positions go to Yu (k_scatter_heavy).
 template <int K, int NL>
-__global__ void __launch_bounds__(256) k_last_level(FusedArgs a, const int* __restrict__ counts,
-                                                    const int* __restrict__ parentL) {
+__global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const int* __restrict__ counts,
+                                                              const int* __restrict__ parentL) {
+  extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
   const int U = ld_count(&counts[a.c.d - 1]);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  float* buf = sk_smem + wib * (nrow * (K + 4));
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
     const int p = __ldg(parentL + u);
-    const float* Cp = a.Psave + (int64_t)p * RP * a.NC;
     const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
     const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+    stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
     for (int q = lane; q < nrow; q += 32) {
-      const int ar = q / nF, jf = q - ar * nF;
-      const float* crow = Cp + (int64_t)ar * a.NC + jf * K;
+      const float* crow = buf + q * (K + 4);
       float o[NL];
 #pragma unroll
       for (int jl = 0; jl < NL; ++jl) o[jl] = 0.f;
 #pragma unroll 4
       for (int r = 0; r < K; r += 4) {
-        const float4 c = __ldg(reinterpret_cast<const float4*>(crow + r));
+        const float4 c = *reinterpret_cast<const float4*>(crow + r);
         const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -725,73 +741,59 @@ __global__ void __launch_bounds__(256) k_last_level(FusedArgs a, const int* __re
         }
       }
     }
+    __syncwarp();
   }
 }
 
 // W_u = P_F[prefix(u)]^T dY_u over all NC columns (K x n_d per distinct ID):
-// the last core's gradient contributions, streamed from the saved P_F.  One
-// warp per ID (grid-stride); each load instruction moves 512 B of a C row:
-// lane l covers rank rows r0..r0+3 of column block jf = jg*JPL + l/(K/4), and
-// the JPL lane groups are combined with a fixed butterfly at the end.
+// the last core's gradient contributions.  Lane owns RPL rank rows and sums
+// over the block's nrow rows (no cross-lane reduction).
 template <int K, int NL>
-__global__ void __launch_bounds__(256) k_fused_w(FusedArgs a, const int* __restrict__ counts,
-                                                 const int* __restrict__ parentL) {
+__global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const int* __restrict__ counts,
+                                                           const int* __restrict__ parentL) {
+  extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
-  constexpr int LPB = K / 4;        // lanes per column block
-  constexpr int JPL = 32 / LPB;     // column blocks per warp-wide load
-  static_assert(LPB >= 1 && LPB <= 32, "rank shape");
+  constexpr int RPL = K >= 32 ? K / 32 : 1;
   const int U = ld_count(&counts[a.c.d - 1]);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int jfo = lane / LPB, r0 = (lane % LPB) * 4;
-  const int RP = a.RP, nF = a.nF;
-  const int ngroups = (nF + JPL - 1) / JPL;
+  const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  float* buf = sk_smem + wib * (nrow * (K + 4));
   const int64_t npad = a.c.npad;
+  const int r0 = lane * RPL;
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
     const int p = __ldg(parentL + u);
-    const float* Cp = a.Psave + (int64_t)p * RP * a.NC;
     const float* Yp = a.dY + (int64_t)u * npad;
-    float wv[4][NL];
+    stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    if (r0 < K) {
+      float wv[RPL][NL];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RPL; ++i)
 #pragma unroll
-      for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
-    const int nq = RP * ngroups;
-#pragma unroll 8
-    for (int q = 0; q < nq; ++q) {
-      const int ar = q / ngroups, jf = (q - ar * ngroups) * JPL + jfo;
-      if (jf < nF) {
-        const float4 cv = __ldg(reinterpret_cast<const float4*>(Cp + (int64_t)ar * a.NC + jf * K + r0));
-        const float* yrow = Yp + ((int64_t)ar * nF + jf) * NL;
-        float yv[NL];
+        for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < nrow; ++q) {
+        float yv[NL], cv[RPL];
 #pragma unroll
         for (int l4 = 0; l4 < NL; l4 += 4) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
+          const float4 x = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)q * NL + l4));
           yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
         }
 #pragma unroll
-        for (int jl = 0; jl < NL; ++jl) {
-          wv[0][jl] = fmaf(cv.x, yv[jl], wv[0][jl]);
-          wv[1][jl] = fmaf(cv.y, yv[jl], wv[1][jl]);
-          wv[2][jl] = fmaf(cv.z, yv[jl], wv[2][jl]);
-          wv[3][jl] = fmaf(cv.w, yv[jl], wv[3][jl]);
-        }
+        for (int i = 0; i < RPL; ++i) cv[i] = buf[q * (K + 4) + r0 + i];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
       }
-    }
-#pragma unroll
-    for (int off = LPB; off < 32; off <<= 1)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int jl = 0; jl < NL; ++jl) wv[i][jl] += __shfl_xor_sync(0xffffffffu, wv[i][jl], off);
-    if (jfo == 0) {
       float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RPL; ++i)
 #pragma unroll
         for (int l4 = 0; l4 < NL; l4 += 4)
           *reinterpret_cast<float4*>(wdst + i * NL + l4) = make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
     }
+    __syncwarp();
   }
 }
 
