@@ -677,10 +677,22 @@ constexpr int SK_WARPS = 8;
 template <int K>
 __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp, int nrow, float* buf, int lane) {
   const int n4 = nrow * (K / 4);
-#pragma unroll 4
-  for (int i = lane; i < n4; i += 32) {
-    const int row = i / (K / 4), c4 = i - row * (K / 4);
-    *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = __ldg(reinterpret_cast<const float4*>(Cp) + i);
+  constexpr int B8 = 8;  // 8 independent 16-byte loads in flight per lane
+  for (int i0 = 0; i0 < n4; i0 += 32 * B8) {
+    float4 v[B8];
+#pragma unroll
+    for (int b = 0; b < B8; ++b) {
+      const int i = i0 + b * 32 + lane;
+      if (i < n4) v[b] = __ldg(reinterpret_cast<const float4*>(Cp) + i);
+    }
+#pragma unroll
+    for (int b = 0; b < B8; ++b) {
+      const int i = i0 + b * 32 + lane;
+      if (i < n4) {
+        const int row = i / (K / 4), c4 = i - row * (K / 4);
+        *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = v[b];
+      }
+    }
   }
   __syncwarp();
 }
@@ -698,15 +710,19 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int RP = a.RP, nF = a.nF, nrow = RP * nF;
-  float* buf = sk_smem + wib * (nrow * (K + 4));
+  float* buf = sk_smem + wib * (nrow * (K + 4) + K * NL);
+  float* Gs = buf + nrow * (K + 4);
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
     const int p = __ldg(parentL + u);
-    const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
+    const float* Gsrc = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
     const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+    for (int i = lane; i < K * NL / 4; i += 32)
+      reinterpret_cast<float4*>(Gs)[i] = __ldg(reinterpret_cast<const float4*>(Gsrc) + i);
     stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    const float* Gp = Gs;
     for (int q = lane; q < nrow; q += 32) {
       const float* crow = buf + q * (K + 4);
       float o[NL];
@@ -720,7 +736,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const
         for (int t = 0; t < 4; ++t)
 #pragma unroll
           for (int l4 = 0; l4 < NL; l4 += 4) {
-            const float4 gv = __ldg(reinterpret_cast<const float4*>(Gp + (r + t) * NL + l4));
+            const float4 gv = *reinterpret_cast<const float4*>(Gp + (r + t) * NL + l4);
             o[l4] = fmaf(cv[t], gv.x, o[l4]);
             o[l4 + 1] = fmaf(cv[t], gv.y, o[l4 + 1]);
             o[l4 + 2] = fmaf(cv[t], gv.z, o[l4 + 2]);
@@ -758,12 +774,15 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const in
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int RP = a.RP, nF = a.nF, nrow = RP * nF;
-  float* buf = sk_smem + wib * (nrow * (K + 4));
+  float* buf = sk_smem + wib * (nrow * (K + 4) + nrow * NL);
+  float* Ys = buf + nrow * (K + 4);
   const int64_t npad = a.c.npad;
   const int r0 = lane * RPL;
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
     const int p = __ldg(parentL + u);
     const float* Yp = a.dY + (int64_t)u * npad;
+    for (int i = lane; i < nrow * NL / 4; i += 32)
+      reinterpret_cast<float4*>(Ys)[i] = __ldg(reinterpret_cast<const float4*>(Yp) + i);
     stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
     if (r0 < K) {
       float wv[RPL][NL];
@@ -776,7 +795,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const in
         float yv[NL], cv[RPL];
 #pragma unroll
         for (int l4 = 0; l4 < NL; l4 += 4) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)q * NL + l4));
+          const float4 x = *reinterpret_cast<const float4*>(Ys + q * NL + l4);
           yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
         }
 #pragma unroll

@@ -37,8 +37,8 @@ __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B,
 // stably with warp match_any peers and write.  Counts stay on the device.
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_PER_WARP = 512;
-constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;  // 4096 keys per tile
+constexpr int RS_PER_WARP = 128;
+constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;  // 1024 keys per tile (>= 148 tiles at B = 256k)
 constexpr int RS_MAXBITS = 11;
 constexpr int RS_MAXBINS = 1 << RS_MAXBITS;
 constexpr size_t RS_SCATTER_SMEM = sizeof(int) * ((size_t)RS_WARPS * RS_MAXBINS + RS_MAXBINS + 64);
