@@ -302,11 +302,15 @@ def main():
     peak_gemm = E.ffma_outer_tflops(local, 4096)
     costs = level_costs(cfg)
     fused = emb.last_path().startswith("fused")
-    last2 = U[-2] * costs[-2] + U[-1] * costs[-1] if len(costs) >= 2 else U[-1] * costs[-1]
+    # algorithmic FLOPs of the fused kernels (the last level's forward and W
+    # run in the streaming kernels k_last_level / k_fused_w):
+    #   k_fused_fwd = 2 U_F c_F;  k_fused_bwd = 4 U_F c_F (dG_F, dA) + 2 U_d c_d (dC pass)
+    uf_cf = U[-2] * costs[-2] if len(costs) >= 2 else 0
+    ud_cd = U[-1] * costs[-1]
     phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
     if fused:
         dom = "k_fused_bwd" if phase_ms["bwd_main"] >= phase_ms["fwd_main"] else "k_fused_fwd"
-        dom_flops = (4.0 if dom == "k_fused_bwd" else 2.0) * last2
+        dom_flops = (4.0 * uf_cf + 2.0 * ud_cd) if dom == "k_fused_bwd" else 2.0 * uf_cf
         dom_ms = phase_ms["bwd_main" if dom == "k_fused_bwd" else "fwd_main"]
     else:
         dom, dom_flops, dom_ms = "whole step (generic path)", flops, ms_per_step
