@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="papers")
     p.add_argument("--seed", type=int, default=2026)
-    p.add_argument("--path", default="auto", choices=["auto", "generic", "tf32x3"])
+    p.add_argument("--path", default="auto", choices=["auto", "generic", "tc"])
     p.add_argument("--cpu-sample", type=int, default=0, help="rows per CPU-baseline step (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")

@@ -113,7 +113,9 @@ int tt_backward_lookup(tt_engine* h, const int64_t* h_indices, int64_t batch,
 int tt_apply_update(tt_engine* h);
 /* One training step through host memory: upload indices and upstream,
  * forward (result copied to h_out, may be NULL), backward on the saved plan,
- * update.  Returns after the step has completed. */
+ * update.  The upstream upload runs on its own copy stream under the plan and
+ * forward, and the row download under the backward and update (pinned host
+ * buffers make both asynchronous).  Returns after the step has completed. */
 int tt_train_step_host(tt_engine* h, const int64_t* h_indices, int64_t batch,
                        const float* h_upstream, float* h_out);
 

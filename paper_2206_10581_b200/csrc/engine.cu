@@ -19,7 +19,7 @@
 #include "kernels_generic.cuh"
 #include "kernels_plan.cuh"
 #include "kernels_rows.cuh"
-#include "kernels_tc.cuh"
+#include "kernels_tcgen05.cuh"
 #include "kernels_update.cuh"
 
 using namespace tt;
@@ -109,6 +109,10 @@ struct tt_engine {
   int64_t* st_idx = nullptr;
   float* st_out = nullptr;
   float* st_up = nullptr;
+  // host-entry copy streams: the upstream upload overlaps the plan + forward,
+  // the row download overlaps the backward + update
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_fwd = nullptr, ev_in = nullptr;
 
   // profiling (tt_set_profiling): event pairs per slot
   bool profiling = false;
@@ -124,6 +128,8 @@ struct tt_engine {
   int last_path = 0;
   bool fused_ok = false;
   FusedShape fs{};
+  bool tc_ok = false;  // tensor-core (tcgen05) kernels exist for this shape
+  TcShape ts{};
 };
 
 namespace {
@@ -511,6 +517,8 @@ int wide_dispatch(tt_engine* h, const FusedShape& f, bool fwd, const FusedArgs& 
   return rc;
 }
 
+bool use_tc(tt_engine* h);
+
 int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   const DevCfg& c = h->dc;
   const FusedShape& f = h->fs;
@@ -544,10 +552,15 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   a.BNj = f.BNjf;
   {
     Phase ph(h, 1, s);
-    if (h->path_pref == 2 && f.K == 64 && f.BNf == 128 && f.RP == 4 && f.NL == 4) {
-      const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
-      const size_t smem = sizeof(float) * (2 * 64 * (128 + 4) + 2 * FB_BM * (64 + 4)) + ints;  // Bhl + As
-      FUSED_LAUNCH((k_fused_fwd_tc<64, 128, 4, 4>), smem, (int)(c.m[f.F] * f.ncbf), s, a);
+    if (use_tc(h)) {
+      a.ncb = h->ts.ncbf;
+      const int grid = (int)(c.m[f.F] * h->ts.ncbf);
+      if (false) {
+      }
+#define TT_TC_FWD_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_tc_fwd<k_, bn_, rp_>), h->ts.smem_fwd, grid, s, a);
+      TT_TC_SHAPES(TT_TC_FWD_CASE)
+#undef TT_TC_FWD_CASE
       h->last_path = 2;
     } else {
       rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
@@ -593,7 +606,19 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   int rc;
   {
     Phase ph(h, 2, s);
-    rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
+    if (h->last_path == 2) {
+      a.ncb = h->ts.ncbb;
+      const int grid = (int)(c.m[f.F] * h->ts.ncbb);
+      rc = TT_OK;
+      if (false) {
+      }
+#define TT_TC_BWD_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, s, a);
+      TT_TC_SHAPES(TT_TC_BWD_CASE)
+#undef TT_TC_BWD_CASE
+    } else {
+      rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
+    }
   }
   if (rc) return rc;
   Phase ph_aux(h, 3, s);
@@ -652,6 +677,7 @@ void touch_counters(tt_engine* h, cudaStream_t s) {
 }
 
 bool use_fused(tt_engine* h) { return h->path_pref != 1 && h->fused_ok; }
+bool use_tc(tt_engine* h) { return h->path_pref == 2 && h->tc_ok; }
 
 int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cudaStream_t s, bool write_out) {
   LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 1);
@@ -854,6 +880,7 @@ int tt_engine_create(const tt_config_c* cfg, int device, tt_engine** out) {
   cudaMemcpy(h->st, &st0, sizeof(st0), cudaMemcpyHostToDevice);
   h->fused_ok = fused_plan_shape(h->dc, &h->fs) &&
                 h->fs.smem_bwd <= 227 * 1024 && h->fs.smem_fwd <= 227 * 1024;
+  h->tc_ok = h->fused_ok && tc_plan_shape(h->fs, &h->ts);
   if (cudaGetLastError() != cudaSuccess) return cleanup(fail(TT_ERR_CUDA, "tt_engine_create: CUDA error"));
   *out = h;
   return TT_OK;
@@ -870,6 +897,10 @@ void tt_engine_destroy(tt_engine* h) {
   void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
   for (void* p : ptrs) cudaFree(p);
   if (h->own) cudaStreamDestroy(h->own);
+  if (h->s_h2d) { cudaStreamSynchronize(h->s_h2d); cudaStreamDestroy(h->s_h2d); }
+  if (h->s_d2h) { cudaStreamSynchronize(h->s_d2h); cudaStreamDestroy(h->s_d2h); }
+  for (cudaEvent_t e : {h->ev_up, h->ev_fwd, h->ev_in})
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 
@@ -1107,16 +1138,35 @@ int tt_train_step_host(tt_engine* h, const int64_t* h_idx, int64_t B, const floa
   CU(cudaSetDevice(h->device));
   int rc = ensure_stage(h, B);
   if (rc) return rc;
+  if (!h->s_h2d) {
+    CU(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  }
   cudaStream_t s = h->own;
+  const size_t rows = sizeof(float) * (size_t)B * (size_t)h->dc.emb_dim;
+  // the compute stream's previous work (and any earlier reader of st_up /
+  // st_out) is ordered before this step's copies
+  CU(cudaEventRecord(h->ev_in, s));
+  CU(cudaStreamWaitEvent(h->s_h2d, h->ev_in, 0));
+  CU(cudaMemcpyAsync(h->st_up, h_up, rows, cudaMemcpyHostToDevice, h->s_h2d));  // under plan + forward
+  CU(cudaEventRecord(h->ev_up, h->s_h2d));
   CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(h->st_up, h_up, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyHostToDevice, s));
   rc = tt_forward(h, h->st_idx, B, h->st_out, s);
   if (rc) return rc;
-  if (h_out) CU(cudaMemcpyAsync(h_out, h->st_out, sizeof(float) * B * h->dc.emb_dim, cudaMemcpyDeviceToHost, s));
+  if (h_out) {  // rows go back under the backward + update
+    CU(cudaEventRecord(h->ev_fwd, s));
+    CU(cudaStreamWaitEvent(h->s_d2h, h->ev_fwd, 0));
+    CU(cudaMemcpyAsync(h_out, h->st_out, rows, cudaMemcpyDeviceToHost, h->s_d2h));
+  }
+  CU(cudaStreamWaitEvent(s, h->ev_up, 0));
   rc = tt_backward(h, nullptr, B, h->st_up, s);
   if (rc) return rc;
   rc = tt_step(h, s);
   if (rc) return rc;
+  CU(cudaStreamSynchronize(h->s_d2h));
   return read_status(h, s);
 }
 

@@ -326,10 +326,10 @@ class TTEmbedding:
         _raise(self._lib.tt_set_dense_grads(self._h, 1 if on else 0), "tt_set_dense_grads")
 
     def set_path(self, path: str) -> None:
-        _raise(self._lib.tt_set_path(self._h, {"auto": 0, "generic": 1, "tf32x3": 2}[path]), "tt_set_path")
+        _raise(self._lib.tt_set_path(self._h, {"auto": 0, "generic": 1, "tc": 2}[path]), "tt_set_path")
 
     def last_path(self) -> str:
-        return ["generic", "fused", "fused-tf32x3"][self._lib.tt_last_path(self._h)]
+        return ["generic", "fused", "fused-tc"][self._lib.tt_last_path(self._h)]
 
     def plan_stats(self) -> List[int]:
         out = np.zeros(self.config.d, np.int64)

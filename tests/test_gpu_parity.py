@@ -72,6 +72,10 @@ SHAPES = {
 }
 
 
+# shapes with tcgen05 kernels (rank >= 32, 128-column blocks)
+TC_SHAPES = ("products", "papers", "billion")
+
+
 @pytest.mark.parametrize("name", list(SHAPES))
 def test_plan_bit_exact(name):
     mk, B, dist = SHAPES[name]
@@ -91,7 +95,7 @@ def test_plan_bit_exact(name):
     assert emb.plan_stats() == oracle.prefix_counts(cfg, idx)
 
 
-@pytest.mark.parametrize("path", ["generic", "auto", "tf32x3"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tc"])
 @pytest.mark.parametrize("name", list(SHAPES))
 def test_forward_parity(name, path):
     import torch
@@ -101,6 +105,8 @@ def test_forward_parity(name, path):
     idx = ids_for(cfg, 4, B, dist)
     out = emb.forward(torch.tensor(idx, device="cuda")).cpu().numpy()
     emb.sync()
+    if path == "tc" and name in TC_SHAPES:
+        assert emb.last_path() == "fused-tc"  # the tcgen05 kernels ran, not the FFMA ones
     ref, bad = oracle.lookup_batch(cfg, cores, idx, 0)
     aref, _ = oracle.lookup_batch(cfg, abs_cores(cores), idx, 0)
     assert bad == -1
@@ -113,7 +119,7 @@ def test_forward_parity(name, path):
     np.testing.assert_array_equal(one, out[:3])
 
 
-@pytest.mark.parametrize("path", ["generic", "auto", "tf32x3"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tc"])
 @pytest.mark.parametrize("name", list(SHAPES))
 def test_backward_parity(name, path):
     import torch
