@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -424,12 +425,13 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
   return a;
 }
 
-#define FUSED_LAUNCH(KER, SMEM, GRID, S, ARGS)                                               \
+#define FUSED_LAUNCH_T(KER, SMEM, GRID, THREADS, S, ARGS)                                    \
   do {                                                                                       \
     CU(cudaFuncSetAttribute(KER, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM)));   \
-    KER<<<(GRID), FB_THREADS, (SMEM), (S)>>>(ARGS);                                          \
+    KER<<<(GRID), (THREADS), (SMEM), (S)>>>(ARGS);                                           \
     ++h->launches;                                                                           \
   } while (0)
+#define FUSED_LAUNCH(KER, SMEM, GRID, S, ARGS) FUSED_LAUNCH_T(KER, SMEM, GRID, FB_THREADS, S, ARGS)
 
 #define FUSED_CASE_F(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.BNf == bn_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_fused_fwd<k_, bn_, rp_, nl_>), f.smem_fwd, grid, s, a);
@@ -554,6 +556,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     Phase ph(h, 1, s);
     if (use_tc(h)) {
       a.ncb = h->ts.ncbf;
+      if (getenv("TT_TC_VARIANT")) a.mode = atoi(getenv("TT_TC_VARIANT"));
       const int grid = (int)(c.m[f.F] * h->ts.ncbf);
       if (false) {
       }
@@ -608,12 +611,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     Phase ph(h, 2, s);
     if (h->last_path == 2) {
       a.ncb = h->ts.ncbb;
+      if (getenv("TT_TC_BVARIANT")) a.mode = atoi(getenv("TT_TC_BVARIANT"));
       const int grid = (int)(c.m[f.F] * h->ts.ncbb);
       rc = TT_OK;
       if (false) {
       }
 #define TT_TC_BWD_CASE(k_, bn_, rp_, nl_) \
-  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, s, a);
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, TCB_THREADS, s, a);
       TT_TC_SHAPES(TT_TC_BWD_CASE)
 #undef TT_TC_BWD_CASE
     } else {

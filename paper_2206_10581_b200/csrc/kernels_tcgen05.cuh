@@ -42,13 +42,17 @@ constexpr size_t tc_bwd_smem() {
   return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + 3 * (size_t)TC_BM * BN * 2 + TC_META;
 }
 
+// Plane writers map 8 consecutive threads to the 8 rows of one core matrix
+// (unit u: row-in-core = u % 8), so each 16-byte store phase covers 128
+// contiguous bytes -- no bank conflicts.
+
 // S block (K x BN) of slice g, column block cb -> planes [K rows][BN cols]
-template <int K, int BN>
+template <int K, int BN, int T>
 __device__ __forceinline__ void tc_stage_slice(const FusedArgs& a, int g, int cb, uint8_t* p0, uint8_t* p1,
                                                uint8_t* p2) {
   const float* src = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
-  for (int u = threadIdx.x; u < K * BN / 8; u += FB_THREADS) {
-    const int k = u / (BN / 8), c0 = (u - k * (BN / 8)) * 8;
+  for (int u = threadIdx.x; u < K * BN / 8; u += T) {
+    const int cc = (u >> 3) % (BN / 8), k = ((u >> 3) / (BN / 8)) * 8 + (u & 7), c0 = cc * 8;
     const float4 x0 = __ldg(reinterpret_cast<const float4*>(src + (int64_t)k * a.NC + c0));
     const float4 x1 = __ldg(reinterpret_cast<const float4*>(src + (int64_t)k * a.NC + c0 + 4));
     const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
@@ -56,31 +60,92 @@ __device__ __forceinline__ void tc_stage_slice(const FusedArgs& a, int g, int cb
   }
 }
 
-// A tile: rows m = j*RP + a of the batch-local nodes [tb, tb+nn) -> planes [128][K]
-template <int K, int RP>
-__device__ __forceinline__ void tc_stage_A(const FusedArgs& a, int tb, int nn, const int64_t* s_aoff, uint8_t* p0,
-                                           uint8_t* p1, uint8_t* p2) {
-  for (int u = threadIdx.x; u < TC_BM * K / 8; u += FB_THREADS) {
-    const int m = u / (K / 8), k0 = (u - m * (K / 8)) * 8;
-    const int j = m / RP;
-    float x[8];
-    if (j < nn) {
-      const float* src = a.Abase + s_aoff[tb + j] + (m - j * RP) * K + k0;
-      const float4 x0 = __ldg(reinterpret_cast<const float4*>(src));
-      const float4 x1 = __ldg(reinterpret_cast<const float4*>(src + 4));
-      x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w; x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
-    } else {
+// A tile: rows m = j*RP + a of the batch-local nodes [tb, tb+nn) -> planes
+// [128][K].  Loading (to registers) and storing (split into the planes) are
+// separate so the next tile's global loads are in flight under the current
+// tile's MMA and epilogue.
+template <int K, int T>
+struct ATileRegs {
+  static constexpr int N = TC_BM * K / 8 / T;  // units per thread
+  static_assert(N >= 1, "A tile smaller than the block");
+  float4 v[N][2];
+};
+
+template <int K, int RP, int T>
+__device__ __forceinline__ void tc_load_A(const FusedArgs& a, int tb, int nn, const int64_t* s_aoff,
+                                          ATileRegs<K, T>& r) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = 0.f;
+  for (int i = 0; i < ATileRegs<K, T>::N; ++i) {
+    const int u = threadIdx.x + i * T;
+    const int kc = (u >> 3) % (K / 8), m = ((u >> 3) / (K / 8)) * 8 + (u & 7);
+    const int j = m / RP;
+    if (j < nn) {
+      const float* src = a.Abase + s_aoff[tb + j] + (m - j * RP) * K + kc * 8;
+      r.v[i][0] = __ldg(reinterpret_cast<const float4*>(src));
+      r.v[i][1] = __ldg(reinterpret_cast<const float4*>(src + 4));
+    } else {
+      r.v[i][0] = r.v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    tc::store_split8(p0, p1, p2, m, k0, K, x);
   }
+}
+
+template <int K, int T>
+__device__ __forceinline__ void tc_store_A(const ATileRegs<K, T>& r, uint8_t* p0, uint8_t* p1, uint8_t* p2) {
+#pragma unroll
+  for (int i = 0; i < ATileRegs<K, T>::N; ++i) {
+    const int u = threadIdx.x + i * T;
+    const int kc = (u >> 3) % (K / 8), m = ((u >> 3) / (K / 8)) * 8 + (u & 7);
+    const float x[8] = {r.v[i][0].x, r.v[i][0].y, r.v[i][0].z, r.v[i][0].w,
+                        r.v[i][1].x, r.v[i][1].y, r.v[i][1].z, r.v[i][1].w};
+    tc::store_split8(p0, p1, p2, m, kc * 8, K, x);
+  }
+}
+
+// Node metadata of nodes [nb0, nb0 + nbn) of the group (kernels_fused.cuh
+// prep_nodes for a block of T threads).  Ends with a barrier.
+template <int T>
+__device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int nbn, int* s_node, int* s_cs0,
+                                              int* s_pref, int64_t* s_aoff, int* s_wsum) {
+  static_assert(T >= FB_NB && T <= 1024, "one thread per staged node");
+  const int t = threadIdx.x;
+  int cnt = 0;
+  if (t < nbn) {
+    const int node = a.orderF[nb0 + t];
+    const int c0 = a.cstartF[node];
+    cnt = a.cstartF[node + 1] - c0;
+    const int p = a.parentF[node];
+    s_node[t] = node;
+    s_cs0[t] = c0;
+    s_aoff[t] = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0] : (int64_t)p * a.RP * a.c.R[a.F];
+  }
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((int)lane_id() >= o) x += y;
+  }
+  if (lane_id() == 31) s_wsum[t >> 5] = x;
+  __syncthreads();
+  if (t < 32) {
+    int w = t < T / 32 ? s_wsum[t] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if ((int)lane_id() >= o) w += y;
+    }
+    if (t < T / 32) s_wsum[t] = w;
+  }
+  __syncthreads();
+  const int excl = x - cnt + ((t >> 5) ? s_wsum[(t >> 5) - 1] : 0);
+  if (t < nbn) s_pref[t] = excl;
+  if (t == nbn - 1) s_pref[nbn] = excl + cnt;
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
 // Forward: P_F tiles on the tensor pipe, saved to Psave.
 template <int K, int BN, int RP>
-__global__ void __launch_bounds__(FB_THREADS, 1) k_tc_fwd(FusedArgs a) {
+__global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
   static_assert(BN % 16 == 0 && BN <= 256 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
   constexpr int NPT = TC_BM / RP;
   constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -109,15 +174,17 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_fwd(FusedArgs a) {
     tc::mbar_init(&bar, 1);
     tc::fence_mbar_init();
   }
-  tc_stage_slice<K, BN>(a, g, cb, S0, S1, S2);
+  tc_stage_slice<K, BN, FB_THREADS>(a, g, cb, S0, S1, S2);
   uint32_t phase = 0;
   const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
+  ATileRegs<K, FB_THREADS> ar;
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    tc_load_A<K, RP, FB_THREADS>(a, 0, min(NPT, nbn), s_aoff, ar);
     for (int tb = 0; tb < nbn; tb += NPT) {
       const int nn = min(NPT, nbn - tb);
-      tc_stage_A<K, RP>(a, tb, nn, s_aoff, A0, A1, A2);
+      if (!(a.mode & 8)) tc_store_A<K, FB_THREADS>(ar, A0, A1, A2);
       tc::fence_async_smem();
       tc::before_sync();
       __syncthreads();
@@ -126,10 +193,11 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_fwd(FusedArgs a) {
       if (threadIdx.x == 0) {
         const tc::Operand oa = tc::kmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
         const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        tc::mma_x3(tm, oa, ob, K, idesc, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm, oa, ob, K, idesc, false);
         tc::commit(&bar);
       }
       __syncwarp();
+      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, FB_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);  // under the MMA
       tc::mbar_wait(&bar, phase);
       phase ^= 1;
       tc::after_sync();
@@ -142,7 +210,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_fwd(FusedArgs a) {
       for (int c = c_lo; c < c_lo + BN / 2; c += 16) {
         float v[16];
         tc::tmem_ld16(tm + ((uint32_t)(32 * (warp & 3)) << 16) + c, v);
-        if (dst) {
+        if (dst && !(a.mode & 4)) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             *reinterpret_cast<float4*>(dst + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -156,12 +224,20 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_fwd(FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Backward: dC on the CUDA cores, dG_F^T and dA on the tensor pipe.
+// Backward: dC on the CUDA cores, dG_F^T and dA on the tensor pipe.  512
+// threads (16 warps) per CTA: the CUDA-core half of a tile is a chain of
+// dependent L2 loads (ID digit -> last-core slice), so latency is hidden by
+// warps, and one CTA holds the whole 192 KB operand set per SM.
+constexpr int TCB_THREADS = 512;
+
 template <int K, int BN, int RP, int NL>
-__global__ void __launch_bounds__(FB_THREADS, 1) k_tc_bwd(FusedArgs a) {
+__global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   static_assert(BN == 128 && K % 16 == 0 && K <= 128 && TC_BM % RP == 0 && RP % 4 == 0, "tcgen05 backward shape");
+  constexpr int T = TCB_THREADS;
   constexpr int NPT = TC_BM / RP;
   constexpr uint32_t TCOLS = 2 * K <= 64 ? 64 : 2 * K <= 128 ? 128 : 256;
+  constexpr int EC = K / 4;  // epilogue columns per warp (16 warps = 4 lane quadrants x 4 column slices)
+  static_assert(EC == 8 || EC == 16, "epilogue column slice");
   extern __shared__ __align__(128) uint8_t tsm[];
   uint8_t* S0 = tsm;
   uint8_t* S1 = S0 + K * BN * 2;
@@ -185,12 +261,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
   if (g0 == g1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quadrant of this warp
+  const int eslice = (warp >> 2) * EC;
   if (warp == 0) tc::tmem_alloc<TCOLS>(&tslot);
   if (threadIdx.x == 32) {
     tc::mbar_init(&bar, 1);
     tc::fence_mbar_init();
   }
-  tc_stage_slice<K, BN>(a, g, cb, S0, S1, S2);
+  tc_stage_slice<K, BN, T>(a, g, cb, S0, S1, S2);
   const int nF = a.nF;
   const int64_t npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
@@ -199,57 +277,72 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   const uint32_t id_a = tc::idesc_bf16(TC_BM, K, 0, 0);   // dA = dC . S^T
   uint32_t phase = 0;
   int tiles = 0;
-  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
-    const int nbn = min(FB_NB, g1 - nb0);
-    prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
-      const int nn = min(NPT, nbn - tb);
-      tc_stage_A<K, RP>(a, tb, nn, s_aoff, A0, A1, A2);
-      // dC units: 4 rows of one node x 8 columns (one core-F column block jf)
-#pragma unroll 1
-      for (int unit = threadIdx.x; unit < (TC_BM / 4) * (BN / 8); unit += FB_THREADS) {
-        const int rg = unit / (BN / 8), c8 = unit - rg * (BN / 8);
-        const int m0 = rg * 4, j = m0 / RP, a0 = m0 - j * RP;
-        const int col0 = cb * BN + c8 * 8, jf = col0 / K, r0 = col0 - jf * K;
-        float acc[4][8];
+  ATileRegs<K, T> ar;
+  // dC unit of this thread: 4 rows of one node x 8 columns (one core-F
+  // column block jf).  unit bits: [0,2) column chunk low, [2] row group low,
+  // [3,5) column chunk high, [5,9) row group high; with the rows of a unit
+  // stored in rotated order (rot = unit % 4) the 8 threads of a store phase
+  // write 8 distinct rows of one core-matrix column: conflict-free.
+  static_assert((TC_BM / 4) * (BN / 8) == T, "one dC unit per thread");
+  const int unit = threadIdx.x;
+  const int c8 = (unit & 3) + 4 * ((unit >> 3) & 3);
+  const int rg = ((unit >> 2) & 1) + 2 * (unit >> 5);
+  const int rot = unit & 3;
+  const int m0 = rg * 4, uj = m0 / RP, a0 = m0 - uj * RP;
+  const int col0 = cb * BN + c8 * 8, jf = col0 / K, r0 = col0 - jf * K;
+  // dC(t) of this thread's unit into registers (loads + FFMA): issued for
+  // tile t+1 while the tensor pipe works on tile t
+  auto compute_dC = [&](int tb, int nn, float (&acc)[4][8]) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int t = 0; t < 8; ++t) acc[i][t] = 0.f;
-        if (j < nn) {
-          const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
-          for (int f = fA; f < fB; ++f) {
-            const int u = cs0 + (f - fA);
-            const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL;
-            float gv[8][NL];
+      for (int t = 0; t < 8; ++t) acc[i][t] = 0.f;
+    if (uj >= nn || (a.mode & 16)) return;
+    const int fA = s_pref[tb + uj], fB = s_pref[tb + uj + 1], cs0 = s_cs0[tb + uj];
+    for (int f = fA; f < fB; ++f) {
+      const int u = cs0 + (f - fA);
+      const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL;
+      const float* Yp = a.dY + (int64_t)u * npad + ((int64_t)a0 * nF + jf) * NL;
+      float yv[4][NL];
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
+      for (int i = 0; i < 4; ++i) {
+        const int ii = (i + rot) & 3;
 #pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + t * NL + l4));
-                gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
-              }
-            const float* Yp = a.dY + (int64_t)u * npad + ((int64_t)a0 * nF + jf) * NL;
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)ii * nF * NL + l4));
+          yv[i][l4] = x.x; yv[i][l4 + 1] = x.y; yv[i][l4 + 2] = x.z; yv[i][l4 + 3] = x.w;
+        }
+      }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float yv[NL];
+      for (int t = 0; t < 8; ++t) {
+        float gv[NL];
 #pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)i * nF * NL + l4));
-                yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
-              }
-#pragma unroll
-              for (int t = 0; t < 8; ++t) {
-                float s = acc[i][t];
-#pragma unroll
-                for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[jl], gv[t][jl], s);
-                acc[i][t] = s;
-              }
-            }
-          }
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + t * NL + l4));
+          gv[l4] = x.x; gv[l4 + 1] = x.y; gv[l4 + 2] = x.z; gv[l4 + 3] = x.w;
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tc::store_split8(D0, D1, D2, m0 + i, c8 * 8, BN, acc[i]);
+        for (int i = 0; i < 4; ++i) {
+          float s = acc[i][t];
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[i][jl], gv[jl], s);
+          acc[i][t] = s;
+        }
+      }
+    }
+  };
+  float acc[4][8];
+  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
+    const int nbn = min(FB_NB, g1 - nb0);
+    tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
+    compute_dC(0, min(NPT, nbn), acc);
+    for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
+      const int nn = min(NPT, nbn - tb);
+      if (!(a.mode & 8)) tc_store_A<K, T>(ar, A0, A1, A2);
+      if (!(a.mode & 32)) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tc::store_split8(D0, D1, D2, m0 + ((i + rot) & 3), c8 * 8, BN, acc[i]);
       }
       tc::fence_async_smem();
       tc::before_sync();
@@ -260,31 +353,35 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_bwd(FusedArgs a) {
         const uint32_t d0 = tc::smem_u32(D0), d1 = tc::smem_u32(D1), d2 = tc::smem_u32(D2);
         const tc::Operand dcT = tc::mnmajor(d0, d1, d2, BN);  // A operand (m = col, k = row)
         const tc::Operand aB = tc::mnmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
-        tc::mma_x3(tm, dcT, aB, TC_BM, id_g, tiles > 0);
+        if (!(a.mode & 2)) tc::mma_x3(tm, dcT, aB, TC_BM, id_g, tiles > 0);
         const tc::Operand dcK = tc::kmajor(d0, d1, d2, BN);   // A operand (m = row, k = col)
         const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        tc::mma_x3(tm + K, dcK, sT, BN, id_a, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm + K, dcK, sT, BN, id_a, false);
         tc::commit(&bar);
       }
       __syncwarp();
+      // this tile's epilogue row, then the next tile's inputs under the MMA
+      const int m = 32 * (warp & 3) + lane;
+      const int j = m / RP;
+      float* dst = (j < nn && !(a.mode & 4))
+                       ? a.dPc + ((int64_t)s_node[tb + j] * a.ncb + cb) * RP * K + (m - j * RP) * K + eslice
+                       : nullptr;
+      if (tb + NPT < nbn) {
+        if (!(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+        compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
+      }
       tc::mbar_wait(&bar, phase);
       phase ^= 1;
       tc::after_sync();
       // dA epilogue -> dPc[(node, cb)][a][r]
       {
-        const int m = 32 * (warp & 3) + lane;
-        const int j = m / RP;
-        const int c_lo = (warp >> 2) * (K / 2);
-        float* dst = j < nn ? a.dPc + ((int64_t)s_node[tb + j] * a.ncb + cb) * RP * K + (m - j * RP) * K : nullptr;
-#pragma unroll 1
-        for (int c = c_lo; c < c_lo + K / 2; c += 16) {
-          float v[16];
-          tc::tmem_ld16(tm + ((uint32_t)(32 * (warp & 3)) << 16) + K + c, v);
-          if (dst) {
+        float v[EC];
+        if constexpr (EC == 16) tc::tmem_ld16(tm + lane_base + K + eslice, v);
+        else tc::tmem_ld8(tm + lane_base + K + eslice, v);
+        if (dst) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              *reinterpret_cast<float4*>(dst + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
+          for (int q = 0; q < EC / 4; ++q)
+            *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
       }
       tc::before_sync();
@@ -296,15 +393,12 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   {
     const uint32_t tm = tslot;
     const int col = 32 * (warp & 3) + lane;
-    const int r_lo = (warp >> 2) * (K / 2);
     float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN + col;
-#pragma unroll 1
-    for (int r = r_lo; r < r_lo + K / 2; r += 16) {
-      float v[16];
-      tc::tmem_ld16(tm + ((uint32_t)(32 * (warp & 3)) << 16) + r, v);
+    float v[EC];
+    if constexpr (EC == 16) tc::tmem_ld16(tm + lane_base + eslice, v);
+    else tc::tmem_ld8(tm + lane_base + eslice, v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) gdst[(int64_t)(r + i) * a.NC] = v[i];
-    }
+    for (int i = 0; i < EC; ++i) gdst[(int64_t)(eslice + i) * a.NC] = v[i];
   }
   tc::before_sync();
   __syncthreads();
