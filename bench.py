@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=0, help="rows per CPU-baseline step (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-tensor-path", action="store_true", help="skip the tensor-core path measurement")
     p.add_argument("--graph", type=int, default=1, help="replay the step as one CUDA graph (1) or launch eagerly (0)")
     return p.parse_args()
 
@@ -210,90 +211,115 @@ def main():
             dp.allreduce()
         emb.step()
 
-    step = step_eager
-    graph = None
-    if a.graph and world == 1:
-        # capture forward + backward + update once (after a warm-up that sizes
-        # every buffer) and replay it: one launch per step instead of ~60
+    def timed(path):
+        """Capture (world 1) and time `a.steps` steps on `path`; returns the
+        max-over-ranks device time and the per-phase kernel times."""
+        emb.set_path(path)
+        step = step_eager
+        graph, graph_kernels = None, 0
+        if a.graph and world == 1:
+            # capture forward + backward + update once (after a warm-up that sizes
+            # every buffer) and replay it: one launch per step instead of ~60
+            emb.snapshot_cores()
+            step_eager()
+            torch.cuda.synchronize()
+            emb.sync()
+            emb.restore_cores()
+            s_cap = torch.cuda.Stream(device=dev)
+            s_cap.wait_stream(torch.cuda.current_stream(dev))
+            graph = torch.cuda.CUDAGraph()
+            n0 = emb.launch_count()
+            with torch.cuda.stream(s_cap):
+                with torch.cuda.graph(graph, stream=s_cap):
+                    step_eager()
+            graph_kernels = emb.launch_count() - n0
+            torch.cuda.current_stream(dev).wait_stream(s_cap)
+            torch.cuda.synchronize()
+            step = graph.replay
+        # Every timed step starts from the same cores (restored outside the
+        # timed events, like the L2 flush): repeated SGD steps on one fixed batch
+        # diverge at the billion config (sum-gradients of Zipf-hot IDs), and a
+        # rejected non-finite update would skip work.
         emb.snapshot_cores()
-        step_eager()
+        for _ in range(a.warmup):
+            emb.restore_cores()
+            step()
         torch.cuda.synchronize()
         emb.sync()
-        emb.restore_cores()
-        s_cap = torch.cuda.Stream(device=dev)
-        s_cap.wait_stream(torch.cuda.current_stream(dev))
-        graph = torch.cuda.CUDAGraph()
-        n0 = emb.launch_count()
-        with torch.cuda.stream(s_cap):
-            with torch.cuda.graph(graph, stream=s_cap):
-                step_eager()
-        graph_kernels = emb.launch_count() - n0
-        torch.cuda.current_stream(dev).wait_stream(s_cap)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-
-        def step():
-            graph.replay()
-
-    # Every timed step starts from the same cores (restored outside the
-    # timed events, like the L2 flush): repeated SGD steps on one fixed batch
-    # diverge at the billion config (sum-gradients of Zipf-hot IDs), and a
-    # rejected non-finite update would skip work.
-    emb.snapshot_cores()
-    for _ in range(a.warmup):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        emb.profile_read()  # drop warm-up records
+        emb.set_profiling(graph is None)
+        l0 = emb.launch_count()
+        for i in range(a.steps):
+            emb.restore_cores()
+            flush.zero_()
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        launches = emb.launch_count() - l0
+        if graph is not None:
+            launches = graph_kernels * a.steps  # kernels replayed from the captured graph
+        emb.set_profiling(False)
+        prof = emb.profile_read()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        emb.sync()
+        per_step = [s.elapsed_time(e) for s, e in ev]
+        tt = torch.tensor([sum(per_step)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        if graph is not None:
+            # per-phase kernel timing needs the eager launches (events on the
+            # launching stream): the same K steps once more, eagerly
+            emb.set_profiling(True)
+            for i in range(a.steps):
+                emb.restore_cores()
+                flush.zero_()
+                step_eager()
+            torch.cuda.synchronize()
+            emb.set_profiling(False)
+            prof = emb.profile_read()
         emb.restore_cores()
-        step()
-    torch.cuda.synchronize()
-    emb.sync()
-    U = emb.plan_stats()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+        return {"t_max": t_max, "per_step": per_step, "launches": launches, "phase_ms": phase_ms,
+                "path": emb.last_path(), "graph": graph is not None}
+
     props = torch.cuda.get_device_properties(local)
     uuid = getattr(props, "uuid", None)
     sampler = ClockSampler(f"GPU-{uuid}" if uuid else str(local))
     sampler.start()
     time.sleep(0.3)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    emb.profile_read()  # drop warm-up records
-    emb.set_profiling(graph is None)
-    l0 = emb.launch_count()
-    for i in range(a.steps):
-        emb.restore_cores()
-        flush.zero_()
-        ev[i][0].record()
-        step()
-        ev[i][1].record()
-    torch.cuda.synchronize()
-    launches = emb.launch_count() - l0
-    if graph is not None:
-        launches = graph_kernels * a.steps  # kernels replayed from the captured graph
-    emb.set_profiling(False)
-    prof = emb.profile_read()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    main_run = timed(a.path)
     clocks = sampler.stop()
-    emb.sync()
-    t_ms = sum(s.elapsed_time(e) for s, e in ev)
-    per_step = [s.elapsed_time(e) for s, e in ev]
-    tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t_max = float(tt.item())
+    U = emb.plan_stats()
+    t_max, per_step, launches, graph_on = main_run["t_max"], main_run["per_step"], main_run["launches"], main_run["graph"]
     value = Bg * a.steps / (t_max / 1e3)
     ms_per_step = t_max / a.steps
+    phase_ms = main_run["phase_ms"]
+    path_used = main_run["path"]
 
-    if graph is not None:
-        # per-phase kernel timing needs the eager launches (events on the
-        # launching stream): the same K steps once more, eagerly
-        emb.set_profiling(True)
-        for i in range(a.steps):
-            emb.restore_cores()
-            flush.zero_()
-            step_eager()
-        torch.cuda.synchronize()
-        emb.set_profiling(False)
-        prof = emb.profile_read()
+    # the optional tensor-core path (tcgen05, BF16x3: fp32-level accuracy),
+    # reported beside the FP32 FFMA headline (north star: "reported separately")
+    tensor = None
+    if a.path == "auto" and not a.no_tensor_path:
+        tc_run = timed("tc")
+        if tc_run["path"] == "fused-tc":
+            tf_ = algorithmic_flops(cfg, U)
+            tc_ms = tc_run["t_max"] / a.steps
+            tensor = {"path": "fused-tc (tcgen05.mma kind::f16, BF16x3 six-product split, FP32 accumulate in TMEM)",
+                      "value": Bg * a.steps / (tc_run["t_max"] / 1e3), "unit": "rows/s", "ms_per_step": tc_ms,
+                      "ms_per_step_each": tc_run["per_step"], "phases_ms_per_step": tc_run["phase_ms"],
+                      "tolerance": "|x - x_ref| <= 1e-5 a_ref (same bound as the FP32 path; tests/test_gpu_parity.py)",
+                      "step_tflops": tf_ / (tc_ms * 1e-3) / 1e12,
+                      "gpu_launches": tc_run["launches"]}
+        emb.set_path(a.path)
 
     # roofline of the dominant kernel: its algorithmic FLOPs per launch over its
     # average launch duration, timed live with CUDA events on its stream
@@ -301,13 +327,12 @@ def main():
     peak = E.ffma_peak_tflops(local, 8192)
     peak_gemm = E.ffma_outer_tflops(local, 4096)
     costs = level_costs(cfg)
-    fused = emb.last_path().startswith("fused")
+    fused = path_used.startswith("fused")
     # algorithmic FLOPs of the fused kernels (the last level's forward and W
     # run in the streaming kernels k_last_level / k_fused_w):
     #   k_fused_fwd = 2 U_F c_F;  k_fused_bwd = 4 U_F c_F (dG_F, dA) + 2 U_d c_d (dC pass)
     uf_cf = U[-2] * costs[-2] if len(costs) >= 2 else 0
     ud_cd = U[-1] * costs[-1]
-    phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
     if fused:
         dom = "k_fused_bwd" if phase_ms["bwd_main"] >= phase_ms["fwd_main"] else "k_fused_fwd"
         dom_flops = (4.0 * uf_cf + 2.0 * ud_cd) if dom == "k_fused_bwd" else 2.0 * uf_cf
@@ -375,8 +400,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": name, "global_batch": Bg, "num_nodes": cfg.num_nodes, "row_factors": cfg.m,
                        "col_factors": cfg.n, "ranks": cfg.R, "optimizer": WORKLOADS[name]["opt"],
-                       "parallelism": f"dp{world}", "path": emb.last_path(),
-                       "cuda_graph": graph is not None,
+                       "parallelism": f"dp{world}", "path": path_used,
+                       "cuda_graph": graph_on,
                        "l2": "256 MB buffer written between timed steps (outside the events)",
                        "cores": "restored from a device snapshot before every step (outside the events)",
                        "unique_per_level_rank0": U},
@@ -389,7 +414,7 @@ def main():
                          "step_frac": flops / (ms_per_step * 1e-3) / 1e12 / peak if peak > 0 else None},
             "phases_ms_per_step": phase_ms,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "ms_per_step_each": per_step,
+            "ms_per_step_each": per_step, "tensor_path": tensor,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

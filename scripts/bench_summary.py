@@ -17,3 +17,7 @@ for path in sys.argv[1:]:
           f"e2e={(e2e.get('value') or 0) / 1e6:.2f}M cpu={(cpu.get('value') or 0) / 1e6:.3f}M "
           f"launches={d.get('gpu_launches')} clocks={d.get('clocks', {}).get('sm_mhz')} "
           f"phases={ {k: round(v, 3) for k, v in (d.get('phases_ms_per_step') or {}).items()} }")
+    t = d.get("tensor_path")
+    if t:
+        print(f"{'':>9} tensor path: ms/step={t['ms_per_step']:.3f} Mrows/s={t['value'] / 1e6:.2f} "
+              f"phases={ {k: round(v, 3) for k, v in (t.get('phases_ms_per_step') or {}).items()} }")
