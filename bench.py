@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-tensor-path", action="store_true", help="skip the tensor-core path measurement")
+    p.add_argument("--shard", default="owner", choices=["owner", "position"], help="N > 1 decomposition (dist.py)")
     p.add_argument("--graph", type=int, default=1, help="replay the step as one CUDA graph (1) or launch eagerly (0)")
     return p.parse_args()
 
@@ -182,7 +183,7 @@ def main():
     import torch.distributed as dist
     from paper_2206_10581_b200 import engine as E
     from paper_2206_10581_b200.config import WORKLOADS, workload_inputs
-    from paper_2206_10581_b200.dist import DataParallelTT, shard_bounds
+    from paper_2206_10581_b200.dist import DataParallelTT, OwnerShardedTT, shard_bounds
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -200,16 +201,21 @@ def main():
     emb.set_path(a.path)
     opt = E.OptimizerState.make(cfg, getattr(E.OptKind, WORKLOADS[name]["opt"]), 0.01)
     emb.configure_optimizer(opt)
-    dp = DataParallelTT(emb) if world > 1 else None
+    dp = None
+    if world > 1:
+        dp = OwnerShardedTT(emb) if a.shard == "owner" else DataParallelTT(emb)
     out = torch.empty((B, cfg.emb_dim), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     def step_eager():
-        emb.forward(idx, out)
-        emb.backward(up)
-        if dp:
-            dp.allreduce()
-        emb.step()
+        if dp is None:
+            emb.forward(idx, out)
+            emb.backward(up)
+            emb.step()
+        else:  # routing / all-reduce inside (dist.py)
+            dp.forward(idx, out)
+            dp.backward(up)
+            dp.step()
 
     def timed(path):
         """Capture (world 1) and time `a.steps` steps on `path`; returns the
@@ -364,11 +370,10 @@ def main():
             else:
                 d_idx = h_idx.to(dev, non_blocking=True)
                 d_up = h_up.to(dev, non_blocking=True)
-                emb.forward(d_idx, out)
+                dp.forward(d_idx, out)
                 h_out.copy_(out, non_blocking=True)
-                emb.backward(d_up)
-                dp.allreduce()
-                emb.step()
+                dp.backward(d_up)
+                dp.step()
                 torch.cuda.synchronize()
 
         e2e_step()
@@ -385,7 +390,7 @@ def main():
         e2e = {"value": Bg * a.steps / float(te.item()), "unit": "rows/s",
                "h2d_bytes_per_step": int(h_idx.numel() * 8 + h_up.numel() * 4),
                "d2h_bytes_per_step": int(h_out.numel() * 4),
-               "api": "tt_train_step_host (C-ABI)" if dp is None else "TTEmbedding + DataParallelTT (Python API)"}
+               "api": "tt_train_step_host (C-ABI)" if dp is None else f"TTEmbedding + {type(dp).__name__} (Python API)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -401,6 +406,9 @@ def main():
             "config": {"workload": name, "global_batch": Bg, "num_nodes": cfg.num_nodes, "row_factors": cfg.m,
                        "col_factors": cfg.n, "ranks": cfg.R, "optimizer": WORKLOADS[name]["opt"],
                        "parallelism": f"dp{world}", "path": path_used,
+                       "shard": None if world == 1 else (
+                           "owner: level-F core sharded by digit, IDs + upstream rows routed by all-to-all, small cores all-reduced"
+                           if a.shard == "owner" else "position: batch by position, whole gradient buffer all-reduced"),
                        "cuda_graph": graph_on,
                        "l2": "256 MB buffer written between timed steps (outside the events)",
                        "cores": "restored from a device snapshot before every step (outside the events)",

@@ -1,7 +1,21 @@
-"""Data parallelism over the index batch: one process per GPU,
-cores replicated, the batch sharded by position, and exactly one exchange
-step -- a sum all-reduce (NCCL over NVLink/NVSwitch via torch.distributed) of
-the single contiguous gradient buffer between backward and update.
+"""Data parallelism over the index batch: one process per GPU.
+
+Two schemes share the engine's single contiguous gradient buffer:
+
+* position sharding (DataParallelTT): cores replicated, the batch sharded by
+  position, and exactly one exchange step -- a sum all-reduce (NCCL over
+  NVLink/NVSwitch via torch.distributed) of the whole buffer between backward
+  and update.  Cross-shard duplicates of a prefix are computed on every rank
+  that sees them (a ~5.3x ceiling at papers on 8 GPUs).
+* ID-owner sharding (OwnerShardedTT): the level-F core (F = d-2, the core of
+  the fused GEMMs -- 63 MB of the 64 MB at papers) is sharded by its digit
+  i_{d-1}: rank r owns the digit range [v_r, v_{r+1}) and so every ID, every
+  level-F prefix and every G_F slice with such a digit.  Each step routes the
+  IDs and their upstream rows to their owners (all-to-all), every prefix is
+  computed exactly once in the job, output rows travel back (all-to-all), and
+  only the small replicated cores' gradients are all-reduced.  The owned G_F
+  slices (and their optimizer state) are only ever read and updated by their
+  owner, so they never cross NVLink.
 
 The buffer holds every core's gradient in the engine's device layout
 ([m_k][R_{k-1}][n_k][R_k]) followed by one touch counter per core slice, so
@@ -95,3 +109,161 @@ class DataParallelTT:
     def step(self):
         self.allreduce()
         self.emb.step()
+
+
+# ---------------------------------------------------------------------------
+# ID-owner sharding
+
+def owner_bounds(cfg: TTConfig, world: int) -> List[int]:
+    """Digit boundaries v_0 = 0 < ... < v_world = m_F of the level-F core
+    (F = d-2; the first core when d = 2): rank r owns digits [v_r, v_{r+1})."""
+    F = max(cfg.d - 2, 0)
+    m = cfg.m[F]
+    return [m * r // world for r in range(world + 1)]
+
+
+def owner_of(cfg: TTConfig, idx, world: int):
+    """Owner rank of every ID (torch int64 tensor, any device): the rank whose
+    digit range holds the ID's level-F digit (tt_config.cpp:176-189 radix)."""
+    import torch
+    F = max(cfg.d - 2, 0)
+    suffix = int(np.prod(cfg.m[F + 1:])) if F + 1 < cfg.d else 1
+    digit = torch.div(idx, suffix, rounding_mode="floor") % cfg.m[F]
+    b = torch.tensor(owner_bounds(cfg, world)[1:-1], dtype=torch.int64, device=idx.device)
+    return torch.bucketize(digit, b, right=True)
+
+
+class Route:
+    """One all-to-all exchange plan: local positions sorted by owner rank."""
+
+    def __init__(self, order, send_counts: List[int], recv_counts: List[int]):
+        self.order, self.send_counts, self.recv_counts = order, send_counts, recv_counts
+
+
+def route_to_owners(cfg: TTConfig, idx, group=None, comm=None):
+    """Send every local ID to its owner.  Returns (received IDs, Route).
+    `comm` is torch.distributed (default) or an object with the same
+    collective calls (tests)."""
+    import torch
+    dist = comm or __import__("torch.distributed", fromlist=["x"])
+    world = dist.get_world_size(group)
+    own = owner_of(cfg, idx, world)
+    order = torch.argsort(own, stable=True)
+    counts = torch.bincount(own, minlength=world)
+    rc = torch.empty_like(counts)
+    dist.all_to_all_single(rc, counts, group=group)
+    send, recv = counts.tolist(), rc.tolist()
+    out = torch.empty(sum(recv), dtype=idx.dtype, device=idx.device)
+    dist.all_to_all_single(out, idx[order].contiguous(), recv, send, group=group)
+    return out, Route(order, send, recv)
+
+
+def route_rows(rows, r: Route, group=None, comm=None):
+    """Local rows (one per local ID) -> the owners, in received-ID order."""
+    import torch
+    dist = comm or __import__("torch.distributed", fromlist=["x"])
+    out = torch.empty((sum(r.recv_counts),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    dist.all_to_all_single(out, rows[r.order].contiguous(), r.recv_counts, r.send_counts, group=group)
+    return out
+
+
+def route_back(rows, r: Route, out=None, group=None, comm=None):
+    """Owner rows (received-ID order) -> back to the local positions."""
+    import torch
+    dist = comm or __import__("torch.distributed", fromlist=["x"])
+    tmp = torch.empty((sum(r.send_counts),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    dist.all_to_all_single(tmp, rows.contiguous(), r.send_counts, r.recv_counts, group=group)
+    if out is None:
+        out = torch.empty_like(tmp)
+    out[r.order] = tmp
+    return out
+
+
+def replicated_segments(cfg: TTConfig) -> List[tuple]:
+    """(offset, length) ranges of the gradient buffer that are all-reduced
+    under owner sharding: every core but the sharded level-F core, and their
+    touch counters (merged where adjacent)."""
+    F = max(cfg.d - 2, 0)
+    spans, off = [], 0
+    sizes = [cfg.core_size(k) for k in range(cfg.d)]
+    for k in range(cfg.d):
+        if k != F:
+            spans.append((off, sizes[k]))
+        off += sizes[k]
+    for k in range(cfg.d):
+        if k != F:
+            spans.append((off, cfg.m[k]))
+        off += cfg.m[k]
+    merged: List[list] = []
+    for o, n in spans:
+        if merged and merged[-1][0] + merged[-1][1] == o:
+            merged[-1][1] += n
+        else:
+            merged.append([o, n])
+    return [tuple(x) for x in merged]
+
+
+class OwnerShardedTT:
+    """One rank of an ID-owner-sharded TT embedding (see the module docstring).
+
+    forward(indices) takes this rank's local batch (any IDs), returns their
+    rows in local order; backward(grad_out) takes the local upstream rows;
+    step() all-reduces the replicated cores' gradients and updates.  Every
+    rank must hold the same initial cores; the level-F slices a rank does not
+    own are never read or written by it (gather_level_core() assembles them).
+    """
+
+    def __init__(self, emb, group=None, comm=None):
+        import torch
+        dist = comm or __import__("torch.distributed", fromlist=["x"])
+        self.emb, self.group, self.dist = emb, group, dist
+        cfg = emb.config
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.bounds = owner_bounds(cfg, self.world)
+        self.segments = replicated_segments(cfg)
+        self.buf = torch.zeros(grad_buffer_len(cfg), dtype=torch.float32, device=f"cuda:{emb.device}")
+        emb.bind_grad_buffer(self.buf)
+        emb.set_dense_grads(True)
+        self._route = None
+        self._recv_idx = None
+
+    def forward(self, indices, out=None):
+        import torch
+        cfg = self.emb.config
+        recv, self._route = route_to_owners(cfg, indices, self.group, self.dist)
+        self._recv_idx = recv
+        rows = self.emb.forward(recv) if recv.numel() else \
+            torch.empty((0, cfg.emb_dim), dtype=torch.float32, device=indices.device)
+        return route_back(rows, self._route, out, self.group, self.dist)
+
+    def backward(self, grad_out):
+        if self._route is None:
+            raise RuntimeError("OwnerShardedTT.backward: no forward on this rank")
+        up = route_rows(grad_out, self._route, self.group, self.dist)
+        if self._recv_idx.numel():
+            self.emb.backward(up)
+        else:  # nothing owned this step: zero gradients (CoreGradients::zeros)
+            self.emb.backward(up, self._recv_idx)
+
+    def allreduce(self):
+        for o, n in self.segments:
+            self.dist.all_reduce(self.buf[o: o + n], group=self.group)
+
+    def step(self):
+        self.allreduce()
+        self.emb.step()
+
+    def gather_level_core(self):
+        """Full level-F core (reference layout) assembled from the owners' slices."""
+        import torch
+        cfg = self.emb.config
+        F = max(cfg.d - 2, 0)
+        mine = torch.from_numpy(np.ascontiguousarray(self.emb.get_cores(np.float32)[F])).to(self.buf.device)
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine, group=self.group)
+        full = mine.clone()
+        for r in range(self.world):
+            lo, hi = self.bounds[r], self.bounds[r + 1]
+            full[:, lo:hi] = parts[r][:, lo:hi]
+        return full.cpu().numpy()
