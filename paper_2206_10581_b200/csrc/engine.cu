@@ -264,7 +264,7 @@ K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, cons
     const int bits = (nbits - shift + (passes - p) - 1) / (passes - p);  // split evenly
     const int bins = 1 << bits;
     LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, bits, h->hist);
-    LAUNCH(k_rs_colscan, (bins + 255) / 256, 256, 0, s, h->hist, tot, n_dev, n_host, bits);
+    LAUNCH(k_rs_colscan, (bins + 31) / 32, 32 * RS_CS_SEG, 0, s, h->hist, tot, n_dev, n_host, bits);
     const size_t smem = sizeof(int) * ((size_t)RS_WARPS * bins + bins + 64);
     LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, smem, s, kin, vin, kout, vo, n_dev, n_host, shift, bits, h->hist,
            tot);

@@ -65,16 +65,40 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
   for (int i = threadIdx.x; i < bins; i += RS_THREADS) hist[blockIdx.x * bins + i] = cnt[i];
 }
 
-// hist[t][d] <- sum_{t' < t} hist[t'][d];  tot[d] = sum_t hist[t][d]
-__global__ void __launch_bounds__(256) k_rs_colscan(int* __restrict__ hist, int* __restrict__ tot, const int* n_dev,
-                                                    int n_host, int nbits) {
+// hist[t][d] <- sum_{t' < t} hist[t'][d];  tot[d] = sum_t hist[t][d].
+// A block owns 32 digits (lanes) x 8 tile segments (warps): each thread sums
+// its segment with independent loads, the 8 segment totals are scanned in
+// shared memory, then each thread rewrites its segment as prefixes.
+constexpr int RS_CS_SEG = 8;
+__global__ void __launch_bounds__(32 * RS_CS_SEG) k_rs_colscan(int* __restrict__ hist, int* __restrict__ tot,
+                                                             const int* n_dev, int n_host, int nbits) {
+  __shared__ int part[RS_CS_SEG][33];
   const int bins = 1 << nbits;
-  const int dgt = blockIdx.x * blockDim.x + threadIdx.x;
-  if (dgt >= bins) return;
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int dgt = blockIdx.x * 32 + lane;
   const int n = rs_count(n_dev, n_host);
   const int ntiles = (n + RS_TILE - 1) / RS_TILE;
-  int run = 0, t = 0;
-  for (; t + 8 <= ntiles; t += 8) {
+  const int per = (ntiles + RS_CS_SEG - 1) / RS_CS_SEG;
+  const int t0 = min(ntiles, seg * per), t1 = min(ntiles, t0 + per);
+  int sum = 0;
+  if (dgt < bins) {
+    int t = t0;
+    for (; t + 8 <= t1; t += 8) {
+      int h[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) h[i] = hist[(t + i) * bins + dgt];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += h[i];
+    }
+    for (; t < t1; ++t) sum += hist[t * bins + dgt];
+  }
+  part[seg][lane] = sum;
+  __syncthreads();
+  int run = 0;
+  for (int q = 0; q < seg; ++q) run += part[q][lane];
+  if (dgt >= bins) return;
+  int t = t0;
+  for (; t + 8 <= t1; t += 8) {
     int h[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[i] = hist[(t + i) * bins + dgt];
@@ -84,12 +108,12 @@ __global__ void __launch_bounds__(256) k_rs_colscan(int* __restrict__ hist, int*
       run += h[i];
     }
   }
-  for (; t < ntiles; ++t) {
+  for (; t < t1; ++t) {
     const int h = hist[t * bins + dgt];
     hist[t * bins + dgt] = run;
     run += h;
   }
-  tot[dgt] = run;
+  if (seg == RS_CS_SEG - 1) tot[dgt] = run;
 }
 
 template <class K>
