@@ -597,8 +597,15 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   const int d = c.d;
   const int64_t cap = h->cap;
   const int64_t chunks = (h->B + DY_CHUNK - 1) / DY_CHUNK;
-  LAUNCH(k_dy_chunks, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
-         h->seg, h->F.dY, h->F.part, h->st);
+  if (c.npad <= 128)
+    LAUNCH(k_dy_chunks<1>, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
+           h->seg, h->F.dY, h->F.part, h->st);
+  else if (c.npad <= 256)
+    LAUNCH(k_dy_chunks<2>, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
+           h->seg, h->F.dY, h->F.part, h->st);
+  else
+    LAUNCH(k_dy_chunks<4>, (int)((chunks + 7) / 8), 256, 0, s, d_up, (int)h->B, c.emb_dim, c.npad, h->flag, h->spos,
+           h->seg, h->F.dY, h->F.part, h->st);
   LAUNCH(k_dy_groups, (int)(((chunks + 31) / 32 + 7) / 8), 256, 0, s, (int)h->B, c.npad, h->flag, h->seg, h->F.part,
          h->F.gpart, h->F.dY, h->st);
   LAUNCH(k_dy_spans, grid_for(h->capk[d - 1] * 32, 256, 148 * 8), 256, 0, s, h->counts, d, c.npad, h->seg, h->F.part,
@@ -1153,11 +1160,13 @@ int tt_train_step_host(tt_engine* h, const int64_t* h_idx, int64_t B, const floa
   const size_t rows = sizeof(float) * (size_t)B * (size_t)h->dc.emb_dim;
   // the compute stream's previous work (and any earlier reader of st_up /
   // st_out) is ordered before this step's copies
+  // the indices go first: host-to-device copies share a copy engine, and the
+  // plan + forward must not queue behind the 128 MB upstream upload
+  CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
   CU(cudaEventRecord(h->ev_in, s));
   CU(cudaStreamWaitEvent(h->s_h2d, h->ev_in, 0));
   CU(cudaMemcpyAsync(h->st_up, h_up, rows, cudaMemcpyHostToDevice, h->s_h2d));  // under plan + forward
   CU(cudaEventRecord(h->ev_up, h->s_h2d));
-  CU(cudaMemcpyAsync(h->st_idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, s));
   rc = tt_forward(h, h->st_idx, B, h->st_out, s);
   if (rc) return rc;
   if (h_out) {  // rows go back under the backward + update

@@ -19,7 +19,9 @@ namespace tt {
 constexpr int DY_CHUNK = 32;
 constexpr int HEAVY_POS = 8;  // IDs with more positions are scattered by k_scatter_heavy
 
-// uid1[s] = (distinct index of sorted slot s) + 1  (the inclusive unique scan)
+// uid1[s] = (distinct index of sorted slot s) + 1  (the inclusive unique scan);
+// NV = ceil(npad / 128) float4 column groups per lane (1, 2 or 4)
+template <int NV>
 __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up, int B, int64_t emb, int64_t npad,
                                                    const int* __restrict__ uid1, const int* __restrict__ spos,
                                                    const int* __restrict__ seg, float* __restrict__ dY,
@@ -33,10 +35,10 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
   const int my_s = lo + lane;
   const int my_u = my_s < hi ? uid1[my_s] - 1 : -1;
   const int my_p = my_s < hi ? spos[my_s] : 0;
-  const int nv = (int)((npad + 127) / 128);  // float4 column groups per lane (<= 4)
-  float4 acc[4];
+  constexpr int nv = NV;
+  float4 acc[NV];
 #pragma unroll
-  for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   int cur = __shfl_sync(0xffffffffu, my_u, 0);
   auto flush = [&](int u) {
     const int s0 = seg[u], s1 = seg[u + 1];
@@ -44,26 +46,41 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
     if (s0 >= lo && s1 <= hi) dst = dY + (int64_t)u * npad;
     else dst = part + ((int64_t)warp * 2 + (s0 < lo ? 0 : 1)) * npad;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < NV; ++v) {
       const int64_t c = (int64_t)v * 128 + lane * 4;
       if (v < nv && c < npad) *reinterpret_cast<float4*>(dst + c) = acc[v];
       acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  for (int i = 0; i < hi - lo; ++i) {
-    const int u = __shfl_sync(0xffffffffu, my_u, i);
-    const int p = __shfl_sync(0xffffffffu, my_p, i);
-    if (u != cur) {
-      flush(cur);
-      cur = u;
-    }
-    const float* row = up + (int64_t)p * emb;
+  // rows are loaded 8 at a time (independent 16-byte loads in flight), then
+  // summed in slot order
+  constexpr int PF = NV <= 2 ? 8 : 4;
+  for (int i0 = 0; i0 < hi - lo; i0 += PF) {
+    float4 x[PF][NV];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int64_t c = (int64_t)v * 128 + lane * 4;
-      if (v < nv && c < emb) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(row + c));
-        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+    for (int b = 0; b < PF; ++b) {
+      const int p = __shfl_sync(0xffffffffu, my_p, (i0 + b) & 31);
+      const float* row = up + (int64_t)p * emb;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = (int64_t)v * 128 + lane * 4;
+        if (i0 + b < hi - lo && v < nv && c < emb) x[b][v] = __ldg(reinterpret_cast<const float4*>(row + c));
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < PF; ++b) {
+      if (i0 + b >= hi - lo) break;
+      const int u = __shfl_sync(0xffffffffu, my_u, i0 + b);
+      if (u != cur) {
+        flush(cur);
+        cur = u;
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = (int64_t)v * 128 + lane * 4;
+        if (v < nv && c < emb) {
+          acc[v].x += x[b][v].x; acc[v].y += x[b][v].y; acc[v].z += x[b][v].z; acc[v].w += x[b][v].w;
+        }
       }
     }
   }

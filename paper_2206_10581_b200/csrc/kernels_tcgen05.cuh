@@ -146,9 +146,11 @@ __device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int n
 // Forward: P_F tiles on the tensor pipe, saved to Psave.
 template <int K, int BN, int RP>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
-  static_assert(BN % 16 == 0 && BN <= 256 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
+  static_assert(BN % 16 == 0 && BN <= 128 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
   constexpr int NPT = TC_BM / RP;
-  constexpr uint32_t TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // two accumulators: the epilogue of tile t-1 drains one while the MMAs of
+  // tile t fill the other (2 CTAs per SM x 256 columns = all of TMEM)
+  constexpr uint32_t TCOLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
   extern __shared__ __align__(128) uint8_t tsm[];
   uint8_t* S0 = tsm;
   uint8_t* S1 = S0 + K * BN * 2;
@@ -178,47 +180,58 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
   uint32_t phase = 0;
   const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
   ATileRegs<K, FB_THREADS> ar;
+  const int m = 32 * (warp & 3) + lane;  // epilogue row (TMEM lane)
+  const int mj = m / RP, ma = m - mj * RP;
+  const int c_lo = (warp >> 2) * (BN / 2);
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  // P_F rows of a finished tile: TMEM accumulator `acc` -> Psave
+  auto epilogue = [&](uint32_t tm, int acc, float* dst) {
+#pragma unroll 1
+    for (int c = c_lo; c < c_lo + BN / 2; c += 16) {
+      float v[16];
+      tc::tmem_ld16(tm + lane_base + acc * BN + c, v);
+      if (dst && !(a.mode & 4)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(dst + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    }
+  };
+  int t = 0;
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
     tc_load_A<K, RP, FB_THREADS>(a, 0, min(NPT, nbn), s_aoff, ar);
-    for (int tb = 0; tb < nbn; tb += NPT) {
+    float* pend = nullptr;  // destination row of the tile whose epilogue is pending
+    bool pending = false;
+    for (int tb = 0; tb < nbn; tb += NPT, ++t) {
       const int nn = min(NPT, nbn - tb);
       if (!(a.mode & 8)) tc_store_A<K, FB_THREADS>(ar, A0, A1, A2);
       tc::fence_async_smem();
       tc::before_sync();
-      __syncthreads();
+      __syncthreads();  // A planes written; the previous epilogue's reads of this accumulator are done
       tc::after_sync();
       const uint32_t tm = tslot;
       if (threadIdx.x == 0) {
         const tc::Operand oa = tc::kmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
         const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm, oa, ob, K, idesc, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm + (t & 1) * BN, oa, ob, K, idesc, false);
         tc::commit(&bar);
       }
       __syncwarp();
-      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, FB_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);  // under the MMA
-      tc::mbar_wait(&bar, phase);
+      float* dst = mj < nn ? a.Psave + ((int64_t)s_node[tb + mj] * RP + ma) * a.NC + cb * BN : nullptr;
+      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, FB_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+      if (pending) epilogue(tm, (t - 1) & 1, pend);  // under this tile's MMAs
+      tc::mbar_wait(&bar, phase);  // this tile's MMAs (A planes free again)
       phase ^= 1;
       tc::after_sync();
-      // epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows), columns half w/4
-      const int m = 32 * (warp & 3) + lane;
-      const int j = m / RP;
-      const int c_lo = (warp >> 2) * (BN / 2);
-      float* dst = j < nn ? a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN : nullptr;
-#pragma unroll 1
-      for (int c = c_lo; c < c_lo + BN / 2; c += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + ((uint32_t)(32 * (warp & 3)) << 16) + c, v);
-        if (dst && !(a.mode & 4)) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(dst + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-      }
+      pend = dst;
+      pending = true;
       tc::before_sync();
-      __syncthreads();  // TMEM drained and A planes free before the next tile
     }
+    if (pending) epilogue(tslot, (t - 1) & 1, pend);
+    tc::before_sync();
+    __syncthreads();
   }
   if (warp == 0) tc::tmem_free<TCOLS>(tslot);
 }
@@ -235,7 +248,9 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   static_assert(BN == 128 && K % 16 == 0 && K <= 128 && TC_BM % RP == 0 && RP % 4 == 0, "tcgen05 backward shape");
   constexpr int T = TCB_THREADS;
   constexpr int NPT = TC_BM / RP;
-  constexpr uint32_t TCOLS = 2 * K <= 64 ? 64 : 2 * K <= 128 ? 128 : 256;
+  // TMEM: dG_F^T [0, K) + two dA accumulators [K, 3K) (tile t's MMAs fill one
+  // while the epilogue of tile t-1 drains the other)
+  constexpr uint32_t TCOLS = 3 * K <= 64 ? 64 : 3 * K <= 128 ? 128 : 256;
   constexpr int EC = K / 4;  // epilogue columns per warp (16 warps = 4 lane quadrants x 4 column slices)
   static_assert(EC == 8 || EC == 16, "epilogue column slice");
   extern __shared__ __align__(128) uint8_t tsm[];
@@ -332,11 +347,26 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
     }
   };
   float acc[4][8];
+  const int em = 32 * (warp & 3) + lane;  // epilogue row (TMEM lane)
+  const int emj = em / RP, ema = em - emj * RP;
+  // dA rows of a finished tile: accumulator `buf` -> dPc[(node, cb)][a][r]
+  auto epilogue = [&](uint32_t tm, int buf, float* dst) {
+    float v[EC];
+    if constexpr (EC == 16) tc::tmem_ld16(tm + lane_base + K + buf * K + eslice, v);
+    else tc::tmem_ld8(tm + lane_base + K + buf * K + eslice, v);
+    if (dst) {
+#pragma unroll
+      for (int q = 0; q < EC / 4; ++q)
+        *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  };
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
     tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
     compute_dC(0, min(NPT, nbn), acc);
+    float* pend = nullptr;
+    bool pending = false;
     for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
       const int nn = min(NPT, nbn - tb);
       if (!(a.mode & 8)) tc_store_A<K, T>(ar, A0, A1, A2);
@@ -356,37 +386,30 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
         if (!(a.mode & 2)) tc::mma_x3(tm, dcT, aB, TC_BM, id_g, tiles > 0);
         const tc::Operand dcK = tc::kmajor(d0, d1, d2, BN);   // A operand (m = row, k = col)
         const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm + K, dcK, sT, BN, id_a, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm + K + (tiles & 1) * K, dcK, sT, BN, id_a, false);
         tc::commit(&bar);
       }
       __syncwarp();
-      // this tile's epilogue row, then the next tile's inputs under the MMA
-      const int m = 32 * (warp & 3) + lane;
-      const int j = m / RP;
-      float* dst = (j < nn && !(a.mode & 4))
-                       ? a.dPc + ((int64_t)s_node[tb + j] * a.ncb + cb) * RP * K + (m - j * RP) * K + eslice
+      float* dst = (emj < nn && !(a.mode & 4))
+                       ? a.dPc + ((int64_t)s_node[tb + emj] * a.ncb + cb) * RP * K + ema * K + eslice
                        : nullptr;
+      // under this tile's MMAs: the previous tile's epilogue, then the next
+      // tile's A tile and dC unit
+      if (pending) epilogue(tm, (tiles - 1) & 1, pend);
       if (tb + NPT < nbn) {
         if (!(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
         compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
       }
-      tc::mbar_wait(&bar, phase);
+      tc::mbar_wait(&bar, phase);  // planes free for the next tile
       phase ^= 1;
       tc::after_sync();
-      // dA epilogue -> dPc[(node, cb)][a][r]
-      {
-        float v[EC];
-        if constexpr (EC == 16) tc::tmem_ld16(tm + lane_base + K + eslice, v);
-        else tc::tmem_ld8(tm + lane_base + K + eslice, v);
-        if (dst) {
-#pragma unroll
-          for (int q = 0; q < EC / 4; ++q)
-            *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-      }
+      pend = dst;
+      pending = true;
       tc::before_sync();
-      __syncthreads();
     }
+    if (pending) epilogue(tslot, (tiles - 1) & 1, pend);
+    tc::before_sync();
+    __syncthreads();
   }
   // dG_F block: TMEM lane = column of the block, TMEM column = rank index r
   tc::after_sync();
