@@ -33,6 +33,18 @@ struct DevStatus {
 
 #define TT_NO_POS 0xFFFFFFFFFFFFFFFFull
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialisation (engine.cu tt_launch), lets its dependent grid be
+// scheduled once all of its CTAs are resident, and waits for the full
+// completion (and memory visibility) of the grid before it before touching
+// any data.  The dependency semantics are those of plain stream order; only
+// the launch latency between consecutive kernels overlaps.
+#define TT_PDL_ENTRY()                                         \
+  do {                                                         \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");         \
+  } while (0)
+
 __device__ __forceinline__ bool tt_failed(const DevStatus* st) {
   return *(volatile const unsigned long long*)&st->bad_pos != TT_NO_POS;
 }

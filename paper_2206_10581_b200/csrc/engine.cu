@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <string>
 #include <vector>
+#include <utility>
 
 #include "../../include/tt_engine.h"
 #include "common.cuh"
@@ -238,10 +239,42 @@ int ensure_generic(tt_engine* h) {
   return TT_OK;
 }
 
-#define LAUNCH(kernel, grid, block, smem, stream, ...)            \
-  do {                                                            \
-    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);   \
-    ++h->launches;                                                \
+// Eager launches use programmatic stream serialisation (PDL): the next kernel
+// of the step is scheduled while the previous one drains, and waits
+// (griddepcontrol.wait, TT_PDL_ENTRY) for its completion -- 0.20 -> 0.16 ms
+// for the plan at papers.  Under stream capture the attribute is left off:
+// a replayed graph already launches back to back, and programmatic edges
+// measured slower there (papers step 2.70 -> 2.80 ms).  TT_NO_PDL=1 turns it
+// off everywhere (A/B).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+void tt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  cfg.numAttrs = (pdl_enabled() && cs == cudaStreamCaptureStatusNone) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                          \
+  do {                                                                          \
+    tt_launch(kernel, dim3(grid), dim3(block), (size_t)(smem), (stream), __VA_ARGS__); \
+    ++h->launches;                                                              \
   } while (0)
 
 template <class K>
@@ -283,8 +316,10 @@ void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int na
   LAUNCH(k_scan_add, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
 }
 
-__global__ void k_set_int(int* p, int v) { *p = v; }
+__global__ void k_set_int(int* p, int v) {
+  TT_PDL_ENTRY(); *p = v; }
 __global__ void k_reset_status(DevStatus* st, int which) {
+  TT_PDL_ENTRY();
   if (which & 1) st->bad_pos = TT_NO_POS;
   if (which & 2) st->bad_core = INT_MAX;
 }
@@ -428,7 +463,7 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
 #define FUSED_LAUNCH_T(KER, SMEM, GRID, THREADS, S, ARGS)                                    \
   do {                                                                                       \
     CU(cudaFuncSetAttribute(KER, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM)));   \
-    KER<<<(GRID), (THREADS), (SMEM), (S)>>>(ARGS);                                           \
+    tt_launch(KER, dim3(GRID), dim3(THREADS), (size_t)(SMEM), (S), ARGS);                     \
     ++h->launches;                                                                           \
   } while (0)
 #define FUSED_LAUNCH(KER, SMEM, GRID, S, ARGS) FUSED_LAUNCH_T(KER, SMEM, GRID, FB_THREADS, S, ARGS)

@@ -319,6 +319,7 @@ __device__ __forceinline__ void transpose_reduce(float (&v)[V], int lane) {
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
+  TT_PDL_ENTRY();
   constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
   using CM = ColMap<BN>;
   constexpr int W4 = CM::W4, NQ = CM::NQ, LPJ = K / W4;
@@ -468,6 +469,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fused_bwd(FusedArgs a) {
+  TT_PDL_ENTRY();
   constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP;
   constexpr int WE = K * NL;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
@@ -704,6 +706,7 @@ __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp,
 template <int K, int NL>
 __global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const int* __restrict__ counts,
                                                               const int* __restrict__ parentL) {
+  TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
   const int U = ld_count(&counts[a.c.d - 1]);
@@ -767,6 +770,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const
 template <int K, int NL>
 __global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const int* __restrict__ counts,
                                                            const int* __restrict__ parentL) {
+  TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
   constexpr int RPL = K >= 32 ? K / 32 : 1;
@@ -823,6 +827,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const in
 __global__ void __launch_bounds__(256) k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __restrict__ goffL,
                                                            const int* __restrict__ orderL, const float* __restrict__ W,
                                                            float* __restrict__ grads, const DevStatus* st) {
+  TT_PDL_ENTRY();
   __shared__ float4 red[256];
   if (tt_failed(st)) return;
   const int v = blockIdx.x;
@@ -874,6 +879,7 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
                                         const int* __restrict__ cstart_pm1, const int* __restrict__ digit0,
                                         const float* __restrict__ dPc, float* __restrict__ dst,
                                         const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int cnt = ld_count(&counts[F - 1]);
   const int64_t total = (int64_t)cnt * per;

@@ -34,6 +34,7 @@ __global__ void k_gen_fwd_level(DevCfg c, int k, const float* __restrict__ param
                                 const int* __restrict__ parent_k, const int* __restrict__ digit0,
                                 const int* __restrict__ seg, const int* __restrict__ spos,
                                 float* __restrict__ out, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int cnt = ld_count(&counts[k]);
   const int64_t rows = c.rows[k], cols = c.cols[k], K = c.R[k];
@@ -60,6 +61,7 @@ __global__ void k_gen_fwd_level(DevCfg c, int k, const float* __restrict__ param
 __global__ void k_gen_dy(DevCfg c, const float* __restrict__ up, const int* __restrict__ counts,
                          const int* __restrict__ seg, const int* __restrict__ spos, float* __restrict__ dY,
                          const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int U = ld_count(&counts[c.d - 1]);
   const int64_t per = c.npad, total = (int64_t)U * per;
@@ -77,6 +79,7 @@ __global__ void k_gen_dy(DevCfg c, const float* __restrict__ up, const int* __re
 __global__ void k_gen_bwd_input(DevCfg c, int k, const float* __restrict__ params, LevelBufs L,
                                 const int* __restrict__ counts, const int* __restrict__ digit_k,
                                 const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int cnt = ld_count(&counts[k]);
   const int64_t rows = c.rows[k], cols = c.cols[k], K = c.R[k];
@@ -100,6 +103,7 @@ __global__ void k_gen_bwd_weight(DevCfg c, int k, const float* __restrict__ para
                                  const int* __restrict__ goff, const int* __restrict__ order,
                                  const int* __restrict__ parent_k, const int* __restrict__ digit0,
                                  float* __restrict__ grads, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int64_t rows = c.rows[k], cols = c.cols[k], K = c.R[k];
   const int64_t per = K * cols, total = c.m[k] * per;
@@ -123,6 +127,7 @@ __global__ void k_gen_bwd_weight(DevCfg c, int k, const float* __restrict__ para
 // dP[k-1][p] = sum of dPc[k][children of p] (children contiguous, ascending)
 __global__ void k_gen_reduce_children(DevCfg c, int k, LevelBufs L, const int* __restrict__ counts,
                                       const int* __restrict__ cstart_km1, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int cnt = ld_count(&counts[k - 1]);
   const int64_t per = c.rows[k] * c.R[k], total = (int64_t)cnt * per;
@@ -138,6 +143,7 @@ __global__ void k_gen_reduce_children(DevCfg c, int k, LevelBufs L, const int* _
 // dG_0[i_1] = dP[0][node] (level-0 nodes are distinct digits)
 __global__ void k_gen_bwd_core0(DevCfg c, LevelBufs L, const int* __restrict__ counts,
                                 const int* __restrict__ digit0, float* __restrict__ grads, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int cnt = ld_count(&counts[0]);
   const int64_t per = c.cols[0], total = (int64_t)cnt * per;
@@ -151,6 +157,7 @@ __global__ void k_gen_bwd_core0(DevCfg c, LevelBufs L, const int* __restrict__ c
 // touch counters: tc[k][v] = nodes with digit v at level k (0 = untouched)
 __global__ void k_touch_counters(DevCfg c, int k, const int* __restrict__ goff, float* __restrict__ grads,
                                  int accumulate, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= c.m[k]) return;

@@ -16,6 +16,7 @@ namespace tt {
 __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B, int64_t num_nodes,
                                      unsigned long long* __restrict__ keys, int* __restrict__ pos,
                                      DevStatus* st) {
+  TT_PDL_ENTRY();
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= B) return;
   int64_t id = idx[b];
@@ -49,6 +50,7 @@ __device__ __forceinline__ int rs_count(const int* n_dev, int n_host) { return n
 template <class K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, const int* n_dev, int n_host,
                                                         int shift, int nbits, int* __restrict__ hist) {
+  TT_PDL_ENTRY();
   __shared__ int cnt[RS_MAXBINS];
   const int n = rs_count(n_dev, n_host);
   const int base = blockIdx.x * RS_TILE;
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
 constexpr int RS_CS_SEG = 8;
 __global__ void __launch_bounds__(32 * RS_CS_SEG) k_rs_colscan(int* __restrict__ hist, int* __restrict__ tot,
                                                              const int* n_dev, int n_host, int nbits) {
+  TT_PDL_ENTRY();
   __shared__ int part[RS_CS_SEG][33];
   const int bins = 1 << nbits;
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
                                                            K* __restrict__ kout, int* __restrict__ vout,
                                                            const int* n_dev, int n_host, int shift, int nbits,
                                                            const int* __restrict__ colpre, const int* __restrict__ tot) {
+  TT_PDL_ENTRY();
   extern __shared__ int rs_smem[];
   int* cnt = rs_smem;                            // [RS_WARPS][bins]
   const int bins = 1 << nbits;
@@ -230,6 +234,7 @@ __device__ __forceinline__ int block_excl_scan_256(int t, int* wsum, int& total)
 __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a, int64_t stride,
                                                             const int* n_dev, int* __restrict__ partial,
                                                             int nblk) {
+  TT_PDL_ENTRY();
   __shared__ int wsum[SC_THREADS / 32];
   const int n = ld_count(n_dev);
   int* arr = a + blockIdx.y * stride;
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a,
 }
 
 __global__ void __launch_bounds__(1024) k_scan_partials(int* __restrict__ partial, int nblk) {
+  TT_PDL_ENTRY();
   // exclusive scan of partial[blockIdx.x * nblk ..]
   __shared__ int wsum[32];
   __shared__ int carry;
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(1024) k_scan_partials(int* __restrict__ partia
 
 __global__ void __launch_bounds__(SC_THREADS) k_scan_add(int* __restrict__ a, int64_t stride, const int* n_dev,
                                                          const int* __restrict__ partial, int nblk) {
+  TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   if (blockIdx.x == 0 || blockIdx.x * SC_BLOCK >= n) return;
   int* arr = a + blockIdx.y * stride;
@@ -306,6 +313,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_add(int* __restrict__ a, in
 // unique IDs over the sorted keys
 __global__ void k_unique_flags(const unsigned long long* __restrict__ skey, int B, int* __restrict__ flag,
                                const DevStatus* st) {
+  TT_PDL_ENTRY();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B || tt_failed(st)) return;
   flag[s] = (s == 0 || skey[s] != skey[s - 1]) ? 1 : 0;
@@ -316,6 +324,7 @@ __global__ void k_unique_flags(const unsigned long long* __restrict__ skey, int 
 __global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B, const int* __restrict__ scan,
                               unsigned long long* __restrict__ uniq, int* __restrict__ seg,
                               int* __restrict__ counts, int d, const DevStatus* st) {
+  TT_PDL_ENTRY();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B) return;
   if (tt_failed(st)) {
@@ -338,6 +347,7 @@ __global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B
 // at unique u.  flags laid out [k][cap].
 __global__ void k_level_flags(DevCfg c, const unsigned long long* __restrict__ uniq, const int* __restrict__ counts,
                               int* __restrict__ flags, int64_t cap) {
+  TT_PDL_ENTRY();
   const int U = ld_count(&counts[c.d - 1]);
   int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= U) return;
@@ -354,6 +364,7 @@ __global__ void k_level_emit(DevCfg c, const unsigned long long* __restrict__ un
                              const int* __restrict__ scan /*[k][cap] inclusive*/, int64_t cap,
                              int* __restrict__ digit /*[k][cap]*/, int* __restrict__ parent,
                              int* __restrict__ first) {
+  TT_PDL_ENTRY();
   const int U = ld_count(&counts[c.d - 1]);
   int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= U) return;
@@ -378,6 +389,7 @@ __global__ void k_level_emit(DevCfg c, const unsigned long long* __restrict__ un
 // child ranges: level-k node n owns level-(k+1) nodes [cs[n], cs[n+1]).
 __global__ void k_children(DevCfg c, const int* __restrict__ counts, const int* __restrict__ scan, int64_t cap,
                            const int* __restrict__ first, int* __restrict__ cstart /*[k][cap+1]*/) {
+  TT_PDL_ENTRY();
   const int k = blockIdx.y;  // 0 .. d-2
   const int cnt = ld_count(&counts[k]);
   int nd = blockIdx.x * blockDim.x + threadIdx.x;
@@ -394,6 +406,7 @@ __global__ void k_children(DevCfg c, const int* __restrict__ counts, const int* 
 // copy node digits into sort keys (values = node index)
 __global__ void k_digits_to_keys(const int* __restrict__ digit, const int* n_dev, unsigned* __restrict__ keys,
                                  int* __restrict__ vals) {
+  TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -409,6 +422,7 @@ struct GroupOffArgs {
 
 // all levels at once: blockIdx.y = level
 __global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ counts) {
+  TT_PDL_ENTRY();
   const int k = blockIdx.y;
   const int n = ld_count(&counts[k]);
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -424,6 +438,7 @@ __global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ cou
 
 // goff[v] = first slot whose sorted digit >= v, v in [0, m]
 __global__ void k_group_offsets(const unsigned* __restrict__ sdig, const int* n_dev, int m, int* __restrict__ goff) {
+  TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > m) return;
@@ -437,11 +452,13 @@ __global__ void k_group_offsets(const unsigned* __restrict__ sdig, const int* n_
 
 // level 0 (i_1 nodes): already sorted by digit and unique -> identity order
 __global__ void k_iota(int* __restrict__ a, const int* n_dev) {
+  TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
 }
 __global__ void k_digits_copy_u32(const int* __restrict__ digit, const int* n_dev, unsigned* __restrict__ out) {
+  TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (unsigned)digit[i];

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
                                                    const int* __restrict__ uid1, const int* __restrict__ spos,
                                                    const int* __restrict__ seg, float* __restrict__ dY,
                                                    float* __restrict__ part, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(256) k_dy_groups(int B, int64_t npad, const in
                                                    const int* __restrict__ seg, const float* __restrict__ part,
                                                    float* __restrict__ gpart, float* __restrict__ dY,
                                                    const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int G = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
                                                   const int* __restrict__ seg, const float* __restrict__ part,
                                                   const float* __restrict__ gpart, float* __restrict__ dY,
                                                   const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int U = ld_count(&counts[d - 1]);
   const int lane = threadIdx.x & 31;
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(256) k_scatter_heavy(int B, int64_t emb, int64
                                                        const int* __restrict__ spos, const int* __restrict__ seg,
                                                        const float* __restrict__ Yu, float* __restrict__ out,
                                                        const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   const int64_t per = emb / 4;
   const int64_t total = (int64_t)B * per;

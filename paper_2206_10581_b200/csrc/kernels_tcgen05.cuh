@@ -146,6 +146,7 @@ __device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int n
 // Forward: P_F tiles on the tensor pipe, saved to Psave.
 template <int K, int BN, int RP>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
+  TT_PDL_ENTRY();
   static_assert(BN % 16 == 0 && BN <= 128 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
   constexpr int NPT = TC_BM / RP;
   // two accumulators: the epilogue of tile t-1 drains one while the MMAs of
@@ -245,6 +246,7 @@ constexpr int TCB_THREADS = 512;
 
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
+  TT_PDL_ENTRY();
   static_assert(BN == 128 && K % 16 == 0 && K <= 128 && TC_BM % RP == 0 && RP % 4 == 0, "tcgen05 backward shape");
   constexpr int T = TCB_THREADS;
   constexpr int NPT = TC_BM / RP;

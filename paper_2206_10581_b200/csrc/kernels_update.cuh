@@ -26,6 +26,7 @@ __device__ __forceinline__ void locate(const DevCfg& c, int64_t e, int& k, int64
 // Vectorised over 4-element groups when every core offset and slice size is a
 // multiple of 4 (then a group never straddles slices); scalar otherwise.
 __global__ void k_check_finite(DevCfg c, const float* __restrict__ grads, int vec4, DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st)) return;
   int bad = INT_MAX;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
@@ -73,6 +74,7 @@ template <int KIND>
 __global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restrict__ grads, float* __restrict__ s1,
                          float* __restrict__ s2, int vec4, float lr, float b1, float b2, float eps,
                          const long long* __restrict__ step_ptr, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (tt_failed(st) || ld_count(&st->bad_core) != INT_MAX) return;
   float bc1 = 1.f, bc2 = 1.f;
   if (KIND == 1) {
@@ -119,17 +121,20 @@ __global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restric
 }
 
 __global__ void k_commit_step(long long* step_ptr, const DevStatus* st) {
+  TT_PDL_ENTRY();
   if (!tt_failed(st) && ld_count(&st->bad_core) == INT_MAX) *step_ptr += 1;
 }
 
 // zero the gradient values of the slices touched by the current batch only
 __global__ void k_zero_grads(float* __restrict__ g, int64_t n) {
+  TT_PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     g[e] = 0.f;
 }
 
 // FFMA throughput microbenchmark: 8 independent chains per thread.
 __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float a, float b) {
+  TT_PDL_ENTRY();
   float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
@@ -145,6 +150,7 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 // GEMM-like FFMA microbenchmark: an 8x8 register outer product per thread
 // (3-register FFMAs, operands reused as in an SGEMM micro-kernel).
 __global__ void __launch_bounds__(256) k_ffma_outer(float* out, int iters, float s0) {
+  TT_PDL_ENTRY();
   float a[8], b[8], acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
