@@ -29,6 +29,7 @@ using namespace tt;
 namespace {
 
 thread_local std::string g_err;
+long long* g_trace_buf = nullptr;  // TT_TC_TRACE: last backward's per-CTA timestamps
 thread_local int64_t g_err_pos = -1;
 thread_local int64_t g_err_val = 0;
 
@@ -517,7 +518,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
   f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints + sizeof(int) * (3 * FB_IDS + 8) + 16;
   f.CHF = 0;
-  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * BN) + ints;
+  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * BN) + ints + sizeof(int) * (FB_IDS + 8);
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
 #define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && f.BNf == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;
@@ -654,6 +655,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     if (h->last_path == 2) {
       a.ncb = h->ts.ncbb;
       if (getenv("TT_TC_BVARIANT")) a.mode = atoi(getenv("TT_TC_BVARIANT"));
+      static long long* trace_buf = nullptr;
+      if (getenv("TT_TC_TRACE")) {
+        if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 4096 * 64);
+        cudaMemsetAsync(trace_buf, 0, sizeof(long long) * 4096 * 64, s);
+        a.dbg = trace_buf;
+        g_trace_buf = trace_buf;
+      }
       const int grid = (int)(c.m[f.F] * h->ts.ncbb);
       rc = TT_OK;
       if (false) {
@@ -663,6 +671,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
       TT_TC_SHAPES(TT_TC_BWD_CASE)
 #undef TT_TC_BWD_CASE
     } else {
+      static long long* trace_buf2 = nullptr;
+      if (getenv("TT_TC_TRACE")) {
+        if (!trace_buf2) cudaMalloc(&trace_buf2, sizeof(long long) * 4096 * 64);
+        cudaMemsetAsync(trace_buf2, 0, sizeof(long long) * 4096 * 64, s);
+        a.dbg = trace_buf2;
+        g_trace_buf = trace_buf2;
+      }
       rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
     }
   }
@@ -1291,6 +1306,15 @@ int64_t tt_plan_sorted(tt_engine* h, int64_t* keys, int32_t* pos, int64_t capn) 
 }
 
 int64_t tt_launch_count(tt_engine* h) { return h ? h->launches : -1; }
+
+// debug: copy the tcgen05 backward's per-CTA phase timestamps (TT_TC_TRACE)
+int64_t tt_debug_trace(long long* out, int64_t n) {
+  if (!g_trace_buf) return 0;
+  cudaDeviceSynchronize();
+  n = std::min<int64_t>(n, 4096 * 64);
+  cudaMemcpy(out, g_trace_buf, sizeof(long long) * n, cudaMemcpyDeviceToHost);
+  return n;
+}
 
 int tt_set_profiling(tt_engine* h, int on) {
   if (!h) return fail(TT_ERR_ARG, "tt_set_profiling: null handle");

@@ -102,6 +102,7 @@ struct FusedArgs {
   float* dPc;
   float* grads;
   const DevStatus* st;
+  long long* dbg;  // optional per-CTA phase timestamps (TT_TC_TRACE builds only)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -487,7 +488,19 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;
   int* s_wsum = s_pref + FB_NB + 4;
+  int* s_bd = s_wsum + 8;  // [FB_IDS] last-core digits of the batch's first IDs (mode 0)
 
+  long long* trace = (a.dbg && blockIdx.x < 4096) ? a.dbg + (int64_t)blockIdx.x * 64 : nullptr;
+  int ntr = 0;
+  auto TR = [&]() {
+    if (trace && threadIdx.x == 0 && ntr < 63) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[1 + ntr++] = t;
+      trace[0] = ntr;
+    }
+  };
+  TR();
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
@@ -511,8 +524,21 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    if (a.mode == 0) {  // digits of the batch's IDs: one L2 round trip per batch, not per ID
+      const int tot = min(s_pref[nbn], FB_IDS);
+      for (int f = threadIdx.x; f < tot; f += FB_THREADS) {
+        int lo = 0, hi = nbn - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
+        }
+        s_bd[f] = __ldg(a.digitL + s_cs0[lo] + (f - s_pref[lo]));
+      }
+      __syncthreads();
+    }
     for (int tb = 0; tb < nbn; tb += NPT) {
       const int nn = min(NPT, nbn - tb);
+      TR();
       load_A_tile<K, RP>(a, tb, nn, s_aoff, As);
       if (a.mode == 1) {  // the materialised dC tile
         for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
@@ -541,7 +567,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
         for (int f = fA; f < fB; ++f) {
           const int u = cs0 + (f - fA);
-          const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
+          const float* Gp = Gl + (int64_t)(f < FB_IDS ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
           const float* Yp = a.dY + (int64_t)u * npad;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
@@ -582,6 +608,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         cp_async_wait<0>();  // slice block + A tile + dC tile
       }
       __syncthreads();
+      TR();
       // dG_F block += A^T dC  (operands double-buffered in registers)
       {
         auto ldA = [&](int m, float* av) {
@@ -617,6 +644,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
           fma_tile(a1, b1);
         }
       }
+      TR();
       // dA = dC . S_block^T  -> per-(node, column block) partials
       {
         const int kg = threadIdx.x % KG, mg = threadIdx.x / KG;
@@ -957,7 +985,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->CHF = (int)std::min<size_t>(32, base_f < half ? (half - base_f) / per_id : 0);
   if (s->CHF < 1) s->CHF = (int)std::min<size_t>(8, ((size_t)FB_SMEM_MAX - base_f) / per_id);
   s->smem_fwd = base_f + s->CHF * per_id;
-  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * BN) + ints;
+  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * BN) + ints + sizeof(int) * (FB_IDS + 8);
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
   s->CHB = 0;

@@ -273,6 +273,17 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
 
+  long long* trace = (a.dbg && blockIdx.x < 4096) ? a.dbg + (int64_t)blockIdx.x * 64 : nullptr;
+  int ntr = 0;
+  auto TR = [&]() {
+    if (trace && threadIdx.x == 0 && ntr < 63) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[1 + ntr++] = t;
+      trace[0] = ntr;
+    }
+  };
+  TR();
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[i][t] = 0.f;
     if (uj >= nn || (a.mode & 16)) return;
-    const int fA = s_pref[tb + uj], fB = s_pref[tb + uj + 1], cs0 = s_cs0[tb + uj];
+    const int fA = s_pref[tb + uj], fB = (a.mode & 64) ? min(s_pref[tb + uj + 1], s_pref[tb + uj] + 1) : s_pref[tb + uj + 1], cs0 = s_cs0[tb + uj];
     for (int f = fA; f < fB; ++f) {
       const int u = cs0 + (f - fA);
       const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL;
@@ -364,11 +375,11 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   };
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
+    TR();
     tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    TR();
     tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
     compute_dC(0, min(NPT, nbn), acc);
-    float* pend = nullptr;
-    bool pending = false;
     for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
       const int nn = min(NPT, nbn - tb);
       if (!(a.mode & 8)) tc_store_A<K, T>(ar, A0, A1, A2);
@@ -380,6 +391,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
       tc::before_sync();
       __syncthreads();
       tc::after_sync();
+      TR();
       const uint32_t tm = tslot;
       if (threadIdx.x == 0) {
         const uint32_t d0 = tc::smem_u32(D0), d1 = tc::smem_u32(D1), d2 = tc::smem_u32(D2);
@@ -395,21 +407,24 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
       float* dst = (emj < nn && !(a.mode & 4))
                        ? a.dPc + ((int64_t)s_node[tb + emj] * a.ncb + cb) * RP * K + ema * K + eslice
                        : nullptr;
-      // under this tile's MMAs: the previous tile's epilogue, then the next
-      // tile's A tile and dC unit
-      if (pending) epilogue(tm, (tiles - 1) & 1, pend);
+      // under this tile's MMAs: the next tile's A tile and dC unit (no TMEM
+      // access -- a tcgen05.ld issued now would queue behind the MMAs)
       if (tb + NPT < nbn) {
         if (!(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+        TR();
         compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
+      } else {
+        TR();
       }
+      TR();
       tc::mbar_wait(&bar, phase);  // planes free for the next tile
       phase ^= 1;
       tc::after_sync();
-      pend = dst;
-      pending = true;
+      TR();
+      epilogue(tm, tiles & 1, dst);
+      TR();
       tc::before_sync();
     }
-    if (pending) epilogue(tslot, (tiles - 1) & 1, pend);
     tc::before_sync();
     __syncthreads();
   }
@@ -428,6 +443,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   tc::before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_free<TCOLS>(tslot);
+  TR();
 }
 
 // (K, BNf, RP, NL) instantiations of the tensor-core path
