@@ -597,7 +597,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
       if (false) {
       }
 #define TT_TC_FWD_CASE(k_, bn_, rp_, nl_) \
-  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_tc_fwd<k_, bn_, rp_>), h->ts.smem_fwd, grid, s, a);
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_fwd<k_, bn_, rp_>), h->ts.smem_fwd, grid, TCF_THREADS, s, a);
       TT_TC_SHAPES(TT_TC_FWD_CASE)
 #undef TT_TC_FWD_CASE
       h->last_path = 2;

@@ -143,15 +143,25 @@ __device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int n
 }
 
 // ---------------------------------------------------------------------------
-// Forward: P_F tiles on the tensor pipe, saved to Psave.
+// Forward: P_F tiles on the tensor pipe, saved to Psave.  512 threads, one
+// CTA per SM.  The epilogue is store-bound (P_F is 666 MB at papers): warp w
+// drains TMEM lanes 32(w%4).. x columns 32(w/4).. of the accumulator, turns
+// its 32 x 32 chunk around in shared memory and writes 4 full 128-byte row
+// segments per store instruction (a TMEM lane per thread would write 32 rows
+// x 16 bytes per instruction, 8x the L2 requests).
+constexpr int TCF_THREADS = 512;
+constexpr int TCF_ES = 36;  // epilogue staging row stride (floats): conflict-free 16-byte stores and loads
+template <int K, int BN>
+constexpr size_t tc_fwd_smem_bytes() {
+  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + (size_t)(TCF_THREADS / 32) * 32 * TCF_ES * 4 + TC_META;
+}
+
 template <int K, int BN, int RP>
-__global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
-  TT_PDL_ENTRY();
-  static_assert(BN % 16 == 0 && BN <= 128 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
+__global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
+  static_assert(BN == 128 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
+  constexpr int T = TCF_THREADS;
   constexpr int NPT = TC_BM / RP;
-  // two accumulators: the epilogue of tile t-1 drains one while the MMAs of
-  // tile t fill the other (2 CTAs per SM x 256 columns = all of TMEM)
-  constexpr uint32_t TCOLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
+  constexpr uint32_t TCOLS = BN;
   extern __shared__ __align__(128) uint8_t tsm[];
   uint8_t* S0 = tsm;
   uint8_t* S1 = S0 + K * BN * 2;
@@ -159,7 +169,8 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
   uint8_t* A0 = S2 + K * BN * 2;
   uint8_t* A1 = A0 + TC_BM * K * 2;
   uint8_t* A2 = A1 + TC_BM * K * 2;
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(A2 + TC_BM * K * 2);
+  float* Es = reinterpret_cast<float*>(A2 + TC_BM * K * 2);  // [16 warps][32][TCF_ES]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Es + (T / 32) * 32 * TCF_ES);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;
@@ -177,60 +188,63 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_tc_fwd(FusedArgs a) {
     tc::mbar_init(&bar, 1);
     tc::fence_mbar_init();
   }
-  tc_stage_slice<K, BN, FB_THREADS>(a, g, cb, S0, S1, S2);
+  tc_stage_slice<K, BN, T>(a, g, cb, S0, S1, S2);
   uint32_t phase = 0;
   const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
-  ATileRegs<K, FB_THREADS> ar;
-  const int m = 32 * (warp & 3) + lane;  // epilogue row (TMEM lane)
-  const int mj = m / RP, ma = m - mj * RP;
-  const int c_lo = (warp >> 2) * (BN / 2);
+  ATileRegs<K, T> ar;
   const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-  // P_F rows of a finished tile: TMEM accumulator `acc` -> Psave
-  auto epilogue = [&](uint32_t tm, int acc, float* dst) {
-#pragma unroll 1
-    for (int c = c_lo; c < c_lo + BN / 2; c += 16) {
-      float v[16];
-      tc::tmem_ld16(tm + lane_base + acc * BN + c, v);
-      if (dst && !(a.mode & 4)) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<float4*>(dst + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      }
-    }
-  };
-  int t = 0;
+  const int ccol = (warp >> 2) * 32;          // this warp's 32 accumulator columns
+  float* Ew = Es + warp * 32 * TCF_ES;
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
-    prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    tc_load_A<K, RP, FB_THREADS>(a, 0, min(NPT, nbn), s_aoff, ar);
-    float* pend = nullptr;  // destination row of the tile whose epilogue is pending
-    bool pending = false;
-    for (int tb = 0; tb < nbn; tb += NPT, ++t) {
+    tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
+    for (int tb = 0; tb < nbn; tb += NPT) {
       const int nn = min(NPT, nbn - tb);
-      if (!(a.mode & 8)) tc_store_A<K, FB_THREADS>(ar, A0, A1, A2);
+      if (!(a.mode & 8)) tc_store_A<K, T>(ar, A0, A1, A2);
       tc::fence_async_smem();
       tc::before_sync();
-      __syncthreads();  // A planes written; the previous epilogue's reads of this accumulator are done
+      __syncthreads();  // A planes written; the previous tile's TMEM reads done
       tc::after_sync();
       const uint32_t tm = tslot;
       if (threadIdx.x == 0) {
         const tc::Operand oa = tc::kmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
         const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm + (t & 1) * BN, oa, ob, K, idesc, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm, oa, ob, K, idesc, false);
         tc::commit(&bar);
       }
       __syncwarp();
-      float* dst = mj < nn ? a.Psave + ((int64_t)s_node[tb + mj] * RP + ma) * a.NC + cb * BN : nullptr;
-      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, FB_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
-      if (pending) epilogue(tm, (t - 1) & 1, pend);  // under this tile's MMAs
-      tc::mbar_wait(&bar, phase);  // this tile's MMAs (A planes free again)
+      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+      tc::mbar_wait(&bar, phase);
       phase ^= 1;
       tc::after_sync();
-      pend = dst;
-      pending = true;
+      // epilogue: TMEM (row = lane) -> staging -> 4 rows x 128 B per store
+      {
+        float v[16];
+        tc::tmem_ld16(tm + lane_base + ccol, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        tc::tmem_ld16(tm + lane_base + ccol + 16, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 16 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+        const int c4 = (lane & 7) * 4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = (lane >> 3) + 4 * i;     // row within the warp's 32
+          const int m = 32 * (warp & 3) + r;     // tile row
+          const int j = m / RP;
+          const float4 x = *reinterpret_cast<const float4*>(Ew + r * TCF_ES + c4);
+          if (j < nn && !(a.mode & 4))
+            *reinterpret_cast<float4*>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN +
+                                       ccol + c4) = x;
+        }
+        __syncwarp();
+      }
       tc::before_sync();
     }
-    if (pending) epilogue(tslot, (t - 1) & 1, pend);
     tc::before_sync();
     __syncthreads();
   }
@@ -250,9 +264,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   static_assert(BN == 128 && K % 16 == 0 && K <= 128 && TC_BM % RP == 0 && RP % 4 == 0, "tcgen05 backward shape");
   constexpr int T = TCB_THREADS;
   constexpr int NPT = TC_BM / RP;
-  // TMEM: dG_F^T [0, K) + two dA accumulators [K, 3K) (tile t's MMAs fill one
-  // while the epilogue of tile t-1 drains the other)
-  constexpr uint32_t TCOLS = 3 * K <= 64 ? 64 : 3 * K <= 128 ? 128 : 256;
+  // TMEM: dG_F^T [0, K) + dA [K, 2K)
+  constexpr uint32_t TCOLS = 2 * K <= 64 ? 64 : 2 * K <= 128 ? 128 : 256;
   constexpr int EC = K / 4;  // epilogue columns per warp (16 warps = 4 lane quadrants x 4 column slices)
   static_assert(EC == 8 || EC == 16, "epilogue column slice");
   extern __shared__ __align__(128) uint8_t tsm[];
@@ -273,17 +286,6 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
 
-  long long* trace = (a.dbg && blockIdx.x < 4096) ? a.dbg + (int64_t)blockIdx.x * 64 : nullptr;
-  int ntr = 0;
-  auto TR = [&]() {
-    if (trace && threadIdx.x == 0 && ntr < 63) {
-      long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[1 + ntr++] = t;
-      trace[0] = ntr;
-    }
-  };
-  TR();
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
   const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
@@ -375,9 +377,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   };
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
-    TR();
     tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    TR();
     tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
     compute_dC(0, min(NPT, nbn), acc);
     for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
@@ -391,7 +391,6 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
       tc::before_sync();
       __syncthreads();
       tc::after_sync();
-      TR();
       const uint32_t tm = tslot;
       if (threadIdx.x == 0) {
         const uint32_t d0 = tc::smem_u32(D0), d1 = tc::smem_u32(D1), d2 = tc::smem_u32(D2);
@@ -400,7 +399,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
         if (!(a.mode & 2)) tc::mma_x3(tm, dcT, aB, TC_BM, id_g, tiles > 0);
         const tc::Operand dcK = tc::kmajor(d0, d1, d2, BN);   // A operand (m = row, k = col)
         const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm + K + (tiles & 1) * K, dcK, sT, BN, id_a, false);
+        if (!(a.mode & 2)) tc::mma_x3(tm + K, dcK, sT, BN, id_a, false);
         tc::commit(&bar);
       }
       __syncwarp();
@@ -411,18 +410,12 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
       // access -- a tcgen05.ld issued now would queue behind the MMAs)
       if (tb + NPT < nbn) {
         if (!(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
-        TR();
         compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
-      } else {
-        TR();
       }
-      TR();
       tc::mbar_wait(&bar, phase);  // planes free for the next tile
       phase ^= 1;
       tc::after_sync();
-      TR();
-      epilogue(tm, tiles & 1, dst);
-      TR();
+      epilogue(tm, 0, dst);
       tc::before_sync();
     }
     tc::before_sync();
@@ -443,7 +436,6 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   tc::before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_free<TCOLS>(tslot);
-  TR();
 }
 
 // (K, BNf, RP, NL) instantiations of the tensor-core path
@@ -461,9 +453,8 @@ inline bool tc_plan_shape(const FusedShape& f, TcShape* t) {
   t->ncbf = f.NC / 128;
   t->BNb = 128;
   t->ncbb = f.NC / 128;
-  t->smem_fwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 + TC_META;
-  // at most two forward CTAs per SM (TMEM: 2 x 128 columns)
-  t->smem_fwd = std::max<size_t>(t->smem_fwd, 80 * 1024);
+  t->smem_fwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 +
+                (size_t)(TCF_THREADS / 32) * 32 * TCF_ES * 4 + TC_META;
   t->smem_bwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 + 3 * (size_t)TC_BM * 128 * 2 + TC_META;
   t->ok = t->smem_bwd <= (size_t)FB_SMEM_MAX;
   return t->ok;
