@@ -127,6 +127,12 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
  * test constructed); every slice counts as touched by the next update. */
 int tt_set_core_grads_f64(tt_engine* h, const double* const* grads, int64_t batch_count);
 
+/* Optimizer state (checkpoint / resume; absent in the reference).
+ * Reference layout per core; s1 = Adagrad accumulator or Adam first moment,
+ * s2 = Adam second moment; NULL skips an array.  `step` is the update count. */
+int tt_opt_state_get_f64(tt_engine* h, double* const* s1, double* const* s2, int64_t* step);
+int tt_opt_state_set_f64(tt_engine* h, const double* const* s1, const double* const* s2, int64_t step);
+
 /* ---- data-parallel plumbing ------------------------------------------------
  * The gradient buffer is one contiguous fp32 array: every core's gradient
  * (device layout) followed by one touch counter per core slice.  With
@@ -159,6 +165,10 @@ int tt_set_profiling(tt_engine* h, int on);
 int tt_profile_read(tt_engine* h, double* ms, int64_t* counts, int nslots);
 /* Kernel launches issued by this handle since creation. */
 int64_t tt_launch_count(tt_engine* h);
+/* Debug: per-CTA phase timestamps of the last backward GEMM launch when the
+ * process runs with TT_TC_TRACE=1 (scripts/tc_trace.py); returns the number
+ * of int64 values copied (0 when tracing is off). */
+int64_t tt_debug_trace(long long* out, int64_t n);
 /* Selects the kernel family: 0 = auto (fused FFMA fast path where the shapes
  * allow), 1 = generic path only, 2 = fused with the optional tensor-core
  * 3xTF32 contraction where compiled for the shape (reported separately). */

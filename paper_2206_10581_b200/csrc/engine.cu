@@ -1018,6 +1018,53 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
   return TT_OK;
 }
 
+// Optimizer state in the reference layout (R_{k-1}, m_k, n_k, R_k): s1 is the
+// Adagrad accumulator / Adam first moment, s2 the Adam second moment (NULL
+// where the optimizer has none).  A checkpoint of these plus the cores and the
+// step counter resumes training bit-exactly (the reference has no resume,
+// SPEC.md:102; tt_io.py writes them next to the TTE1 core file).
+int tt_opt_state_get_f64(tt_engine* h, double* const* s1, double* const* s2, int64_t* step) {
+  if (!h) return fail(TT_ERR_ARG, "tt_opt_state_get: null handle");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  std::vector<float> buf((size_t)h->dc.nparams);
+  if (s1 && h->s1) {
+    CU(cudaMemcpy(buf.data(), h->s1, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    from_device_layout(h->dc, buf, s1, nullptr);
+  }
+  if (s2 && h->s2) {
+    CU(cudaMemcpy(buf.data(), h->s2, buf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    from_device_layout(h->dc, buf, s2, nullptr);
+  }
+  if (step) {
+    long long v = 0;
+    CU(cudaMemcpy(&v, h->d_step, sizeof(v), cudaMemcpyDeviceToHost));
+    *step = v;
+  }
+  return TT_OK;
+}
+
+int tt_opt_state_set_f64(tt_engine* h, const double* const* s1, const double* const* s2, int64_t step) {
+  if (!h) return fail(TT_ERR_ARG, "tt_opt_state_set: null handle");
+  if (step < 0) return fail(TT_ERR_ARG, "tt_opt_state_set: negative step");
+  if ((s1 && !h->s1) || (s2 && !h->s2))
+    return fail(TT_ERR_STATE, "tt_opt_state_set: the configured optimizer has no such state (call tt_opt_init)");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  std::vector<float> buf;
+  if (s1) {
+    to_device_layout(h->dc, s1, buf);
+    CU(cudaMemcpy(h->s1, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  if (s2) {
+    to_device_layout(h->dc, s2, buf);
+    CU(cudaMemcpy(h->s2, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  const long long v = step;
+  CU(cudaMemcpy(h->d_step, &v, sizeof(v), cudaMemcpyHostToDevice));
+  return TT_OK;
+}
+
 int tt_cores_snapshot(tt_engine* h, void* stream) {
   if (!h) return fail(TT_ERR_ARG, "tt_cores_snapshot: null handle");
   CU(cudaSetDevice(h->device));

@@ -86,13 +86,14 @@ __global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restric
   float dummy = 0.f;
   if (vec4) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < c.nparams / 4; q += stride) {
-      if (KIND != 1) {
-        int k;
-        int64_t v;
-        locate(c, q * 4, k, v);
-        if (!(grads[c.tc_off[k] + v] > 0.f)) continue;
-      }
-      const float4 g = reinterpret_cast<const float4*>(grads)[q];
+      int k;
+      int64_t v;
+      locate(c, q * 4, k, v);
+      const bool touched = grads[c.tc_off[k] + v] > 0.f;
+      if (KIND != 1 && !touched) continue;
+      // Adam runs densely; a slice this batch did not touch has g = 0 (the
+      // buffer may still hold an earlier batch's values there)
+      const float4 g = touched ? reinterpret_cast<const float4*>(grads)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 pv = reinterpret_cast<float4*>(p)[q];
       float4 hv = KIND != 0 ? reinterpret_cast<float4*>(s1)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 vv = KIND == 1 ? reinterpret_cast<float4*>(s2)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -106,14 +107,14 @@ __global__ void k_update(DevCfg c, float* __restrict__ p, const float* __restric
     }
   } else {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.nparams; e += stride) {
-      if (KIND != 1) {
-        int k;
-        int64_t v;
-        locate(c, e, k, v);
-        if (!(grads[c.tc_off[k] + v] > 0.f)) continue;
-      }
+      int k;
+      int64_t v;
+      locate(c, e, k, v);
+      const bool touched = grads[c.tc_off[k] + v] > 0.f;
+      if (KIND != 1 && !touched) continue;
       float h = KIND != 0 ? s1[e] : 0.f, v2 = KIND == 1 ? s2[e] : 0.f;
-      upd1<KIND>(p[e], grads[e], KIND != 0 ? s1[e] : dummy, KIND == 1 ? s2[e] : dummy, lr, b1, b2, eps, bc1, bc2);
+      upd1<KIND>(p[e], touched ? grads[e] : 0.f, KIND != 0 ? s1[e] : dummy, KIND == 1 ? s2[e] : dummy, lr, b1, b2, eps,
+                 bc1, bc2);
       (void)h;
       (void)v2;
     }

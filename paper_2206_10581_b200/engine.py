@@ -57,6 +57,7 @@ SYMBOLS = [
     "tt_train_step_host", "tt_get_core_grads_f64", "tt_set_core_grads_f64", "tt_grad_buffer", "tt_set_dense_grads", "tt_bind_grad_buffer",
     "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
+    "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_debug_trace",
 ]
 
 
@@ -93,6 +94,8 @@ def load_library(build_if_missing: bool = True):
         "tt_last_error_position": (i64, []), "tt_last_error_value": (i64, []),
         "tt_last_error": (C.c_char_p, []), "tt_ffma_peak_tflops": (dbl, [i32, i32]),
         "tt_ffma_outer_tflops": (dbl, [i32, i32]),
+        "tt_opt_state_get_f64": (i32, [vp, vp, vp, vp]), "tt_opt_state_set_f64": (i32, [vp, vp, vp, i64]),
+        "tt_debug_trace": (i64, [vp, i64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -374,6 +377,29 @@ class TTEmbedding:
 
     def launch_count(self) -> int:
         return int(self._lib.tt_launch_count(self._h))
+
+    def get_opt_state(self):
+        """(s1, s2, step): optimizer state in the reference core layout (fp64),
+        s1 = Adagrad accumulator / Adam first moment, s2 = Adam second moment;
+        None where the configured optimizer has no such state."""
+        cfg = self.config
+        kind = self._opt.kind if self._opt is not None else OptKind.sgd
+        s1 = [np.zeros(cfg.core_shape(k)) for k in range(cfg.d)] if kind != OptKind.sgd else None
+        s2 = [np.zeros(cfg.core_shape(k)) for k in range(cfg.d)] if kind == OptKind.adam else None
+        st = C.c_int64()
+        _raise(self._lib.tt_opt_state_get_f64(self._h, _ptr_array(s1, None) if s1 else None,
+                                              _ptr_array(s2, None) if s2 else None, C.byref(st)), "tt_opt_state_get")
+        return s1, s2, int(st.value)
+
+    def set_opt_state(self, s1, s2, step: int) -> None:
+        """Restores get_opt_state()'s arrays (after configure_optimizer)."""
+        cfg = self.config
+        a1 = [np.ascontiguousarray(x, np.float64).reshape(cfg.core_shape(k)) for k, x in enumerate(s1)] if s1 else None
+        a2 = [np.ascontiguousarray(x, np.float64).reshape(cfg.core_shape(k)) for k, x in enumerate(s2)] if s2 else None
+        _raise(self._lib.tt_opt_state_set_f64(self._h, _ptr_array(a1, None) if a1 else None,
+                                              _ptr_array(a2, None) if a2 else None, int(step)), "tt_opt_state_set")
+        if self._opt is not None:
+            self._opt.step = int(step)
 
     def opt_step(self) -> int:
         s = C.c_int64()
