@@ -707,7 +707,7 @@ constexpr int SK_WARPS = 8;
 template <int K>
 __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp, int nrow, float* buf, int lane) {
   const int n4 = nrow * (K / 4);
-  constexpr int B8 = 8;  // 8 independent 16-byte loads in flight per lane
+  constexpr int B8 = 16;  // the whole block (<= 2048 floats) in flight: one latency per ID
   for (int i0 = 0; i0 < n4; i0 += 32 * B8) {
     float4 v[B8];
 #pragma unroll
@@ -732,7 +732,7 @@ __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp,
 // outputs are contiguous, so a warp writes one contiguous output row per batch
 // position.  IDs with more than HEAVY_POS positions go to Yu (k_scatter_heavy).
 template <int K, int NL>
-__global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const int* __restrict__ counts,
+__global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, const int* __restrict__ counts,
                                                               const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32) k_last_level(FusedArgs a, const
 // the last core's gradient contributions.  Lane owns RPL rank rows and sums
 // over the block's nrow rows (no cross-lane reduction).
 template <int K, int NL>
-__global__ void __launch_bounds__(SK_WARPS * 32) k_fused_w(FusedArgs a, const int* __restrict__ counts,
+__global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const int* __restrict__ counts,
                                                            const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
