@@ -14,6 +14,6 @@ for path in auto tc; do
 done
 for path in auto tc; do
   CMD="python bench.py --config papers --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-tensor-path --path $path"
-  ncu --set full --clock-control none --import-source on -k regex:"k_fused_(fwd|bwd)<|k_tc_(fwd|bwd)" -c 2 -o gpurun_out/ev_full_$path $CMD > gpurun_out/ev_ncu_full_$path.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"k_fused_fwd|k_fused_bwd|k_tc_fwd|k_tc_bwd|k_last_level|k_fused_w" -c 4 -o gpurun_out/ev_full_$path $CMD > gpurun_out/ev_ncu_full_$path.log 2>&1
   python scripts/ncu_stalls.py gpurun_out/ev_full_$path.ncu-rep > gpurun_out/ev_stalls_$path.txt
 done
