@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-tensor-path", action="store_true", help="skip the tensor-core path measurement")
     p.add_argument("--shard", default="owner", choices=["owner", "position"], help="N > 1 decomposition (dist.py)")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: functional smoke test of the N > 1 path (ranks may share a GPU); not a measurement")
     p.add_argument("--graph", type=int, default=1, help="replay the step as one CUDA graph (1) or launch eagerly (0)")
     return p.parse_args()
 
@@ -185,9 +187,17 @@ def main():
     from paper_2206_10581_b200.config import WORKLOADS, workload_inputs
     from paper_2206_10581_b200.dist import DataParallelTT, OwnerShardedTT, shard_bounds
 
+    if a.dist_backend == "gloo":
+        # functional smoke test of the N > 1 code path on fewer GPUs than ranks:
+        # host-side collectives, so no kernel waits on another rank; never a
+        # measurement (the line says so)
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = a.config
     cfg, idx_all, up_all, cores = workload_inputs(name, a.seed)
     Bg = len(idx_all)
@@ -424,6 +434,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "ms_per_step_each": per_step, "tensor_path": tensor,
         }
+        if a.dist_backend == "gloo":
+            line["data"] = "synthetic; gloo smoke run of the N > 1 code path (ranks may share a GPU): not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -140,6 +140,17 @@ class Route:
         self.order, self.send_counts, self.recv_counts = order, send_counts, recv_counts
 
 
+def _a2a(dist, out, inp, out_splits, in_splits, group):
+    """all_to_all_single; under gloo (CPU collectives, smoke tests) CUDA
+    tensors hop through host memory."""
+    if inp.is_cuda and hasattr(dist, "get_backend") and dist.is_initialized() and dist.get_backend(group) == "gloo":
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
 def route_to_owners(cfg: TTConfig, idx, group=None, comm=None):
     """Send every local ID to its owner.  Returns (received IDs, Route).
     `comm` is torch.distributed (default) or an object with the same
@@ -151,10 +162,10 @@ def route_to_owners(cfg: TTConfig, idx, group=None, comm=None):
     order = torch.argsort(own, stable=True)
     counts = torch.bincount(own, minlength=world)
     rc = torch.empty_like(counts)
-    dist.all_to_all_single(rc, counts, group=group)
+    _a2a(dist, rc, counts, None, None, group)
     send, recv = counts.tolist(), rc.tolist()
     out = torch.empty(sum(recv), dtype=idx.dtype, device=idx.device)
-    dist.all_to_all_single(out, idx[order].contiguous(), recv, send, group=group)
+    _a2a(dist, out, idx[order].contiguous(), recv, send, group)
     return out, Route(order, send, recv)
 
 
@@ -163,7 +174,7 @@ def route_rows(rows, r: Route, group=None, comm=None):
     import torch
     dist = comm or __import__("torch.distributed", fromlist=["x"])
     out = torch.empty((sum(r.recv_counts),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
-    dist.all_to_all_single(out, rows[r.order].contiguous(), r.recv_counts, r.send_counts, group=group)
+    _a2a(dist, out, rows[r.order].contiguous(), r.recv_counts, r.send_counts, group)
     return out
 
 
@@ -172,7 +183,7 @@ def route_back(rows, r: Route, out=None, group=None, comm=None):
     import torch
     dist = comm or __import__("torch.distributed", fromlist=["x"])
     tmp = torch.empty((sum(r.send_counts),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
-    dist.all_to_all_single(tmp, rows.contiguous(), r.send_counts, r.recv_counts, group=group)
+    _a2a(dist, tmp, rows.contiguous(), r.send_counts, r.recv_counts, group)
     if out is None:
         out = torch.empty_like(tmp)
     out[r.order] = tmp
