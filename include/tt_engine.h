@@ -127,6 +127,13 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
  * test constructed); every slice counts as touched by the next update. */
 int tt_set_core_grads_f64(tt_engine* h, const double* const* grads, int64_t batch_count);
 
+/* Node relabelling (graph.cpp:218-252 apply_permutation after a hierarchical
+ * reorder): with a permutation set, ID v is served by row perm[v] in every
+ * lookup and backward (mapped on the device; range checks stay on v).  perm
+ * is a host array of num_nodes entries, a bijection on [0, num_nodes); NULL
+ * clears it.  TT_ERR_ARG on a size mismatch or a non-permutation. */
+int tt_set_permutation(tt_engine* h, const int64_t* perm, int64_t n);
+
 /* Optimizer state (checkpoint / resume; absent in the reference).
  * Reference layout per core; s1 = Adagrad accumulator or Adam first moment,
  * s2 = Adam second moment; NULL skips an array.  `step` is the update count. */

@@ -77,6 +77,7 @@ struct tt_engine {
   float* s1 = nullptr;
   float* s2 = nullptr;
   float* snap = nullptr;  // tt_cores_snapshot
+  int* perm = nullptr;    // tt_set_permutation (node relabelling), int32 on the device
   long long* d_step = nullptr;
   DevStatus* st = nullptr;
   int opt_kind = TT_OPT_SGD;
@@ -337,7 +338,8 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   h->last_idx = d_idx;
   LAUNCH(k_set_int, 1, 1, 0, s, h->counts + TT_MAXD, (int)B);
   h->d_B = h->counts + TT_MAXD;
-  LAUNCH(k_decompose_validate, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, c.num_nodes, h->keys_a, h->pos_a, h->st);
+  LAUNCH(k_decompose_validate, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, c.num_nodes, h->keys_a, h->pos_a, h->st,
+         (const int*)h->perm);
   const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
   h->skeys = radix_sort<unsigned long long>(h, s, h->keys_a, h->pos_a, h->keys_b, h->pos_b, nullptr, (int)B, B,
                                             idbits, &h->spos);
@@ -955,7 +957,8 @@ void tt_engine_destroy(tt_engine* h) {
   for (auto& v : h->prof_ev)
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
-  void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up};
+  void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up,
+                  h->perm};
   for (void* p : ptrs) cudaFree(p);
   if (h->own) cudaStreamDestroy(h->own);
   if (h->s_h2d) { cudaStreamSynchronize(h->s_h2d); cudaStreamDestroy(h->s_h2d); }
@@ -1023,6 +1026,38 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
 // where the optimizer has none).  A checkpoint of these plus the cores and the
 // step counter resumes training bit-exactly (the reference has no resume,
 // SPEC.md:102; tt_io.py writes them next to the TTE1 core file).
+// Node relabelling: after a hierarchical reorder
+// (partition.cpp:428-552 -> graph.cpp:218-252 apply_permutation) node v's row
+// is perm[v]; with a permutation set, every lookup / backward maps its IDs
+// through it on the device.  perm must be a bijection on [0, num_nodes);
+// NULL (or n == 0) clears it.
+int tt_set_permutation(tt_engine* h, const int64_t* perm, int64_t n) {
+  if (!h) return fail(TT_ERR_ARG, "tt_set_permutation: null handle");
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  if (!perm || n == 0) {
+    cudaFree(h->perm);
+    h->perm = nullptr;
+    h->plan_valid = false;
+    return TT_OK;
+  }
+  if (n != h->dc.num_nodes) return fail(TT_ERR_ARG, "apply_permutation: permutation size mismatch");
+  if (n > INT_MAX) return fail(TT_ERR_ARG, "tt_set_permutation: more than 2^31 nodes");
+  std::vector<int> p32((size_t)n);
+  std::vector<unsigned char> seen((size_t)n, 0);
+  for (int64_t v = 0; v < n; ++v) {
+    const int64_t t = perm[v];
+    if (t < 0 || t >= n || seen[(size_t)t])
+      return fail(TT_ERR_ARG, "tt_set_permutation: not a permutation of [0, num_nodes) (entry " + std::to_string(v) + ")");
+    seen[(size_t)t] = 1;
+    p32[(size_t)v] = (int)t;
+  }
+  if (!h->perm) CU(dalloc(&h->perm, n));
+  CU(cudaMemcpy(h->perm, p32.data(), sizeof(int) * (size_t)n, cudaMemcpyHostToDevice));
+  h->plan_valid = false;
+  return TT_OK;
+}
+
 int tt_opt_state_get_f64(tt_engine* h, double* const* s1, double* const* s2, int64_t* step) {
   if (!h) return fail(TT_ERR_ARG, "tt_opt_state_get: null handle");
   CU(cudaSetDevice(h->device));

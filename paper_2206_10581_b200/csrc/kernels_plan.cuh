@@ -13,9 +13,12 @@ namespace tt {
 // K1: validate every index (tt_embedding.cpp:112-117, autodiff.cpp:57-60) and
 // emit (key, position) pairs.  The minimum offending position is recorded
 // (the reference reports the first in input order).
+// perm (optional): the node relabelling of a hierarchical reorder
+// (graph.cpp:218-252 apply_permutation): row perm[id] serves id.  Validation
+// is on the caller's id.
 __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B, int64_t num_nodes,
                                      unsigned long long* __restrict__ keys, int* __restrict__ pos,
-                                     DevStatus* st) {
+                                     DevStatus* st, const int* __restrict__ perm) {
   TT_PDL_ENTRY();
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -26,7 +29,7 @@ __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B,
     // lowest bad lane of the warp reports: one atomic per warp
     if (bad && (ballot & lanemask_lt()) == 0) atomicMin(&st->bad_pos, (unsigned long long)b);
   }
-  keys[b] = bad ? 0ull : (unsigned long long)id;
+  keys[b] = bad ? 0ull : (unsigned long long)(perm ? (int64_t)__ldg(perm + id) : id);
   pos[b] = (int)b;
 }
 

@@ -57,7 +57,7 @@ SYMBOLS = [
     "tt_train_step_host", "tt_get_core_grads_f64", "tt_set_core_grads_f64", "tt_grad_buffer", "tt_set_dense_grads", "tt_bind_grad_buffer",
     "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
-    "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_debug_trace",
+    "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_debug_trace", "tt_set_permutation",
 ]
 
 
@@ -95,7 +95,7 @@ def load_library(build_if_missing: bool = True):
         "tt_last_error": (C.c_char_p, []), "tt_ffma_peak_tflops": (dbl, [i32, i32]),
         "tt_ffma_outer_tflops": (dbl, [i32, i32]),
         "tt_opt_state_get_f64": (i32, [vp, vp, vp, vp]), "tt_opt_state_set_f64": (i32, [vp, vp, vp, i64]),
-        "tt_debug_trace": (i64, [vp, i64]),
+        "tt_debug_trace": (i64, [vp, i64]), "tt_set_permutation": (i32, [vp, vp, i64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -377,6 +377,15 @@ class TTEmbedding:
 
     def launch_count(self) -> int:
         return int(self._lib.tt_launch_count(self._h))
+
+    def set_permutation(self, perm) -> None:
+        """Node relabelling of a hierarchical reorder (graph.cpp:218-252): ID v
+        is served by row perm[v] from now on (None clears)."""
+        if perm is None:
+            _raise(self._lib.tt_set_permutation(self._h, None, 0), "tt_set_permutation")
+            return
+        p = np.ascontiguousarray(perm, dtype=np.int64)
+        _raise(self._lib.tt_set_permutation(self._h, p.ctypes.data, len(p)), "tt_set_permutation")
 
     def get_opt_state(self):
         """(s1, s2, step): optimizer state in the reference core layout (fp64),
