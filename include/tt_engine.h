@@ -127,6 +127,16 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
  * test constructed); every slice counts as touched by the next update. */
 int tt_set_core_grads_f64(tt_engine* h, const double* const* grads, int64_t batch_count);
 
+/* init_ortho_core (initializer.cpp:103-132) computed on `device` in fp64:
+ * per core, n_k R_{k-1} orthonormal vectors of length m_k R_k (Gram-Schmidt
+ * with one re-orthogonalisation pass), vector (r, j) -> slice G_k(r,:,j,:),
+ * all cores scaled by target_scale^(1/2d) when target_scale > 0.  Writes
+ * host buffers in the reference layout (set them with tt_set_cores_f64).
+ * Infeasible ranks: TT_ERR_ARG and, if `bad` is non-NULL,
+ * bad = {core, vectors needed, vector length} (InfeasibleRanksError). */
+int tt_ortho_cores_f64(const tt_config_c* cfg, int device, uint64_t seed, double target_scale,
+                       double* const* cores, int64_t* bad);
+
 /* Node relabelling (graph.cpp:218-252 apply_permutation after a hierarchical
  * reorder): with a permutation set, ID v is served by row perm[v] in every
  * lookup and backward (mapped on the device; range checks stay on v).  perm

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_generic.cuh"
+#include "kernels_init.cuh"
 #include "kernels_plan.cuh"
 #include "kernels_rows.cuh"
 #include "kernels_tcgen05.cuh"
@@ -1031,6 +1032,78 @@ int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_cou
 // is perm[v]; with a permutation set, every lookup / backward maps its IDs
 // through it on the device.  perm must be a bijection on [0, num_nodes);
 // NULL (or n == 0) clears it.
+// init_ortho_core (initializer.cpp:103-132) on the device: fp64 cores in the
+// reference layout, written to host buffers (the caller sets them into an
+// engine, as the reference's initializer returns a TTEmbedding).
+int tt_ortho_cores_f64(const tt_config_c* cfgc, int device, uint64_t seed, double target_scale,
+                       double* const* cores, int64_t* bad) {
+  std::string why;
+  if (validate_cfg(cfgc, &why)) return fail(TT_ERR_ARG, why);
+  if (!cores) return fail(TT_ERR_ARG, "tt_ortho_cores_f64: null output");
+  const int d = cfgc->d;
+  for (int k = 0; k < d; ++k) {
+    const int64_t count = cfgc->col_factors[k] * cfgc->ranks[k];
+    const int64_t dim = cfgc->row_factors[k] * cfgc->ranks[k + 1];
+    if (count > dim) {
+      if (bad) { bad[0] = k; bad[1] = count; bad[2] = dim; }
+      return fail(TT_ERR_ARG, "ortho-core init infeasible at core " + std::to_string(k) + ": needs " +
+                                  std::to_string(count) + " orthonormal vectors of length " + std::to_string(dim) +
+                                  " (require n_k*R_{k-1} <= m_k*R_k)", k, count);
+    }
+  }
+  if (target_scale < 0.0) return fail(TT_ERR_ARG, "target_scale must be positive");  // 0: no rescaling
+  CU(cudaSetDevice(device));
+  const double c = target_scale > 0.0 ? std::pow(target_scale, 1.0 / (2.0 * d)) : 1.0;
+  for (int k = 0; k < d; ++k) {
+    const int64_t rp = cfgc->ranks[k], rn = cfgc->ranks[k + 1], m = cfgc->row_factors[k], n = cfgc->col_factors[k];
+    const int64_t count = n * rp, dim = m * rn;
+    double *Q = nullptr, *dots = nullptr, *sc = nullptr;
+    CU(cudaMalloc(&Q, sizeof(double) * (size_t)(count * dim)));
+    CU(cudaMalloc(&dots, sizeof(double) * (size_t)std::max<int64_t>(count, 1)));
+    CU(cudaMalloc(&sc, sizeof(double)));
+    auto cleanup = [&] { cudaFree(Q); cudaFree(dots); cudaFree(sc); };
+    const int gdim = (int)std::min<int64_t>((dim + 255) / 256, 148 * 8);
+    for (int64_t i = 0; i < count; ++i) {
+      double* v = Q + i * dim;
+      bool placed = false;
+      for (int attempt = 0; attempt < 8 && !placed; ++attempt) {
+        k_gs_draw<<<gdim, 256>>>(v, dim, (unsigned long long)seed, k, (int)i, attempt);
+        k_gs_sumsq<<<1, 256>>>(v, dim, sc);
+        double raw2 = 0, nrm2 = 0;
+        if (cudaMemcpy(&raw2, sc, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) { cleanup(); return fail(TT_ERR_CUDA, "ortho init"); }
+        for (int pass = 0; pass < 2 && i > 0; ++pass) {
+          k_gs_dots<<<(int)i, 256>>>(Q, v, dim, dots);
+          k_gs_axpy<<<gdim, 256>>>(Q, v, dim, dots, (int)i);
+        }
+        k_gs_sumsq<<<1, 256>>>(v, dim, sc);
+        if (cudaMemcpy(&nrm2, sc, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) { cleanup(); return fail(TT_ERR_CUDA, "ortho init"); }
+        const double raw = std::sqrt(raw2), nrm = std::sqrt(nrm2);
+        if (nrm > 1e-10 * raw && nrm > 0.0) {
+          k_gs_scale<<<gdim, 256>>>(v, dim, 1.0 / nrm);
+          placed = true;
+        }
+      }
+      if (!placed) {
+        cleanup();
+        return fail(TT_ERR_STATE, "gram_schmidt_rows: degenerate draws for vector " + std::to_string(i) + " after 8 retries");
+      }
+    }
+    std::vector<double> hq((size_t)(count * dim));
+    const cudaError_t e = cudaMemcpy(hq.data(), Q, sizeof(double) * hq.size(), cudaMemcpyDeviceToHost);
+    cleanup();
+    if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("ortho init: ") + cudaGetErrorString(e));
+    // vector (r, j) becomes the slice G_k(r, :, j, :), reshaped (m, R_k)
+    double* core = cores[k];
+    for (int64_t r = 0; r < rp; ++r)
+      for (int64_t j = 0; j < n; ++j) {
+        const double* vec = hq.data() + (r * n + j) * dim;
+        for (int64_t i2 = 0; i2 < m; ++i2)
+          for (int64_t s2 = 0; s2 < rn; ++s2) core[((r * m + i2) * n + j) * rn + s2] = c * vec[i2 * rn + s2];
+      }
+  }
+  return TT_OK;
+}
+
 int tt_set_permutation(tt_engine* h, const int64_t* perm, int64_t n) {
   if (!h) return fail(TT_ERR_ARG, "tt_set_permutation: null handle");
   CU(cudaSetDevice(h->device));

@@ -58,6 +58,7 @@ SYMBOLS = [
     "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
     "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_debug_trace", "tt_set_permutation",
+    "tt_ortho_cores_f64",
 ]
 
 
@@ -96,6 +97,7 @@ def load_library(build_if_missing: bool = True):
         "tt_ffma_outer_tflops": (dbl, [i32, i32]),
         "tt_opt_state_get_f64": (i32, [vp, vp, vp, vp]), "tt_opt_state_set_f64": (i32, [vp, vp, vp, i64]),
         "tt_debug_trace": (i64, [vp, i64]), "tt_set_permutation": (i32, [vp, vp, i64]),
+        "tt_ortho_cores_f64": (i32, [vp, i32, C.c_uint64, dbl, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
