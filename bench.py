@@ -106,6 +106,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _traffic(config_name, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(config_name, {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
+        return None
+
+
 def level_costs(cfg):
     """c_l = N_{l-1} R_{l-1} n_l R_l MACs for levels l = 2..d (0-based k = 1..d-1)."""
     out, N = [], cfg.n[0]
@@ -329,11 +338,36 @@ def main():
         if tc_run["path"] == "fused-tc":
             tf_ = algorithmic_flops(cfg, U)
             tc_ms = tc_run["t_max"] / a.steps
+            # dominant tensor kernel: k_tc_bwd (dG_F^T and dA on the tensor pipe,
+            # dC on the CUDA cores) -- algorithmic FLOPs per launch as for the
+            # FFMA kernel; the BF16x3 split issues 6 BF16 MMAs per algorithmic MAC
+            # of its two products, compared with the measured dense BF16 peak
+            costs_ = level_costs(cfg)
+            uf_cf_ = U[-2] * costs_[-2] if len(costs_) >= 2 else 0
+            ud_cd_ = U[-1] * costs_[-1]
+            bwd_ms = tc_run["phase_ms"].get("bwd_main", 0.0)
+            bwd_flops = 4.0 * uf_cf_ + 2.0 * ud_cd_
+            mma_flops = 6.0 * 4.0 * uf_cf_
+            peaks = {}
+            try:
+                peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            except (OSError, ValueError):
+                pass
+            bf16_peak = peaks.get("bf16_tflops")
             tensor = {"path": "fused-tc (tcgen05.mma kind::f16, BF16x3 six-product split, FP32 accumulate in TMEM)",
                       "value": Bg * a.steps / (tc_run["t_max"] / 1e3), "unit": "rows/s", "ms_per_step": tc_ms,
                       "ms_per_step_each": tc_run["per_step"], "phases_ms_per_step": tc_run["phase_ms"],
                       "tolerance": "|x - x_ref| <= 1e-5 a_ref (same bound as the FP32 path; tests/test_gpu_parity.py)",
                       "step_tflops": tf_ / (tc_ms * 1e-3) / 1e12,
+                      "roofline": {
+                          "bound": "tensor", "kernel": "k_tc_bwd", "unit": "TFLOP/s",
+                          "achieved": bwd_flops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None,
+                          "bf16_mma_tflops": mma_flops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None,
+                          "peak": bf16_peak, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst)",
+                          "frac": (mma_flops / (bwd_ms * 1e-3) / 1e12 / bf16_peak) if (bwd_ms > 0 and bf16_peak) else None,
+                          "traffic": _traffic(name, "k_tc_bwd"), "flops_per_launch": bwd_flops, "ms_per_launch": bwd_ms,
+                          "note": "frac = issued BF16 MMA FLOPs (6 per algorithmic MAC of dG_F and dA) over the "
+                                  "dense BF16 peak; the N = K = 64 MMAs are shared-memory bound (DESIGN.md c2)"},
                       "gpu_launches": tc_run["launches"]}
         emb.set_path(a.path)
 
