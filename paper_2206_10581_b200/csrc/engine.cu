@@ -249,6 +249,27 @@ int ensure_generic(tt_engine* h) {
 // a replayed graph already launches back to back, and programmatic edges
 // measured slower there (papers step 2.70 -> 2.80 ms).  TT_NO_PDL=1 turns it
 // off everywhere (A/B).
+// Diagnostic switches, read once per process (all off by default):
+//   TT_TC_VARIANT / TT_TC_BVARIANT = bit mask handed to the tcgen05 forward /
+//     backward as FusedArgs::mode to skip parts of the work for attribution
+//     (2 MMAs, 4 epilogue stores, 8 A staging, 16 dC formation, 32 dC planes,
+//     64 one ID per node); results are wrong while set (scripts/tc_variants.sh);
+//   TT_TC_TRACE = per-CTA phase timestamps of the backward GEMM kernels
+//     (tt_debug_trace, scripts/tc_trace.py).
+struct DiagEnv {
+  int tc_fwd_variant = 0, tc_bwd_variant = 0;
+  bool trace = false;
+  DiagEnv() {
+    if (const char* e = getenv("TT_TC_VARIANT")) tc_fwd_variant = atoi(e);
+    if (const char* e = getenv("TT_TC_BVARIANT")) tc_bwd_variant = atoi(e);
+    if (const char* e = getenv("TT_TC_TRACE")) trace = *e && *e != '0';
+  }
+};
+const DiagEnv& diag() {
+  static const DiagEnv d;
+  return d;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("TT_NO_PDL");
@@ -595,7 +616,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     Phase ph(h, 1, s);
     if (use_tc(h)) {
       a.ncb = h->ts.ncbf;
-      if (getenv("TT_TC_VARIANT")) a.mode = atoi(getenv("TT_TC_VARIANT"));
+      a.mode = diag().tc_fwd_variant;
       const int grid = (int)(c.m[f.F] * h->ts.ncbf);
       if (false) {
       }
@@ -657,9 +678,9 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     Phase ph(h, 2, s);
     if (h->last_path == 2) {
       a.ncb = h->ts.ncbb;
-      if (getenv("TT_TC_BVARIANT")) a.mode = atoi(getenv("TT_TC_BVARIANT"));
+      a.mode = diag().tc_bwd_variant;
       static long long* trace_buf = nullptr;
-      if (getenv("TT_TC_TRACE")) {
+      if (diag().trace) {
         if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 4096 * 64);
         cudaMemsetAsync(trace_buf, 0, sizeof(long long) * 4096 * 64, s);
         a.dbg = trace_buf;
@@ -675,7 +696,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
 #undef TT_TC_BWD_CASE
     } else {
       static long long* trace_buf2 = nullptr;
-      if (getenv("TT_TC_TRACE")) {
+      if (diag().trace) {
         if (!trace_buf2) cudaMalloc(&trace_buf2, sizeof(long long) * 4096 * 64);
         cudaMemsetAsync(trace_buf2, 0, sizeof(long long) * 4096 * 64, s);
         a.dbg = trace_buf2;
