@@ -206,7 +206,7 @@ int ensure_plan(tt_engine* h, int64_t B) {
   CU(dalloc(&h->uniq, cap));
   CU(dalloc(&h->pos_a, cap));
   CU(dalloc(&h->pos_b, cap));
-  CU(dalloc(&h->hist, ntiles * RS_MAXBINS + RS_MAXBINS));
+  CU(dalloc(&h->hist, (int64_t)TT_MAXD * (ntiles + 1) * RS_MAXBINS));  // rs_hist slots
   CU(dalloc(&h->flag, cap));
   CU(dalloc(&h->seg, cap + 1));
   CU(dalloc(&h->lflags, (int64_t)d * cap));
@@ -302,29 +302,38 @@ void tt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   } while (0)
 
 template <class K>
+void rs_set_attrs() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_rs_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SCATTER_SMEM);
+    done = true;
+  }
+}
+
+// hist/tot region of sort slot y: (ntiles + 1) * RS_MAXBINS ints each
+int* rs_hist(tt_engine* h, int y, int ntiles) { return h->hist + (int64_t)y * (ntiles + 1) * RS_MAXBINS; }
+
+template <class K>
 K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, const int* n_dev, int n_host,
               int64_t nmax, int nbits, int** vout) {
   const int ntiles = (int)((nmax + RS_TILE - 1) / RS_TILE);
   const int passes = (nbits + RS_MAXBITS - 1) / RS_MAXBITS;
   K* kin = ka; K* kout = kb;
   int* vin = va; int* vo = vb;
-  int* tot = h->hist + (int64_t)ntiles * RS_MAXBINS;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_rs_scatter<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)RS_SCATTER_SMEM);
-    cudaFuncSetAttribute(k_rs_scatter<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SCATTER_SMEM);
-    attr_set = true;
-  }
+  rs_set_attrs<K>();
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (nbits - shift + (passes - p) - 1) / (passes - p);  // split evenly
     const int bins = 1 << bits;
-    LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, kin, n_dev, n_host, shift, bits, h->hist);
-    LAUNCH(k_rs_colscan, (bins + 31) / 32, 32 * RS_CS_SEG, 0, s, h->hist, tot, n_dev, n_host, bits);
+    RSBatch<K> rb{};
+    rb.kin[0] = kin; rb.vin[0] = vin; rb.kout[0] = kout; rb.vout[0] = vo; rb.n_dev[0] = n_dev;
+    rb.hist[0] = rs_hist(h, 0, ntiles);
+    rb.tot[0] = rb.hist[0] + (int64_t)ntiles * RS_MAXBINS;
+    rb.n_host = n_host;
+    LAUNCH(k_rs_hist<K>, ntiles, RS_THREADS, 0, s, rb, shift, bits);
+    LAUNCH(k_rs_colscan<K>, (bins + 31) / 32, 32 * RS_CS_SEG, 0, s, rb, bits);
     const size_t smem = sizeof(int) * ((size_t)RS_WARPS * bins + bins + 64);
-    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, smem, s, kin, vin, kout, vo, n_dev, n_host, shift, bits, h->hist,
-           tot);
+    LAUNCH(k_rs_scatter<K>, ntiles, RS_THREADS, smem, s, rb, shift, bits);
     std::swap(kin, kout);
     std::swap(vin, vo);
     shift += bits;
@@ -333,15 +342,46 @@ K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, cons
   return kin;
 }
 
-void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax) {
+// The plan's per-level digit sorts (levels 1..d-1) in one pass for all levels
+// at once (3 launches instead of 4 per level): stable by node index.
+// Requires every m_k <= 2^RS_MAXBITS.
+void sort_levels(tt_engine* h, cudaStream_t s) {
+  const DevCfg& c = h->dc;
+  const int d = c.d;
+  const int64_t cap = h->cap;
+  const int ntiles = (int)((cap + RS_TILE - 1) / RS_TILE);
+  int nbits = 1;
+  for (int k = 1; k < d; ++k) nbits = std::max<int>(nbits, (int)bitlen((uint64_t)(c.m[k] - 1)));
+  rs_set_attrs<unsigned>();
+  RSBatch<unsigned> rb{};
+  for (int k = 1; k < d; ++k) {
+    const int y = k - 1;
+    rb.kin[y] = reinterpret_cast<const unsigned*>(h->digit + k * cap);
+    rb.vin[y] = nullptr;
+    rb.kout[y] = h->gk[k][1];
+    rb.vout[y] = h->gv[k][1];
+    rb.n_dev[y] = h->counts + k;
+    rb.hist[y] = rs_hist(h, 1 + y, ntiles);
+    rb.tot[y] = rb.hist[y] + (int64_t)ntiles * RS_MAXBINS;
+    h->sdig[k] = h->gk[k][1];
+    h->order[k] = h->gv[k][1];
+  }
+  rb.n_host = 0;
+  const int bins = 1 << nbits;
+  LAUNCH(k_rs_hist<unsigned>, dim3(ntiles, d - 1), RS_THREADS, 0, s, rb, 0, nbits);
+  LAUNCH(k_rs_colscan<unsigned>, dim3((bins + 31) / 32, d - 1), 32 * RS_CS_SEG, 0, s, rb, nbits);
+  const size_t smem = sizeof(int) * ((size_t)RS_WARPS * bins + bins + 64);
+  LAUNCH(k_rs_scatter<unsigned>, dim3(ntiles, d - 1), RS_THREADS, smem, s, rb, 0, nbits);
+}
+
+void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax,
+                    const unsigned long long* skey = nullptr) {
   const int nblk = (int)((nmax + SC_BLOCK - 1) / SC_BLOCK);
-  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
+  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk, skey);
   LAUNCH(k_scan_partials, narr, 1024, 0, s, h->partial, nblk);
   LAUNCH(k_scan_add, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
 }
 
-__global__ void k_set_int(int* p, int v) {
-  TT_PDL_ENTRY(); *p = v; }
 __global__ void k_reset_status(DevStatus* st, int which) {
   TT_PDL_ENTRY();
   if (which & 1) st->bad_pos = TT_NO_POS;
@@ -358,15 +398,13 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   const int64_t cap = h->cap;
   h->B = B;
   h->last_idx = d_idx;
-  LAUNCH(k_set_int, 1, 1, 0, s, h->counts + TT_MAXD, (int)B);
   h->d_B = h->counts + TT_MAXD;
   LAUNCH(k_decompose_validate, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, c.num_nodes, h->keys_a, h->pos_a, h->st,
-         (const int*)h->perm);
+         (const int*)h->perm, h->counts + TT_MAXD);
   const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
   h->skeys = radix_sort<unsigned long long>(h, s, h->keys_a, h->pos_a, h->keys_b, h->pos_b, nullptr, (int)B, B,
                                             idbits, &h->spos);
-  LAUNCH(k_unique_flags, grid_for(B, 256, INT_MAX), 256, 0, s, h->skeys, (int)B, h->flag, h->st);
-  scan_inclusive(h, s, h->flag, 0, 1, h->d_B, B);
+  scan_inclusive(h, s, h->flag, 0, 1, h->d_B, B, h->skeys);  // unique flags formed in the scan
   LAUNCH(k_unique_emit, grid_for(B, 256, INT_MAX), 256, 0, s, h->skeys, (int)B, h->flag, h->uniq, h->seg, h->counts,
          d, h->st);
   const int* U = h->counts + (d - 1);
@@ -377,18 +415,22 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   LAUNCH(k_children, dim3(grid_for(B + 1, 256, INT_MAX), d - 1), 256, 0, s, c, h->counts, h->lflags, cap, h->first,
          h->cstart);
   // digit groups: level 0 is already digit-sorted and distinct
-  LAUNCH(k_iota, grid_for(B, 256, INT_MAX), 256, 0, s, h->gv[0][0], h->counts);
-  LAUNCH(k_digits_copy_u32, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit, h->counts, h->gk[0][0]);
+  LAUNCH(k_level0_order, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit, h->counts, h->gv[0][0], h->gk[0][0]);
   h->order[0] = h->gv[0][0];
   h->sdig[0] = h->gk[0][0];
 
-  for (int k = 1; k < d; ++k) {
-    LAUNCH(k_digits_to_keys, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit + k * cap, h->counts + k, h->gk[k][0],
-           h->gv[k][0]);
-    const int nb = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.m[k] - 1)));
-    h->sdig[k] = radix_sort<unsigned>(h, s, h->gk[k][0], h->gv[k][0], h->gk[k][1], h->gv[k][1], h->counts + k, 0,
-                                      h->capk[k], nb, &h->order[k]);
-
+  bool batched = true;
+  for (int k = 1; k < d; ++k) batched = batched && bitlen((uint64_t)(c.m[k] - 1)) <= RS_MAXBITS;
+  if (batched) {
+    sort_levels(h, s);
+  } else {
+    for (int k = 1; k < d; ++k) {
+      LAUNCH(k_digits_to_keys, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit + k * cap, h->counts + k, h->gk[k][0],
+             h->gv[k][0]);
+      const int nb = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.m[k] - 1)));
+      h->sdig[k] = radix_sort<unsigned>(h, s, h->gk[k][0], h->gv[k][0], h->gk[k][1], h->gv[k][1], h->counts + k, 0,
+                                        h->capk[k], nb, &h->order[k]);
+    }
   }
   GroupOffArgs ga{};
   int64_t mmax = 0;

@@ -18,9 +18,10 @@ namespace tt {
 // is on the caller's id.
 __global__ void k_decompose_validate(const int64_t* __restrict__ idx, int64_t B, int64_t num_nodes,
                                      unsigned long long* __restrict__ keys, int* __restrict__ pos,
-                                     DevStatus* st, const int* __restrict__ perm) {
+                                     DevStatus* st, const int* __restrict__ perm, int* __restrict__ nB) {
   TT_PDL_ENTRY();
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b == 0) *nB = (int)B;  // the batch size as a device count
   if (b >= B) return;
   int64_t id = idx[b];
   bool bad = id < 0 || id >= num_nodes;
@@ -49,13 +50,30 @@ constexpr size_t RS_SCATTER_SMEM = sizeof(int) * ((size_t)RS_WARPS * RS_MAXBINS 
 
 __device__ __forceinline__ int rs_count(const int* n_dev, int n_host) { return n_dev ? ld_count(n_dev) : n_host; }
 
+// One launch sorts up to TT_MAXD independent arrays (blockIdx.y selects the
+// array): the ID sort uses one, the per-level digit sorts of the plan run
+// batched in a single pass.
+template <class K>
+struct RSBatch {
+  const K* kin[TT_MAXD];
+  const int* vin[TT_MAXD];  // nullptr: the value is the key's index
+  K* kout[TT_MAXD];
+  int* vout[TT_MAXD];
+  const int* n_dev[TT_MAXD];
+  int* hist[TT_MAXD];       // [tiles][bins] per-tile histograms -> exclusive column prefixes
+  int* tot[TT_MAXD];        // [bins] digit totals
+  int n_host;
+};
+
 // per-tile digit histogram -> hist[tile * bins + digit]
 template <class K>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, const int* n_dev, int n_host,
-                                                        int shift, int nbits, int* __restrict__ hist) {
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(RSBatch<K> rb, int shift, int nbits) {
   TT_PDL_ENTRY();
   __shared__ int cnt[RS_MAXBINS];
-  const int n = rs_count(n_dev, n_host);
+  const int y = blockIdx.y;
+  const K* __restrict__ keys = rb.kin[y];
+  int* __restrict__ hist = rb.hist[y];
+  const int n = rs_count(rb.n_dev[y], rb.n_host);
   const int base = blockIdx.x * RS_TILE;
   if (base >= n) return;
   const int bins = 1 << nbits;
@@ -75,10 +93,14 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
 // its segment with independent loads, the 8 segment totals are scanned in
 // shared memory, then each thread rewrites its segment as prefixes.
 constexpr int RS_CS_SEG = 8;
-__global__ void __launch_bounds__(32 * RS_CS_SEG) k_rs_colscan(int* __restrict__ hist, int* __restrict__ tot,
-                                                             const int* n_dev, int n_host, int nbits) {
+template <class K>
+__global__ void __launch_bounds__(32 * RS_CS_SEG) k_rs_colscan(RSBatch<K> rb, int nbits) {
   TT_PDL_ENTRY();
   __shared__ int part[RS_CS_SEG][33];
+  int* __restrict__ hist = rb.hist[blockIdx.y];
+  int* __restrict__ tot = rb.tot[blockIdx.y];
+  const int* n_dev = rb.n_dev[blockIdx.y];
+  const int n_host = rb.n_host;
   const int bins = 1 << nbits;
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
   const int dgt = blockIdx.x * 32 + lane;
@@ -123,11 +145,17 @@ __global__ void __launch_bounds__(32 * RS_CS_SEG) k_rs_colscan(int* __restrict__
 }
 
 template <class K>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const int* __restrict__ vin,
-                                                           K* __restrict__ kout, int* __restrict__ vout,
-                                                           const int* n_dev, int n_host, int shift, int nbits,
-                                                           const int* __restrict__ colpre, const int* __restrict__ tot) {
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(RSBatch<K> rb, int shift, int nbits) {
   TT_PDL_ENTRY();
+  const int y = blockIdx.y;
+  const K* __restrict__ kin = rb.kin[y];
+  const int* __restrict__ vin = rb.vin[y];
+  K* __restrict__ kout = rb.kout[y];
+  int* __restrict__ vout = rb.vout[y];
+  const int* n_dev = rb.n_dev[y];
+  const int n_host = rb.n_host;
+  const int* __restrict__ colpre = rb.hist[y];
+  const int* __restrict__ tot = rb.tot[y];
   extern __shared__ int rs_smem[];
   int* cnt = rs_smem;                            // [RS_WARPS][bins]
   const int bins = 1 << nbits;
@@ -193,7 +221,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     if (g < n) {
       const int dst = cnt[w * bins + dig] + __popc(peers & lanemask_lt());
       kout[dst] = key;
-      vout[dst] = vin[g];
+      vout[dst] = vin ? vin[g] : g;
     }
     __syncwarp();
     if (g < n && lane == 31 - __clz(peers)) cnt[w * bins + dig] += __popc(peers);
@@ -234,9 +262,11 @@ __device__ __forceinline__ int block_excl_scan_256(int t, int* wsum, int& total)
   return r;
 }
 
+// skey != nullptr: the scanned values are the unique-ID flags of the sorted
+// keys (1 where a new ID starts), computed here and not read from `a`
 __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a, int64_t stride,
                                                             const int* n_dev, int* __restrict__ partial,
-                                                            int nblk) {
+                                                            int nblk, const unsigned long long* __restrict__ skey) {
   TT_PDL_ENTRY();
   __shared__ int wsum[SC_THREADS / 32];
   const int n = ld_count(n_dev);
@@ -250,7 +280,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a,
   int t = 0;
 #pragma unroll
   for (int j = 0; j < SC_ITEMS; ++j) {
-    v[j] = (i0 + j < n) ? arr[i0 + j] : 0;
+    const int s = i0 + j;
+    v[j] = s < n ? (skey ? ((s == 0 || skey[s] != skey[s - 1]) ? 1 : 0) : arr[s]) : 0;
     t += v[j];
     v[j] = t;
   }
@@ -313,15 +344,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_add(int* __restrict__ a, in
 }
 
 // ---------------------------------------------------------------------------
-// unique IDs over the sorted keys
-__global__ void k_unique_flags(const unsigned long long* __restrict__ skey, int B, int* __restrict__ flag,
-                               const DevStatus* st) {
-  TT_PDL_ENTRY();
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= B || tt_failed(st)) return;
-  flag[s] = (s == 0 || skey[s] != skey[s - 1]) ? 1 : 0;
-}
-
+// unique IDs over the sorted keys (flags formed inside k_scan_blocks)
 // After the inclusive scan: uniq[u] = key, seg[u] = first sorted slot.
 // counts[d-1] = U, seg[U] = B.
 __global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B, const int* __restrict__ scan,
@@ -454,17 +477,16 @@ __global__ void k_group_offsets(const unsigned* __restrict__ sdig, const int* n_
 }
 
 // level 0 (i_1 nodes): already sorted by digit and unique -> identity order
-__global__ void k_iota(int* __restrict__ a, const int* n_dev) {
+// and the digits as the sorted keys
+__global__ void k_level0_order(const int* __restrict__ digit, const int* n_dev, int* __restrict__ order,
+                               unsigned* __restrict__ sdig) {
   TT_PDL_ENTRY();
   const int n = ld_count(n_dev);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = i;
-}
-__global__ void k_digits_copy_u32(const int* __restrict__ digit, const int* n_dev, unsigned* __restrict__ out) {
-  TT_PDL_ENTRY();
-  const int n = ld_count(n_dev);
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (unsigned)digit[i];
+  if (i < n) {
+    order[i] = i;
+    sdig[i] = (unsigned)digit[i];
+  }
 }
 
 }  // namespace tt
