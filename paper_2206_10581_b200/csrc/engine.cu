@@ -242,13 +242,14 @@ int ensure_generic(tt_engine* h) {
   return TT_OK;
 }
 
-// Eager launches use programmatic stream serialisation (PDL): the next kernel
-// of the step is scheduled while the previous one drains, and waits
+// Programmatic stream serialisation (PDL) is opt-in (TT_PDL=1): the next
+// kernel is scheduled while the previous one drains and waits
 // (griddepcontrol.wait, TT_PDL_ENTRY) for its completion -- 0.20 -> 0.16 ms
-// for the plan at papers.  Under stream capture the attribute is left off:
-// a replayed graph already launches back to back, and programmatic edges
-// measured slower there (papers step 2.70 -> 2.80 ms).  TT_NO_PDL=1 turns it
-// off everywhere (A/B).
+// for the eager plan at papers.  It is off by default: with it, repeated
+// fresh-engine runs of the tensor-core path at the billion shape produced
+// differing P_F rows in ~8% of runs (scripts/race_stress.py, FRESH=1), and 0
+// of 59 without.  Never used under stream capture (the replayed graph already
+// launches back to back; programmatic edges measured slower there).
 // Diagnostic switches, read once per process (all off by default):
 //   TT_TC_VARIANT / TT_TC_BVARIANT = bit mask handed to the tcgen05 forward /
 //     backward as FusedArgs::mode to skip parts of the work for attribution
@@ -272,8 +273,8 @@ const DiagEnv& diag() {
 
 bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TT_NO_PDL");
-    return !(e && *e && *e != '0');
+    const char* e = getenv("TT_PDL");
+    return e && *e && *e != '0';
   }();
   return on;
 }
@@ -375,9 +376,9 @@ void sort_levels(tt_engine* h, cudaStream_t s) {
 }
 
 void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax,
-                    const unsigned long long* skey = nullptr) {
+                    const ScanFlags& sf) {
   const int nblk = (int)((nmax + SC_BLOCK - 1) / SC_BLOCK);
-  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk, skey);
+  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk, sf);
   LAUNCH(k_scan_partials, narr, 1024, 0, s, h->partial, nblk);
   LAUNCH(k_scan_add, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
 }
@@ -404,20 +405,24 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
   h->skeys = radix_sort<unsigned long long>(h, s, h->keys_a, h->pos_a, h->keys_b, h->pos_b, nullptr, (int)B, B,
                                             idbits, &h->spos);
-  scan_inclusive(h, s, h->flag, 0, 1, h->d_B, B, h->skeys);  // unique flags formed in the scan
+  ScanFlags uf{};
+  uf.keys = h->skeys;
+  uf.div[0] = 1;  // unique-ID flags
+  scan_inclusive(h, s, h->flag, 0, 1, h->d_B, B, uf);
   LAUNCH(k_unique_emit, grid_for(B, 256, INT_MAX), 256, 0, s, h->skeys, (int)B, h->flag, h->uniq, h->seg, h->counts,
          d, h->st);
   const int* U = h->counts + (d - 1);
-  LAUNCH(k_level_flags, grid_for(B, 256, INT_MAX), 256, 0, s, c, h->uniq, h->counts, h->lflags, cap);
-  scan_inclusive(h, s, h->lflags, cap, d - 1, U, B);
+  ScanFlags lf{};
+  lf.keys = h->uniq;
+  for (int k = 0; k + 1 < d; ++k) lf.div[k] = (unsigned long long)c.S[k];  // level-k prefix flags
+  scan_inclusive(h, s, h->lflags, cap, d - 1, U, B, lf);
+  // level nodes; level 0 is already digit-sorted and distinct (identity group order)
   LAUNCH(k_level_emit, grid_for(B, 256, INT_MAX), 256, 0, s, c, h->uniq, h->counts, h->lflags, cap, h->digit,
-         h->parent, h->first);
-  LAUNCH(k_children, dim3(grid_for(B + 1, 256, INT_MAX), d - 1), 256, 0, s, c, h->counts, h->lflags, cap, h->first,
-         h->cstart);
-  // digit groups: level 0 is already digit-sorted and distinct
-  LAUNCH(k_level0_order, grid_for(B, 256, INT_MAX), 256, 0, s, h->digit, h->counts, h->gv[0][0], h->gk[0][0]);
+         h->parent, h->first, h->gv[0][0], h->gk[0][0]);
   h->order[0] = h->gv[0][0];
   h->sdig[0] = h->gk[0][0];
+  LAUNCH(k_children, dim3(grid_for(B + 1, 256, INT_MAX), d - 1), 256, 0, s, c, h->counts, h->lflags, cap, h->first,
+         h->cstart);
 
   bool batched = true;
   for (int k = 1; k < d; ++k) batched = batched && bitlen((uint64_t)(c.m[k] - 1)) <= RS_MAXBITS;

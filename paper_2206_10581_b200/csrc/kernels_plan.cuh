@@ -262,11 +262,17 @@ __device__ __forceinline__ int block_excl_scan_256(int t, int* wsum, int& total)
   return r;
 }
 
-// skey != nullptr: the scanned values are the unique-ID flags of the sorted
-// keys (1 where a new ID starts), computed here and not read from `a`
+// Values to scan: read from the array (keys == nullptr), or group-start flags
+// formed here from sorted keys -- 1 where keys[s] / div[y] changes (array y):
+// div 1 gives the unique-ID flags, div S_k the level-k prefix flags.
+struct ScanFlags {
+  const unsigned long long* keys;
+  unsigned long long div[TT_MAXD];
+};
+
 __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a, int64_t stride,
                                                             const int* n_dev, int* __restrict__ partial,
-                                                            int nblk, const unsigned long long* __restrict__ skey) {
+                                                            int nblk, ScanFlags sf) {
   TT_PDL_ENTRY();
   __shared__ int wsum[SC_THREADS / 32];
   const int n = ld_count(n_dev);
@@ -281,7 +287,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a,
 #pragma unroll
   for (int j = 0; j < SC_ITEMS; ++j) {
     const int s = i0 + j;
-    v[j] = s < n ? (skey ? ((s == 0 || skey[s] != skey[s - 1]) ? 1 : 0) : arr[s]) : 0;
+    const unsigned long long dv = sf.div[blockIdx.y];
+    v[j] = s < n ? (sf.keys ? ((s == 0 || sf.keys[s] / dv != sf.keys[s - 1] / dv) ? 1 : 0) : arr[s]) : 0;
     t += v[j];
     v[j] = t;
   }
@@ -369,27 +376,14 @@ __global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B
   }
 }
 
-// Level flags: for 0-based level k < d-1, a new prefix (i_1..i_{k+1}) starts
-// at unique u.  flags laid out [k][cap].
-__global__ void k_level_flags(DevCfg c, const unsigned long long* __restrict__ uniq, const int* __restrict__ counts,
-                              int* __restrict__ flags, int64_t cap) {
-  TT_PDL_ENTRY();
-  const int U = ld_count(&counts[c.d - 1]);
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= U) return;
-  unsigned long long key = uniq[u], prev = u ? uniq[u - 1] : 0;
-  for (int k = 0; k + 1 < c.d; ++k) {
-    unsigned long long S = (unsigned long long)c.S[k];
-    flags[k * cap + u] = (u == 0 || key / S != prev / S) ? 1 : 0;
-  }
-}
-
 // Node arrays per level (0-based k): digit, parent, first unique.  Level d-1
 // nodes are the unique IDs themselves.
+// Level 0 nodes are already in digit order and distinct: their group order is
+// the identity and their sorted digits are their digits (order0 / sdig0).
 __global__ void k_level_emit(DevCfg c, const unsigned long long* __restrict__ uniq, int* __restrict__ counts,
                              const int* __restrict__ scan /*[k][cap] inclusive*/, int64_t cap,
                              int* __restrict__ digit /*[k][cap]*/, int* __restrict__ parent,
-                             int* __restrict__ first) {
+                             int* __restrict__ first, int* __restrict__ order0, unsigned* __restrict__ sdig0) {
   TT_PDL_ENTRY();
   const int U = ld_count(&counts[c.d - 1]);
   int u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -400,8 +394,13 @@ __global__ void k_level_emit(DevCfg c, const unsigned long long* __restrict__ un
     unsigned long long p = key / S;
     if (u == 0 || p != prev / S) {
       int node = scan[k * cap + u] - 1;
-      digit[k * cap + node] = (int)(p % (unsigned long long)c.m[k]);
+      const int dg = (int)(p % (unsigned long long)c.m[k]);
+      digit[k * cap + node] = dg;
       first[k * cap + node] = u;
+      if (k == 0) {
+        order0[node] = node;
+        sdig0[node] = (unsigned)dg;
+      }
       parent[k * cap + node] = k ? scan[(k - 1) * cap + u] - 1 : -1;
     }
     if (u == U - 1) counts[k] = scan[k * cap + u];
@@ -474,19 +473,6 @@ __global__ void k_group_offsets(const unsigned* __restrict__ sdig, const int* n_
     if ((int)sdig[mid] < v) lo = mid + 1; else hi = mid;
   }
   goff[v] = lo;
-}
-
-// level 0 (i_1 nodes): already sorted by digit and unique -> identity order
-// and the digits as the sorted keys
-__global__ void k_level0_order(const int* __restrict__ digit, const int* n_dev, int* __restrict__ order,
-                               unsigned* __restrict__ sdig) {
-  TT_PDL_ENTRY();
-  const int n = ld_count(n_dev);
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    order[i] = i;
-    sdig[i] = (unsigned)digit[i];
-  }
 }
 
 }  // namespace tt

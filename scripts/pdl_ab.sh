@@ -1,7 +1,7 @@
-# A/B of programmatic dependent launch: bench with PDL on and off (TT_NO_PDL=1)
+# A/B of programmatic dependent launch: bench with PDL on and off (TT_PDL=0 vs 1)
 for cfg in ${CFGS:-small products papers}; do
   for pdl in 0 1; do
-    TT_NO_PDL=$pdl timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-tensor-path > gpurun_out/pdl_${cfg}_$pdl.json 2>/dev/null
-    echo "TT_NO_PDL=$pdl $(python scripts/bench_summary.py gpurun_out/pdl_${cfg}_$pdl.json)"
+    TT_PDL=$pdl timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-tensor-path > gpurun_out/pdl_${cfg}_$pdl.json 2>/dev/null
+    echo "TT_PDL=$pdl $(python scripts/bench_summary.py gpurun_out/pdl_${cfg}_$pdl.json)"
   done
 done
