@@ -13,12 +13,11 @@
 // FFMA (fp32) out of shared memory.  Ranks are uniform on this path
 // (R_{F+1} = R_F = K).
 //
-// Forward epilogue: the last level (R_d = 1) is applied from the C tile in
-// shared memory -- for every distinct ID under the tile's nodes,
-// out[(a, j_F, j_l)] = sum_r C[a][(j_F, r)] G_{d-1}[r, i_d, j_l] (slices staged
-// transposed in shared memory) -- and written to the ID's batch positions
-// (IDs with more than HEAVY_POS positions go through Yu and the balanced
-// k_scatter_heavy).  The C tile is saved (P_F) for the backward.
+// Forward: the C tile is saved (P_F); the last level (R_d = 1) runs as the
+// streaming kernel k_last_level over it -- for every distinct ID,
+// out[(a, j_F, j_l)] = sum_r P_F[a][(j_F, r)] G_{d-1}[r, i_d, j_l] -- written to
+// the ID's batch positions (IDs with more than HEAVY_POS positions go through
+// Yu and the balanced k_scatter_heavy).
 //
 // Backward per unit, for each row tile (C-tile load overlapped with compute):
 //   dC   (rows x BN)      = sum_u dY_u . G_{d-1}[i_d(u)]^T        (dP_F)
@@ -167,25 +166,6 @@ __device__ __forceinline__ void prep_nodes(const FusedArgs& a, int nb0, int nbn,
 
 constexpr int FB_IDS = 512;  // per-batch distinct IDs whose metadata is staged
 
-// digit i_d and slot range of the batch's first FB_IDS distinct IDs (flat
-// index f = position in the batch's ID prefix s_pref).  Ends with a barrier.
-__device__ __forceinline__ void prep_ids(const FusedArgs& a, int nbn, const int* s_cs0, const int* s_pref, int* s_bd,
-                                         int* s_bs0, int* s_bs1) {
-  const int tot = min(s_pref[nbn], FB_IDS);
-  for (int f = threadIdx.x; f < tot; f += FB_THREADS) {
-    int lo = 0, hi = nbn - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
-    }
-    const int u = s_cs0[lo] + (f - s_pref[lo]);
-    s_bd[f] = __ldg(a.digitL + u);
-    s_bs0[f] = __ldg(a.seg + u);
-    s_bs1[f] = __ldg(a.seg + u + 1);
-  }
-  __syncthreads();
-}
-
 // A tile (BM x K, row-major) of batch-local nodes [tb, tb+nn) by cp.async;
 // rows past the tile's nodes are zero-filled.
 template <int K, int RP>
@@ -197,56 +177,6 @@ __device__ __forceinline__ void load_A_tile(const FusedArgs& a, int tb, int nn, 
     if (j < nn) cp_async16(dst, a.Abase + s_aoff[tb + j] + (m - j * RP) * K + q * 4);
     else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-}
-
-// node (batch-local, in [lo, hi)) owning flat distinct-ID index f
-__device__ __forceinline__ int find_node(const int* s_pref, int lo, int hi, int f) {
-  hi -= 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Stage distinct IDs [f0, f0 + nc) of tile nodes [tb, tb+nn): s_u (ID),
-// s_j (tile-local node), s_s0/s_s1 (sorted-slot range) and, if want_g, the
-// last-core slices transposed: Gs[(ci*NL + jl)*(K+4) + r] = G[r, i_d(u), jl].
-template <int K, int NL>
-__device__ __forceinline__ void stage_ids(const FusedArgs& a, int f0, int nc, int tb, int nn, const int* s_cs0,
-                                          const int* s_pref, int* s_u, int* s_j, int* s_s0, int* s_s1, float* Gs,
-                                          bool want_g) {
-  for (int ci = threadIdx.x; ci < nc; ci += FB_THREADS) {
-    const int j = find_node(s_pref, tb, tb + nn, f0 + ci);
-    const int u = s_cs0[j] + (f0 + ci - s_pref[j]);
-    s_j[ci] = j - tb;
-    s_u[ci] = u;
-    s_s0[ci] = a.seg[u];
-    s_s1[ci] = a.seg[u + 1];
-  }
-  __syncthreads();
-  if (!want_g) return;
-  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
-  const int64_t sliceL = a.c.slice[a.c.d - 1];
-  for (int i = threadIdx.x; i < nc * K * NL / 4; i += FB_THREADS) {
-    const int ci = i / (K * NL / 4), e = (i - ci * (K * NL / 4)) * 4;  // e = r*NL + jl0
-    const int r = e / NL, jl0 = e - r * NL;
-    const float4 v = __ldg(reinterpret_cast<const float4*>(Gl + (int64_t)a.digitL[s_u[ci]] * sliceL + e));
-    float* g = Gs + (ci * NL + jl0) * (K + 4) + r;
-    g[0] = v.x;
-    g[K + 4] = v.y;
-    g[2 * (K + 4)] = v.z;
-    g[3 * (K + 4)] = v.w;
-  }
-  __syncthreads();
-}
-
-// column n of the thread's micro-tile (GEMM layout): TN >= 4 -> q*128 + lane*4 + t
-template <int BN>
-__device__ __forceinline__ int tile_col(int lane, int jcol) {
-  constexpr int TN = BN / 32;
-  if constexpr (TN >= 4) return (jcol >> 2) * 128 + lane * 4 + (jcol & 3);
-  else return lane * TN + jcol;
 }
 
 template <int BN>
@@ -281,15 +211,10 @@ __device__ __forceinline__ void store_row_frag(float* row, int lane, const float
 }
 
 // ---------------------------------------------------------------------------
-// Register-level last-core contraction.  A warp's micro-tile holds rows
-// m0..m0+7 and, per lane, NQ column groups of W4 consecutive columns; group q
-// of lane l covers columns q*128 + l*W4 .. (+W4) for BN >= 128 and l*W4.. for
-// BN = 64, i.e. core-F column block jf = col / K and rank index r = col % K.
-// LPJ = K / W4 lanes share one jf, so a contraction over r is W4 FMAs per
-// lane followed by a reduction across those LPJ lanes.  The reduction is a
-// transpose-reduce: V values per lane, log2(LPJ) butterfly levels in which a
-// lane keeps half and ships half, ending with V/LPJ fully reduced values per
-// lane (value index (lane % LPJ) * (V/LPJ) + k).  Fixed tree: deterministic.
+// Column map of a warp's micro-tile (the backward's dC pass): rows m0..m0+7
+// and, per lane, NQ column groups of W4 consecutive columns; group q of lane l
+// covers columns q*128 + l*W4 .. (+W4) for BN >= 128 and l*W4.. for BN = 64,
+// i.e. core-F column block jf = col / K and rank index r = col % K.
 template <int BN>
 struct ColMap {
   static constexpr int TN = BN / 32;
@@ -298,36 +223,11 @@ struct ColMap {
   __device__ static int col(int lane, int q) { return TN >= 4 ? q * 128 + lane * 4 : lane * W4; }
 };
 
-template <int V, int LPJ>
-__device__ __forceinline__ void transpose_reduce(float (&v)[V], int lane) {
-  int cnt = V;
-#pragma unroll
-  for (int off = LPJ / 2; off >= 1; off >>= 1) {
-    const bool sel = (lane & off) != 0;
-    const int half = cnt / 2;
-#pragma unroll
-    for (int i = 0; i < V / 2; ++i) {
-      if (i < half) {
-        const float send = sel ? v[i] : v[i + half];
-        const float keep = sel ? v[i + half] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    }
-    cnt = half;
-  }
-}
-
 // ---------------------------------------------------------------------------
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   TT_PDL_ENTRY();
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, BNJ = BN / K, NPT = BM / RP;
-  using CM = ColMap<BN>;
-  constexpr int W4 = CM::W4, NQ = CM::NQ, LPJ = K / W4;
-  constexpr int NR = RP < 8 ? RP : 8;   // rows of one node inside a warp's 8 rows
-  constexpr int NPW = 8 / NR;           // nodes (or node halves) per warp
-  constexpr int V = NR * NL;            // values per lane per column group before reduction
-  static_assert(V % LPJ == 0 && V >= LPJ, "epilogue reduction shape");
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, NPT = BM / RP;
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;                      // [K][SB]
   float* As0 = Bs + K * SB;              // [2][BM][K]
@@ -336,11 +236,6 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;            // [FB_NB + 1]
   int* s_wsum = s_pref + FB_NB + 4;
-  // per-ID metadata of the batch (first FB_IDS IDs) and the tile's staged slices
-  int* s_bd = s_wsum + 8;                 // digit i_d
-  int* s_bs0 = s_bd + FB_IDS;             // seg[u]
-  int* s_bs1 = s_bs0 + FB_IDS;            // seg[u+1]
-  float* Gst = reinterpret_cast<float*>(s_bs1 + FB_IDS);  // [CH][K*NL], 16-byte aligned
 
   if (tt_failed(a.st)) return;
   const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
@@ -348,17 +243,12 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   if (g0 == g1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = warp * 8;
-  const int64_t emb = a.c.emb_dim, npad = a.c.npad;
-  const int nF = a.nF;
-  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
-  const int64_t sliceL = a.c.slice[a.c.d - 1];
 
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
   cp_async_commit();
   for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
     const int nbn = min(FB_NB, g1 - nb0);
     prep_nodes(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    if (a.out) prep_ids(a, nbn, s_cs0, s_pref, s_bd, s_bs0, s_bs1);
     load_A_tile<K, RP>(a, 0, min(NPT, nbn), s_aoff, As0);
     cp_async_commit();
     int buf = 0;
@@ -368,13 +258,6 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
       __syncthreads();
       if (tb + NPT < nbn) {  // prefetch the next tile's A under this tile's GEMM
         load_A_tile<K, RP>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
-      }
-      // the tile's last-core slices (first CH IDs) land under the GEMM too
-      const int tfA = s_pref[tb];
-      const int nstage = a.out ? max(0, min(a.CH, min(s_pref[tb + nn], FB_IDS) - tfA)) : 0;
-      for (int i = threadIdx.x; i < nstage * (K * NL / 4); i += FB_THREADS) {
-        const int ci = i / (K * NL / 4), q = i - ci * (K * NL / 4);
-        cp_async16(Gst + ci * K * NL + q * 4, Gl + (int64_t)s_bd[tfA + ci] * sliceL + q * 4);
       }
       cp_async_commit();
       const float* As = As0 + buf * BM * K;
@@ -400,68 +283,12 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
           }
         }
       }
-      // saved P_F for the backward
-      if (a.Psave) {
+      // P_F rows of the tile (saved for the last level and the backward)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int m = m0 + i, j = m / RP;
-          if (j < nn)
-            store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
-        }
-      }
-      if (!a.out) continue;
-      cp_async_wait<0>();  // staged slices (and the next A tile)
-      __syncthreads();
-      // last level from the registers: per node of this warp, per distinct ID
-#pragma unroll
-      for (int jw = 0; jw < NPW; ++jw) {
-        const int j = (m0 + jw * NR) / RP;  // tile-local node
-        if (j >= nn) continue;
-        const int ar0 = (m0 + jw * NR) % RP;
-        const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
-        for (int f = fA; f < fB; ++f) {
-          const int u = cs0 + (f - fA);
-          const bool staged = f - tfA < nstage;
-          const bool known = f < FB_IDS;
-          const float* Gp = staged ? Gst + (f - tfA) * K * NL
-                                   : Gl + (int64_t)(known ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
-          const int s0 = known ? s_bs0[f] : __ldg(a.seg + u), s1 = known ? s_bs1[f] : __ldg(a.seg + u + 1);
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const int colb = CM::col(lane, q);
-            const int r0 = colb % K, jf = colb / K;
-            float gv[W4][NL];
-#pragma unroll
-            for (int t = 0; t < W4; ++t)
-#pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = *reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4);
-                gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
-              }
-            float v[V];
-#pragma unroll
-            for (int ii = 0; ii < NR; ++ii)
-#pragma unroll
-              for (int jl = 0; jl < NL; ++jl) {
-                float s = 0.f;
-#pragma unroll
-                for (int t = 0; t < W4; ++t) s = fmaf(acc[jw * NR + ii][q * W4 + t], gv[t][jl], s);
-                v[ii * NL + jl] = s;
-              }
-            transpose_reduce<V, LPJ>(v, lane);
-#pragma unroll
-            for (int k2 = 0; k2 < V / LPJ; ++k2) {
-              const int idx = (lane % LPJ) * (V / LPJ) + k2;
-              const int ii = idx / NL, jl = idx - ii * NL;
-              const int64_t col = ((int64_t)((ar0 + ii) * nF + cb * BNJ + jf)) * NL + jl;
-              if (s1 - s0 > HEAVY_POS) {
-                a.Yu[(int64_t)u * npad + col] = v[k2];
-              } else if (col < emb) {
-                for (int s = s0; s < s1; ++s) a.out[(int64_t)__ldg(a.spos + s) * emb + col] = v[k2];
-              }
-            }
-          }
-        }
+      for (int i = 0; i < 8; ++i) {
+        const int m = m0 + i, j = m / RP;
+        if (j < nn)
+          store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
       }
     }
   }
