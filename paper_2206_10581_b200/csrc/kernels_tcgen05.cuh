@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
       if (threadIdx.x == 0) {
         const tc::Operand oa = tc::kmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
         const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm, oa, ob, K, idesc, false);
+        if (!(a.mode & 2)) tc::mma_x3<K / 16>(tm, oa, ob, idesc, false);
         tc::commit(&bar);
       }
       __syncwarp();
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   const int eslice = (warp >> 2) * EC;
   if (warp == 0) tc::tmem_alloc<TCOLS>(&tslot);
   if (threadIdx.x == 32) {
-    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&bar, 2);  // two issuers commit per tile (dG_F^T and dA)
     tc::fence_mbar_init();
   }
   tc_stage_slice<K, BN, T>(a, g, cb, S0, S1, S2);
@@ -392,26 +392,31 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
       __syncthreads();
       tc::after_sync();
       const uint32_t tm = tslot;
-      if (threadIdx.x == 0) {
-        const uint32_t d0 = tc::smem_u32(D0), d1 = tc::smem_u32(D1), d2 = tc::smem_u32(D2);
-        const tc::Operand dcT = tc::mnmajor(d0, d1, d2, BN);  // A operand (m = col, k = row)
+      // the next tile's A loads go out first (they land while the issuers
+      // below block on the tensor pipe's queue)
+      const bool more = tb + NPT < nbn;
+      if (more && !(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+      // two issuers in different warps (the products write separate TMEM
+      // accumulators): issuing blocks while the tensor pipe's queue is full,
+      // so each product's 48 MMAs hold up only its own warp
+      if (threadIdx.x == 0) {  // dG_F^T += dC^T . A   (accumulated over the group)
+        const tc::Operand dcT = tc::mnmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
         const tc::Operand aB = tc::mnmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
-        if (!(a.mode & 2)) tc::mma_x3(tm, dcT, aB, TC_BM, id_g, tiles > 0);
-        const tc::Operand dcK = tc::kmajor(d0, d1, d2, BN);   // A operand (m = row, k = col)
+        if (!(a.mode & 2)) tc::mma_x3<TC_BM / 16>(tm, dcT, aB, id_g, tiles > 0);
+        tc::commit(&bar);
+      } else if (threadIdx.x == 32) {  // dA = dC . S^T
+        const tc::Operand dcK = tc::kmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
         const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3(tm + K, dcK, sT, BN, id_a, false);
+        if (!(a.mode & 2)) tc::mma_x3<BN / 16>(tm + K, dcK, sT, id_a, false);
         tc::commit(&bar);
       }
       __syncwarp();
       float* dst = (emj < nn && !(a.mode & 4))
                        ? a.dPc + ((int64_t)s_node[tb + emj] * a.ncb + cb) * RP * K + ema * K + eslice
                        : nullptr;
-      // under this tile's MMAs: the next tile's A tile and dC unit (no TMEM
-      // access -- a tcgen05.ld issued now would queue behind the MMAs)
-      if (tb + NPT < nbn) {
-        if (!(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
-        compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
-      }
+      // under this tile's MMAs: the next tile's dC unit (no TMEM access -- a
+      // tcgen05.ld issued now would queue behind the MMAs)
+      if (more) compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
       tc::mbar_wait(&bar, phase);  // planes free for the next tile
       phase ^= 1;
       tc::after_sync();

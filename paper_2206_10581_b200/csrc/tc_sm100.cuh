@@ -159,19 +159,29 @@ struct Operand {
   uint32_t kstep;     // byte advance per 16 K
 };
 
-__device__ __forceinline__ void mma_x3(uint32_t d_tmem, const Operand& A, const Operand& B, int K, uint32_t idesc,
+// The issuing thread is on the critical path of every tile (the rest of the
+// CTA waits for the tensor pipe), so the six descriptors per plane pair are
+// built once and advanced by adding the per-16-K step to their start-address
+// field (bits 0..13, in 16-byte units; shared addresses stay below 256 KB, so
+// the field never carries): two 64-bit adds per MMA, the loop fully unrolled.
+template <int KSTEPS>
+__device__ __forceinline__ void mma_x3(uint32_t d_tmem, const Operand& A, const Operand& B, uint32_t idesc,
                                        bool accumulate) {
   // small terms first: (b1b1, b0b2, b2b0, b0b1, b1b0, b0b0)
-  const int pa[6] = {1, 0, 2, 0, 1, 0};
-  const int pb[6] = {1, 2, 0, 1, 0, 0};
-#pragma unroll 1
-  for (int k = 0; k < K / 16; ++k) {
+  constexpr int pa[6] = {1, 0, 2, 0, 1, 0};
+  constexpr int pb[6] = {1, 2, 0, 1, 0, 0};
+  uint64_t da[3], db[3];
 #pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      const uint64_t da = sdesc(A.plane[pa[t]] + k * A.kstep, A.lbo, A.sbo);
-      const uint64_t db = sdesc(B.plane[pb[t]] + k * B.kstep, B.lbo, B.sbo);
-      mma_bf16(d_tmem, da, db, idesc, (accumulate || k > 0 || t > 0) ? 1u : 0u);
-    }
+  for (int i = 0; i < 3; ++i) {
+    da[i] = sdesc(A.plane[i], A.lbo, A.sbo);
+    db[i] = sdesc(B.plane[i], B.lbo, B.sbo);
+  }
+  const uint64_t sa = A.kstep >> 4, sb = B.kstep >> 4;
+#pragma unroll
+  for (int k = 0; k < KSTEPS; ++k) {
+#pragma unroll
+    for (int t = 0; t < 6; ++t)
+      mma_bf16(d_tmem, da[pa[t]] + k * sa, db[pb[t]] + k * sb, idesc, (accumulate || k > 0 || t > 0) ? 1u : 0u);
   }
 }
 

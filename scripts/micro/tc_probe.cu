@@ -56,7 +56,7 @@ __global__ void probe(const float* A, const float* B, float* D, int a_mn, int b_
                       : kmajor(smem_u32(pa[0]), smem_u32(pa[1]), smem_u32(pa[2]), aC);
     Operand ob = b_mn ? mnmajor(smem_u32(pb[0]), smem_u32(pb[1]), smem_u32(pb[2]), bC)
                       : kmajor(smem_u32(pb[0]), smem_u32(pb[1]), smem_u32(pb[2]), bC);
-    mma_x3(tm, oa, ob, K, idesc_bf16(M, N, a_mn, b_mn), false);
+    mma_x3<K / 16>(tm, oa, ob, idesc_bf16(M, N, a_mn, b_mn), false);
     commit(&bar);
   }
   __syncwarp();

@@ -42,13 +42,13 @@ print(f"prologue (entry -> first tile's planes ready) mean {pro.mean():.2f} us")
 tiles = []
 for i in live:
     k = 4
-    while k + 4 <= n[i]:
-        p = [tr[i, k + j] for j in range(5)]
-        nxt = tr[i, k + 5] if k + 5 <= n[i] else p[4]
-        tiles.append([(p[j + 1] - p[j]) / 1e3 for j in range(4)] + [(nxt - p[4]) / 1e3])
-        k += 5
+    while k + 3 <= n[i]:
+        p = [tr[i, k + j] for j in range(4)]
+        nxt = tr[i, k + 4] if k + 4 <= n[i] else p[3]
+        tiles.append([(p[j + 1] - p[j]) / 1e3 for j in range(3)] + [(nxt - p[3]) / 1e3])
+        k += 4
 tiles = np.array(tiles)
-names = ["A(t+1) load", "dC(t+1)", "MMA wait", "epilogue(t)", "planes(t+1)+sync"]
+names = ["A(t+1) loads", "dC(t+1)", "MMA wait", "epilogue(t)+planes(t+1)+sync"]
 if os.environ.get("TRACE_PATH") == "auto":
     t3 = []
     for i in live:
