@@ -259,11 +259,11 @@ int ensure_generic(tt_engine* h) {
 //     (tt_debug_trace, scripts/tc_trace.py).
 struct DiagEnv {
   int tc_fwd_variant = 0, tc_bwd_variant = 0;
-  bool trace = false;
+  int trace = 0;  // 1: backward, 2: forward
   DiagEnv() {
     if (const char* e = getenv("TT_TC_VARIANT")) tc_fwd_variant = atoi(e);
     if (const char* e = getenv("TT_TC_BVARIANT")) tc_bwd_variant = atoi(e);
-    if (const char* e = getenv("TT_TC_TRACE")) trace = *e && *e != '0';
+    if (const char* e = getenv("TT_TC_TRACE")) trace = atoi(e);
   }
 };
 const DiagEnv& diag() {
@@ -664,7 +664,21 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     if (use_tc(h)) {
       a.ncb = h->ts.ncbf;
       a.mode = diag().tc_fwd_variant;
-      const int grid = (int)(c.m[f.F] * h->ts.ncbf);
+      static long long* trace_fwd = nullptr;
+      if (diag().trace == 2) {  // TT_TC_TRACE=2: trace the forward instead of the backward
+        if (!trace_fwd) cudaMalloc(&trace_fwd, sizeof(long long) * 4096 * 64);
+        cudaMemsetAsync(trace_fwd, 0, sizeof(long long) * 4096 * 64, s);
+        a.dbg = trace_fwd;
+        g_trace_buf = trace_fwd;
+      }
+      // persistent: one CTA per SM over the (group, column block) items
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      const int grid = (int)std::min<int64_t>(c.m[f.F] * h->ts.ncbf, sms);
       if (false) {
       }
 #define TT_TC_FWD_CASE(k_, bn_, rp_, nl_) \
@@ -727,7 +741,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
       a.ncb = h->ts.ncbb;
       a.mode = diag().tc_bwd_variant;
       static long long* trace_buf = nullptr;
-      if (diag().trace) {
+      if (diag().trace == 1) {
         if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 4096 * 64);
         cudaMemsetAsync(trace_buf, 0, sizeof(long long) * 4096 * 64, s);
         a.dbg = trace_buf;
@@ -743,7 +757,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
 #undef TT_TC_BWD_CASE
     } else {
       static long long* trace_buf2 = nullptr;
-      if (diag().trace) {
+      if (diag().trace == 1) {
         if (!trace_buf2) cudaMalloc(&trace_buf2, sizeof(long long) * 4096 * 64);
         cudaMemsetAsync(trace_buf2, 0, sizeof(long long) * 4096 * 64, s);
         a.dbg = trace_buf2;

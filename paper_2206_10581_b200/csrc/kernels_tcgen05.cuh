@@ -143,112 +143,209 @@ __device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int n
 }
 
 // ---------------------------------------------------------------------------
-// Forward: P_F tiles on the tensor pipe, saved to Psave.  512 threads, one
-// CTA per SM.  The epilogue is store-bound (P_F is 666 MB at papers): warp w
-// drains TMEM lanes 32(w%4).. x columns 32(w/4).. of the accumulator, turns
-// its 32 x 32 chunk around in shared memory and writes 4 full 128-byte row
-// segments per store instruction (a TMEM lane per thread would write 32 rows
-// x 16 bytes per instruction, 8x the L2 requests).
-constexpr int TCF_THREADS = 512;
+// Forward: P_F tiles on the tensor pipe, saved to Psave.  Persistent (one
+// CTA per SM) and warp-specialised; the roles are coupled by mbarriers only:
+//   warps 0-7   loaders, two sets of four.  Set s owns A stage s (tiles
+//               t % 2 == s): thread (w % 4, lane) loads row m = 32 (w % 4) +
+//               lane of its tile (all K), splits it into three BF16 slices and
+//               writes them to TMEM with tcgen05.st -- A never touches shared
+//               memory, so the tensor pipe reads only S from it.  The next
+//               tile's row loads are in flight while the other set's tile is
+//               on the tensor pipe.  Both sets stage half of each item's S
+//               block (K x BN) into the shared-memory S ring.
+//   warps 8-15  epilogue: accumulator lanes 32 (w % 4).. x columns
+//               64 ((w - 8) / 4).. drained to registers (the accumulator is
+//               released at once), turned around in shared memory, written as
+//               4 full 128-byte row segments per store instruction.
+//   warp 16     one thread issues the six-product MMAs (A from TMEM).
+// TMEM: accumulators 2 x BN columns, then A slices 2 stages x 3 x K/2.
+// Work items (digit group g, column block cb) are dealt round-robin over the
+// CTAs with cb fastest, so consecutive items of a CTA share their A rows.
+constexpr int TCF_LOADERS = 8;   // two sets of four warps
+constexpr int TCF_EPI = 8;
+constexpr int TCF_THREADS = 32 * (TCF_LOADERS + TCF_EPI + 1);
 constexpr int TCF_ES = 36;  // epilogue staging row stride (floats): conflict-free 16-byte stores and loads
 template <int K, int BN>
 constexpr size_t tc_fwd_smem_bytes() {
-  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + (size_t)(TCF_THREADS / 32) * 32 * TCF_ES * 4 + TC_META;
+  return 2 * 3 * (size_t)K * BN * 2 + (size_t)TCF_EPI * 32 * TCF_ES * 4;
 }
 
 template <int K, int BN, int RP>
 __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
-  static_assert(BN == 128 && K % 16 == 0 && TC_BM % RP == 0, "tcgen05 forward shape");
-  constexpr int T = TCF_THREADS;
-  constexpr int NPT = TC_BM / RP;
-  constexpr uint32_t TCOLS = BN;
+  static_assert(BN == 128 && K % 32 == 0 && K <= 64 && TC_BM % RP == 0 && 32 % RP == 0, "tcgen05 forward shape");
+  constexpr int NPT = TC_BM / RP;                 // nodes per tile
+  constexpr uint32_t SPL = (uint32_t)K * BN * 2;  // bytes per S slice plane
+  constexpr uint32_t ACOLS = K / 2;               // TMEM columns per A slice
   extern __shared__ __align__(128) uint8_t tsm[];
-  uint8_t* S0 = tsm;
-  uint8_t* S1 = S0 + K * BN * 2;
-  uint8_t* S2 = S1 + K * BN * 2;
-  uint8_t* A0 = S2 + K * BN * 2;
-  uint8_t* A1 = A0 + TC_BM * K * 2;
-  uint8_t* A2 = A1 + TC_BM * K * 2;
-  float* Es = reinterpret_cast<float*>(A2 + TC_BM * K * 2);  // [16 warps][32][TCF_ES]
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Es + (T / 32) * 32 * TCF_ES);
-  int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
-  int* s_cs0 = s_node + FB_NB;
-  int* s_pref = s_cs0 + FB_NB;
-  int* s_wsum = s_pref + FB_NB + 4;
-  __shared__ uint64_t bar;
+  float* Es = reinterpret_cast<float*>(tsm + 2 * 3 * SPL);
+  __shared__ uint64_t s_full[2], s_empty[2], a_full[2], a_empty[2], c_full[2], c_empty[2];
   __shared__ uint32_t tslot;
 
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
-  const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
-  if (g0 == g1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) tc::tmem_alloc<TCOLS>(&tslot);
+  if (warp == 0) tc::tmem_alloc<512>(&tslot);
   if (threadIdx.x == 32) {
-    tc::mbar_init(&bar, 1);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s_full[i], TCF_LOADERS);
+      tc::mbar_init(&s_empty[i], 1);
+      tc::mbar_init(&a_full[i], TCF_LOADERS / 2);
+      tc::mbar_init(&a_empty[i], 1);
+      tc::mbar_init(&c_full[i], 1);
+      tc::mbar_init(&c_empty[i], TCF_EPI);
+    }
     tc::fence_mbar_init();
   }
-  tc_stage_slice<K, BN, T>(a, g, cb, S0, S1, S2);
-  uint32_t phase = 0;
-  const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
-  ATileRegs<K, T> ar;
-  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-  const int ccol = (warp >> 2) * 32;          // this warp's 32 accumulator columns
-  float* Ew = Es + warp * 32 * TCF_ES;
-  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
-    const int nbn = min(FB_NB, g1 - nb0);
-    tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
-    tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
-    for (int tb = 0; tb < nbn; tb += NPT) {
-      const int nn = min(NPT, nbn - tb);
-      if (!(a.mode & 8)) tc_store_A<K, T>(ar, A0, A1, A2);
-      tc::fence_async_smem();
-      tc::before_sync();
-      __syncthreads();  // A planes written; the previous tile's TMEM reads done
-      tc::after_sync();
-      const uint32_t tm = tslot;
-      if (threadIdx.x == 0) {
-        const tc::Operand oa = tc::kmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
-        const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
-        if (!(a.mode & 2)) tc::mma_x3<K / 16>(tm, oa, ob, idesc, false);
-        tc::commit(&bar);
-      }
-      __syncwarp();
-      if (tb + NPT < nbn && !(a.mode & 8)) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
-      tc::mbar_wait(&bar, phase);
-      phase ^= 1;
-      tc::after_sync();
-      // epilogue: TMEM (row = lane) -> staging -> 4 rows x 128 B per store
-      {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + ccol, v);
+  tc::before_sync();
+  __syncthreads();
+  tc::after_sync();
+  const uint32_t tm = tslot;
+  const uint32_t tacc = tm, ta = tm + 2 * BN;
+  const int nitems = (int)a.c.m[a.F] * a.ncb;
+
+  if (warp < TCF_LOADERS) {
+    // ---------------- loaders ----------------
+    const int set = warp >> 2, q = warp & 3;
+    const int m = 32 * q + lane, jm = m / RP, am = m - jm * RP;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const int su = (int)(threadIdx.x & 127);  // thread within the set
+    uint32_t t = 0, i = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int g = it / a.ncb, cb = it - g * a.ncb;
+      const int g0 = a.goffF[g], n = a.goffF[g + 1] - g0;
+      if (n == 0) continue;
+      {  // half of the S block (rows k of the set's half) into S stage i % 2
+        const int s = i & 1;
+        tc::mbar_wait(&s_empty[s], ((i >> 1) & 1) ^ 1);
+        uint8_t* S0 = tsm + s * 3 * SPL;
+        const float* src = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
+        constexpr int UH = K * BN / 16;  // units (8 values) per set
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        tc::tmem_ld16(tm + lane_base + ccol + 16, v);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 16 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        __syncwarp();
-        const int c4 = (lane & 7) * 4;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = (lane >> 3) + 4 * i;     // row within the warp's 32
-          const int m = 32 * (warp & 3) + r;     // tile row
-          const int j = m / RP;
-          const float4 x = *reinterpret_cast<const float4*>(Ew + r * TCF_ES + c4);
-          if (j < nn && !(a.mode & 4))
-            *reinterpret_cast<float4*>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN +
-                                       ccol + c4) = x;
+        for (int uu = 0; uu < UH / 128; ++uu) {
+          const int u = set * UH + su + uu * 128;
+          const int cc = (u >> 3) % (BN / 8), k = ((u >> 3) / (BN / 8)) * 8 + (u & 7), c0 = cc * 8;
+          const float4 x0 = __ldg(reinterpret_cast<const float4*>(src + (int64_t)k * a.NC + c0));
+          const float4 x1 = __ldg(reinterpret_cast<const float4*>(src + (int64_t)k * a.NC + c0 + 4));
+          const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          tc::store_split8(S0, S0 + SPL, S0 + 2 * SPL, k, c0, BN, x);
         }
+        tc::fence_async_smem();
         __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&s_full[s]);
+        ++i;
       }
-      tc::before_sync();
+      for (int tb = 0; tb < n; tb += NPT, ++t) {
+        if ((int)(t & 1) != set) continue;
+        const int nn = min(NPT, n - tb);
+        float x[K];
+        if (jm < nn) {
+          const int node = __ldg(a.orderF + g0 + tb + jm);
+          const int p = __ldg(a.parentF + node);
+          const int64_t aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
+                                        : (int64_t)p * RP * a.c.R[a.F];
+          const float4* src = reinterpret_cast<const float4*>(a.Abase + aoff + am * K);
+#pragma unroll
+          for (int v = 0; v < K / 4; ++v) {
+            const float4 y = __ldg(src + v);
+            x[4 * v] = y.x; x[4 * v + 1] = y.y; x[4 * v + 2] = y.z; x[4 * v + 3] = y.w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < K; ++v) x[v] = 0.f;
+        }
+        tc::mbar_wait(&a_empty[set], ((t >> 1) & 1) ^ 1);  // the (t/2)-th use of this set's stage
+        tc::after_sync();
+        const uint32_t base = ta + set * 3 * ACOLS + lane_off;
+#pragma unroll
+        for (int c = 0; c < K / 16; ++c) {  // 8 columns (16 values) per slice per step
+          uint32_t p0[8], p1[8], p2[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) tc::split3(x[16 * c + 2 * v], x[16 * c + 2 * v + 1], p0[v], p1[v], p2[v]);
+          tc::tmem_st8(base + 8 * c, p0);
+          tc::tmem_st8(base + ACOLS + 8 * c, p1);
+          tc::tmem_st8(base + 2 * ACOLS + 8 * c, p2);
+        }
+        tc::tmem_st_wait();
+        tc::before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&a_full[set]);
+      }
     }
-    tc::before_sync();
-    __syncthreads();
+  } else if (warp < TCF_LOADERS + TCF_EPI) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3, h = (warp - TCF_LOADERS) >> 2;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    float* Ew = Es + (warp - TCF_LOADERS) * 32 * TCF_ES;
+    const int c4 = (lane & 7) * 4;
+    uint32_t t = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int g = it / a.ncb, cb = it - g * a.ncb;
+      const int g0 = a.goffF[g], n = a.goffF[g + 1] - g0;
+      for (int tb = 0; tb < n; tb += NPT, ++t) {
+        const int nn = min(NPT, n - tb);
+        // nodes of this warp's 32 rows (32 / RP of them), one per lane
+        const int jl0 = 32 * q / RP;
+        const int mynode = (lane < 32 / RP && jl0 + lane < nn) ? __ldg(a.orderF + g0 + tb + jl0 + lane) : 0;
+        const int st = t & 1;
+        tc::mbar_wait(&c_full[st], (t >> 1) & 1);
+        tc::after_sync();
+        uint32_t v[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tmem_ld16_async(tacc + st * BN + lane_off + 64 * h + 16 * c, v + 16 * c);
+        tc::tmem_ld_wait();
+        tc::before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&c_empty[st]);
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq)
+            *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 4 * qq) =
+                make_float4(__uint_as_float(v[32 * hc + 4 * qq]), __uint_as_float(v[32 * hc + 4 * qq + 1]),
+                            __uint_as_float(v[32 * hc + 4 * qq + 2]), __uint_as_float(v[32 * hc + 4 * qq + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int r = (lane >> 3) + 4 * rr;  // row within the warp's 32
+            const int jl = r / RP;               // node within the warp's rows
+            const int node = __shfl_sync(0xffffffffu, mynode, jl);
+            const float4 x = *reinterpret_cast<const float4*>(Ew + r * TCF_ES + c4);
+            if (jl0 + jl < nn)
+              *reinterpret_cast<float4*>(a.Psave + ((int64_t)node * RP + (r - jl * RP)) * a.NC + cb * BN + 64 * h +
+                                         32 * hc + c4) = x;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
+    uint32_t t = 0, i = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int g = it / a.ncb;
+      const int n = a.goffF[g + 1] - a.goffF[g];
+      if (n == 0) continue;
+      const int s = i & 1;
+      tc::mbar_wait(&s_full[s], (i >> 1) & 1);
+      uint8_t* S0 = tsm + s * 3 * SPL;
+      const tc::Operand ob = tc::mnmajor(tc::smem_u32(S0), tc::smem_u32(S0 + SPL), tc::smem_u32(S0 + 2 * SPL), BN);
+      for (int tb = 0; tb < n; tb += NPT, ++t) {
+        const int st = t & 1;
+        tc::mbar_wait(&a_full[st], (t >> 1) & 1);
+        tc::mbar_wait(&c_empty[st], ((t >> 1) & 1) ^ 1);
+        tc::after_sync();
+        tc::mma_x3_ts<K / 16>(tacc + st * BN, ta + st * 3 * ACOLS, ob, idesc, false);
+        tc::commit(&a_empty[st]);
+        tc::commit(&c_full[st]);
+      }
+      tc::commit(&s_empty[s]);
+      ++i;
+    }
   }
-  if (warp == 0) tc::tmem_free<TCOLS>(tslot);
+  tc::before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tm);
 }
 
 // ---------------------------------------------------------------------------
@@ -458,8 +555,7 @@ inline bool tc_plan_shape(const FusedShape& f, TcShape* t) {
   t->ncbf = f.NC / 128;
   t->BNb = 128;
   t->ncbb = f.NC / 128;
-  t->smem_fwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 +
-                (size_t)(TCF_THREADS / 32) * 32 * TCF_ES * 4 + TC_META;
+  t->smem_fwd = 2 * 3 * (size_t)f.K * 128 * 2 + (size_t)TCF_EPI * 32 * TCF_ES * 4;
   t->smem_bwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 + 3 * (size_t)TC_BM * 128 * 2 + TC_META;
   t->ok = t->smem_bwd <= (size_t)FB_SMEM_MAX;
   return t->ok;

@@ -7,7 +7,8 @@ import sys
 
 import numpy as np
 
-os.environ["TT_TC_TRACE"] = "1"
+FWD = os.environ.get("TRACE_KERNEL") == "fwd"
+os.environ["TT_TC_TRACE"] = "2" if FWD else "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -22,6 +23,8 @@ ti, tu = torch.tensor(idx, device="cuda"), torch.tensor(up, device="cuda")
 for _ in range(2):
     emb.forward(ti)
     emb.backward(tu)
+if FWD:
+    emb.forward(ti)
 emb.sync()
 lib = E.load_library()
 lib.tt_debug_trace.restype = C.c_int64
@@ -35,6 +38,21 @@ dur = np.array([tr[i, n[i]] - tr[i, 1] for i in live]) / 1e3
 start = (tr[live, 1] - t0) / 1e3
 end = np.array([tr[i, n[i]] for i in live] - t0) / 1e3
 print(f"CTAs {len(live)}  kernel span {end.max():.1f} us  CTA duration mean {dur.mean():.2f} median {np.median(dur):.2f} max {dur.max():.2f} us")
+if FWD:
+    # entry, S staged, batch prepared, then per tile: planes ready, issued, MMA done, epilogue done
+    pre = np.array([[(tr[i, j + 1] - tr[i, j]) / 1e3 for j in (1, 2, 3)] for i in live])
+    print("prologue: alloc+S staging %.2f, prep %.2f, first A + planes %.2f us" % tuple(pre.mean(0)))
+    tl = []
+    for i in live:
+        k = 4
+        while k + 3 <= n[i]:
+            tl.append([(tr[i, k + j + 1] - tr[i, k + j]) / 1e3 for j in range(3)])
+            k += 4
+    tl = np.array(tl)
+    print(f"tiles {len(tl)} ({len(tl) / len(live):.2f}/CTA): issue + next A loads {tl[:, 0].mean():.2f}, "
+          f"MMA wait {tl[:, 1].mean():.2f}, epilogue + sync {tl[:, 2].mean():.2f} us")
+    print("CTA start quantiles (us):", np.round(np.quantile(start, [0, .1, .5, .9, 1]), 1))
+    sys.exit(0)
 # prologue: entry -> batch start -> prep done -> first planes-ready
 pro = np.array([tr[i, 4] - tr[i, 1] for i in live]) / 1e3
 print(f"prologue (entry -> first tile's planes ready) mean {pro.mean():.2f} us")
