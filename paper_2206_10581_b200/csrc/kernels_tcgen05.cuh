@@ -160,15 +160,38 @@ __device__ __forceinline__ void tc_prep_nodes(const FusedArgs& a, int nb0, int n
 //   warp 16     one thread issues the six-product MMAs (A from TMEM).
 // TMEM: accumulators 2 x BN columns, then A slices 2 stages x 3 x K/2.
 // Work items (digit group g, column block cb) are dealt round-robin over the
-// CTAs with cb fastest, so consecutive items of a CTA share their A rows.
+// CTAs, so the ncb items of a group run at the same time on neighbouring CTAs
+// and share their A rows in L2.
+// Experiment bits (FusedArgs::mode, TT_TC_VARIANT): 2 no MMAs, 4 no P_F
+// stores, 8 no A loads.
 constexpr int TCF_LOADERS = 8;   // two sets of four warps
 constexpr int TCF_EPI = 8;
 constexpr int TCF_THREADS = 32 * (TCF_LOADERS + TCF_EPI + 1);
-constexpr int TCF_ES = 36;  // epilogue staging row stride (floats): conflict-free 16-byte stores and loads
+constexpr int TCF_ES = 132;  // epilogue staging row stride (floats): 128 columns + pad, conflict-free 16-byte stores
 template <int K, int BN>
 constexpr size_t tc_fwd_smem_bytes() {
-  return 2 * 3 * (size_t)K * BN * 2 + (size_t)TCF_EPI * 32 * TCF_ES * 4;
+  return 2 * 3 * (size_t)K * BN * 2 + (size_t)4 * 32 * TCF_ES * 4;
 }
+
+// A CTA's static tile schedule: items it = blockIdx.x + k * gridDim.x, tiles
+// of npt nodes (tb = first node of the tile within the item's group)
+struct TileCursor {
+  int it, g0, n, tb;
+  __device__ __forceinline__ void seek(const FusedArgs& a, int nitems) {
+    while (it < nitems) {
+      const int g = it / a.ncb;
+      g0 = a.goffF[g];
+      n = a.goffF[g + 1] - g0;
+      if (tb < n) return;
+      it += gridDim.x;
+      tb = 0;
+    }
+  }
+  __device__ __forceinline__ void advance(const FusedArgs& a, int nitems, int npt) {
+    tb += npt;
+    seek(a, nitems);
+  }
+};
 
 template <int K, int BN, int RP>
 __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
@@ -202,6 +225,17 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
   const uint32_t tm = tslot;
   const uint32_t tacc = tm, ta = tm + 2 * BN;
   const int nitems = (int)a.c.m[a.F] * a.ncb;
+  // TT_TC_TRACE=2: per-tile %globaltimer stamps, 256 per role and CTA:
+  // [0] MMA issued, [1] epilogue has the accumulator, [2] epilogue done,
+  // [3] A stage handed over by the loaders
+  long long* trace = (a.dbg && blockIdx.x < 256) ? a.dbg + (int64_t)blockIdx.x * 1024 : nullptr;
+  auto TR = [&](int role, uint32_t t) {
+    if (trace && t < 256) {
+      long long x;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
+      trace[role * 256 + t] = x;
+    }
+  };
 
   if (warp < TCF_LOADERS) {
     // ---------------- loaders ----------------
@@ -238,11 +272,9 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
         if ((int)(t & 1) != set) continue;
         const int nn = min(NPT, n - tb);
         float x[K];
-        if (jm < nn) {
-          const int node = __ldg(a.orderF + g0 + tb + jm);
-          const int p = __ldg(a.parentF + node);
-          const int64_t aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
-                                        : (int64_t)p * RP * a.c.R[a.F];
+        if (jm < nn && !(a.mode & 8)) {
+          const int pv = __ldg(a.prevF + g0 + tb + jm);
+          const int64_t aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)pv * a.c.slice[0] : (int64_t)pv * RP * a.c.R[a.F];
           const float4* src = reinterpret_cast<const float4*>(a.Abase + aoff + am * K);
 #pragma unroll
           for (int v = 0; v < K / 4; ++v) {
@@ -269,55 +301,85 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
         tc::before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&a_full[set]);
+        if (threadIdx.x == 0 || threadIdx.x == 128) TR(3, t);
       }
     }
   } else if (warp < TCF_LOADERS + TCF_EPI) {
     // ---------------- epilogue ----------------
     const int q = warp & 3, h = (warp - TCF_LOADERS) >> 2;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-    float* Ew = Es + (warp - TCF_LOADERS) * 32 * TCF_ES;
-    const int c4 = (lane & 7) * 4;
-    uint32_t t = 0;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const int g = it / a.ncb, cb = it - g * a.ncb;
-      const int g0 = a.goffF[g], n = a.goffF[g + 1] - g0;
-      for (int tb = 0; tb < n; tb += NPT, ++t) {
-        const int nn = min(NPT, n - tb);
-        // nodes of this warp's 32 rows (32 / RP of them), one per lane
-        const int jl0 = 32 * q / RP;
-        const int mynode = (lane < 32 / RP && jl0 + lane < nn) ? __ldg(a.orderF + g0 + tb + jl0 + lane) : 0;
-        const int st = t & 1;
-        tc::mbar_wait(&c_full[st], (t >> 1) & 1);
-        tc::after_sync();
-        uint32_t v[64];
+    float* Ew = Es + q * 32 * TCF_ES;  // the quadrant's 32 staging rows (shared by its two warps)
+    // the node ids of the next tile are loaded while this tile is drained
+    const int jl0 = 32 * q / RP;
+    auto tile_node = [&](const TileCursor& c) {
+      return (c.it < nitems && lane < 32 / RP && jl0 + lane < min(NPT, c.n - c.tb))
+                 ? __ldg(a.orderF + c.g0 + c.tb + jl0 + lane)
+                 : 0;
+    };
+    // one tile: accumulator stage t % 2 -> Psave rows of the tile's nodes
+    // (node ids in `mynode`, one per lane, loaded a tile ahead)
+    auto drain = [&](uint32_t t, const TileCursor& c, int mynode) {
+      const int cb = c.it % a.ncb;
+      const int nn = min(NPT, c.n - c.tb);
+      const int st = t & 1;
+      tc::mbar_wait(&c_full[st], (t >> 1) & 1);
+      tc::after_sync();
+      if (threadIdx.x == 32 * TCF_LOADERS) TR(1, t);
+      uint32_t v[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tmem_ld16_async(tacc + st * BN + lane_off + 64 * h + 16 * c, v + 16 * c);
-        tc::tmem_ld_wait();
-        tc::before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&c_empty[st]);
+      for (int cc = 0; cc < 4; ++cc) tc::tmem_ld16_async(tacc + st * BN + lane_off + 64 * h + 16 * cc, v + 16 * cc);
+      tc::tmem_ld_wait();
+      tc::before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&c_empty[st]);
+      // row (32 q + lane) of the tile: warps (q, h = 0) and (q, h = 1) write
+      // the two 64-column halves of its staging row, then warp h = 0 issues
+      // one 512-byte bulk (TMA) store of the row to its Psave segment (the
+      // TMA unit's per-operation cost makes 512-byte copies twice as fast as
+      // 256-byte ones).  The staging row is rewritten once the previous
+      // tile's copy has read it (named barrier per quadrant, 64 threads).
+      if (h == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+      float* er = Ew + lane * TCF_ES + 64 * h;
 #pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq)
-            *reinterpret_cast<float4*>(Ew + lane * TCF_ES + 4 * qq) =
-                make_float4(__uint_as_float(v[32 * hc + 4 * qq]), __uint_as_float(v[32 * hc + 4 * qq + 1]),
-                            __uint_as_float(v[32 * hc + 4 * qq + 2]), __uint_as_float(v[32 * hc + 4 * qq + 3]));
-          __syncwarp();
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            const int r = (lane >> 3) + 4 * rr;  // row within the warp's 32
-            const int jl = r / RP;               // node within the warp's rows
-            const int node = __shfl_sync(0xffffffffu, mynode, jl);
-            const float4 x = *reinterpret_cast<const float4*>(Ew + r * TCF_ES + c4);
-            if (jl0 + jl < nn)
-              *reinterpret_cast<float4*>(a.Psave + ((int64_t)node * RP + (r - jl * RP)) * a.NC + cb * BN + 64 * h +
-                                         32 * hc + c4) = x;
-          }
-          __syncwarp();
+      for (int qq = 0; qq < 16; ++qq)
+        *reinterpret_cast<float4*>(er + 4 * qq) = make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                                                              __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
+      tc::fence_async_smem();
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+      if (h == 0) {
+        const int jl = lane / RP;
+        const int node = __shfl_sync(0xffffffffu, mynode, jl);
+        if (jl0 + jl < nn && !(a.mode & 4)) {
+          float* dst = a.Psave + ((int64_t)node * RP + (lane - jl * RP)) * a.NC + cb * BN;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;\n" ::"l"(dst),
+                       "r"(tc::smem_u32(Ew + lane * TCF_ES))
+                       : "memory");
         }
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
+      if (threadIdx.x == 32 * TCF_LOADERS) TR(2, t);
+    };
+    // unrolled by two with alternating node registers: a register copy of a
+    // pending load would wait for it
+    TileCursor cur{(int)blockIdx.x, 0, 0, 0};
+    cur.seek(a, nitems);
+    TileCursor nxt = cur;
+    if (nxt.it < nitems) nxt.advance(a, nitems, NPT);
+    int nodeA = tile_node(cur), nodeB = 0;
+    uint32_t t = 0;
+    while (cur.it < nitems) {
+      nodeB = tile_node(nxt);
+      drain(t++, cur, nodeA);
+      cur = nxt;
+      if (nxt.it < nitems) nxt.advance(a, nitems, NPT);
+      if (cur.it >= nitems) break;
+      nodeA = tile_node(nxt);
+      drain(t++, cur, nodeB);
+      cur = nxt;
+      if (nxt.it < nitems) nxt.advance(a, nitems, NPT);
     }
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   } else if (lane == 0) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
@@ -335,7 +397,8 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
         tc::mbar_wait(&a_full[st], (t >> 1) & 1);
         tc::mbar_wait(&c_empty[st], ((t >> 1) & 1) ^ 1);
         tc::after_sync();
-        tc::mma_x3_ts<K / 16>(tacc + st * BN, ta + st * 3 * ACOLS, ob, idesc, false);
+        TR(0, t);
+        if (!(a.mode & 2)) tc::mma_x3_ts<K / 16>(tacc + st * BN, ta + st * 3 * ACOLS, ob, idesc, false);
         tc::commit(&a_empty[st]);
         tc::commit(&c_full[st]);
       }
@@ -555,7 +618,7 @@ inline bool tc_plan_shape(const FusedShape& f, TcShape* t) {
   t->ncbf = f.NC / 128;
   t->BNb = 128;
   t->ncbb = f.NC / 128;
-  t->smem_fwd = 2 * 3 * (size_t)f.K * 128 * 2 + (size_t)TCF_EPI * 32 * TCF_ES * 4;
+  t->smem_fwd = 2 * 3 * (size_t)f.K * 128 * 2 + (size_t)4 * 32 * TCF_ES * 4;
   t->smem_bwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 + 3 * (size_t)TC_BM * 128 * 2 + TC_META;
   t->ok = t->smem_bwd <= (size_t)FB_SMEM_MAX;
   return t->ok;

@@ -51,6 +51,24 @@ __global__ void rate(long long* out, int reps, int a_mn, int b_mn, int mode, int
     }
     if (acc.x == 1234.f) sink[t] = acc.y;
   }
+  if (t >= 32 && noise == 4) {
+    // TMEM loads of an idle region (columns 448..511) while the MMAs run:
+    // count completed 4 x 16-column load groups
+    const int w = t >> 5;
+    uint32_t r[64];
+    long long iters = 0;
+    while (!done) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16_async(tm + ((uint32_t)(32 * w) << 16) + 448 + 16 * c, r + 16 * c);
+      tmem_ld_wait();
+      ++iters;
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) x ^= r[i];
+    if (x == 12345u) sink[t] = 1.f;
+    if ((t & 31) == 0) out[148 + blockIdx.x * 4 + w] = iters;
+  }
   if (t >= 32 && noise == 1) {
     // LSU traffic: 16-byte shared loads over the operand region
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -93,7 +111,8 @@ __global__ void rate(long long* out, int reps, int a_mn, int b_mn, int mode, int
 template <int N>
 void run(int a_mn, int b_mn, int mode, int noise) {
   const int distinct = mode >= 1;
-  long long* d; cudaMalloc(&d, 148 * 8);
+  long long* d; cudaMalloc(&d, 148 * 8 * 5);
+  cudaMemset(d, 0, 148 * 8 * 5);
   float* sink; cudaMalloc(&sink, (size_t)148 << 24);  // 16 MB per CTA
   const int smem = (mode == 2 ? 3 * N * 128 : (distinct ? 3 : 1) * (128 * 128 + N * 128)) * 2;
   if (smem > 227 * 1024) { cudaFree(d); return; }
@@ -103,19 +122,27 @@ void run(int a_mn, int b_mn, int mode, int noise) {
   rate<N><<<148, 128, smem>>>(d, reps, a_mn, b_mn, mode, noise, sink);
   const cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("N=%d mode=%d noise=%d: %s\n", N, mode, noise, cudaGetErrorString(e)); exit(1); }
-  long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  long long h[148 * 5]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  if (noise == 4) {
+    double it = 0;
+    for (int i = 0; i < 148; ++i) it += h[148 + i * 4 + 1];
+    it /= 148;
+    printf("    TMEM-load warp: %.0f groups of 4 x ld16 during %.0f cycles of MMAs = %.0f cycles per group\n", it,
+           (double)h[0], h[0] / (it > 0 ? it : 1));
+  }
   double cyc = 0; for (int i = 0; i < 148; ++i) cyc += h[i]; cyc /= 148;
   const double per = cyc / (reps * 48.0);
   const double macs = 128.0 * N * 16;
   const double opbytes = (mode == 2 ? 0 : 128 * 16 * 2) + N * 16 * 2;
   printf("%s%s M=128 N=%3d a_mn=%d b_mn=%d: %.1f cycles/MMA  (%.0f MAC/clk/SM, floor %d cyc; operand smem %.0f B/clk)\n",
-         mode == 2 ? "A in TMEM       " : distinct ? "distinct planes " : "aliased planes  ", noise == 1 ? " +LDS" : noise == 2 ? " +STG" : noise == 3 ? " +LDG" : "     ", N,
+         mode == 2 ? "A in TMEM       " : distinct ? "distinct planes " : "aliased planes  ", noise == 1 ? " +LDS" : noise == 2 ? " +STG" : noise == 3 ? " +LDG" : noise == 4 ? " +TLD" : "     ", N,
          a_mn, b_mn, per, macs / per, 128 * N / 256, opbytes / per);
   cudaFree(d); cudaFree(sink);
 }
 
 int main() {
-  for (int noise = 0; noise < 4; ++noise) {
+  for (int noise = 0; noise < 5; ++noise) {
+    if (noise > 0 && noise < 4) continue;
     run<64>(0, 1, 1, noise); run<128>(0, 1, 1, noise);
     run<64>(0, 1, 2, noise); run<128>(0, 1, 2, noise); run<256>(0, 1, 2, noise);
   }

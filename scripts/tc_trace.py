@@ -26,11 +26,36 @@ for _ in range(2):
 if FWD:
     emb.forward(ti)
 emb.sync()
+def fwd_report(buf):
+    # per CTA 4 x 256 stamps: MMA issued, epilogue has acc, epilogue done, A handed over
+    T = buf[: 256 * 1024].reshape(256, 4, 256).astype(np.float64)
+    ctas = [b for b in range(256) if T[b, 0, 0] > 0]
+    t0 = min(T[b, 0, 0] for b in ctas)
+    gaps, epi, lag, lead = [], [], [], []
+    for b in ctas:
+        nt = int((T[b, 0] > 0).sum())
+        mma, e1, e2, ld = T[b, 0, :nt], T[b, 1, :nt], T[b, 2, :nt], T[b, 3, :nt]
+        gaps += list(np.diff(mma) / 1e3)
+        epi += list((e2 - e1) / 1e3)
+        lag += list((e1 - mma) / 1e3)
+        lead += list((mma - ld) / 1e3)
+    print(f"CTAs {len(ctas)}  tiles/CTA {np.mean([(T[b, 0] > 0).sum() for b in ctas]):.1f}  span {(max(T[b, 2][T[b, 2] > 0].max() for b in ctas) - t0) / 1e3:.1f} us")
+    for nm, v in (("MMA issue -> next MMA issue", gaps), ("epilogue (acc -> done)", epi),
+                  ("MMA issue -> epilogue has acc", lag), ("A handed over -> MMA issue", lead)):
+        v = np.array(v)
+        print(f"  {nm:32s} mean {v.mean():6.2f}  median {np.median(v):6.2f}  p90 {np.quantile(v, .9):6.2f} us")
+    first = np.array([(T[b, 0, 0] - t0) / 1e3 for b in ctas])
+    print(f"  first MMA after kernel start: mean {first.mean():.2f} us")
+
+
 lib = E.load_library()
 lib.tt_debug_trace.restype = C.c_int64
 buf = np.zeros(4096 * 64, np.int64)
 lib.tt_debug_trace(buf.ctypes.data_as(C.POINTER(C.c_longlong)), buf.size)
 tr = buf.reshape(4096, 64)
+if FWD:
+    fwd_report(buf)
+    sys.exit(0)
 n = tr[:, 0]
 live = np.flatnonzero(n > 2)
 t0 = tr[live, 1].min()
@@ -38,21 +63,6 @@ dur = np.array([tr[i, n[i]] - tr[i, 1] for i in live]) / 1e3
 start = (tr[live, 1] - t0) / 1e3
 end = np.array([tr[i, n[i]] for i in live] - t0) / 1e3
 print(f"CTAs {len(live)}  kernel span {end.max():.1f} us  CTA duration mean {dur.mean():.2f} median {np.median(dur):.2f} max {dur.max():.2f} us")
-if FWD:
-    # entry, S staged, batch prepared, then per tile: planes ready, issued, MMA done, epilogue done
-    pre = np.array([[(tr[i, j + 1] - tr[i, j]) / 1e3 for j in (1, 2, 3)] for i in live])
-    print("prologue: alloc+S staging %.2f, prep %.2f, first A + planes %.2f us" % tuple(pre.mean(0)))
-    tl = []
-    for i in live:
-        k = 4
-        while k + 3 <= n[i]:
-            tl.append([(tr[i, k + j + 1] - tr[i, k + j]) / 1e3 for j in range(3)])
-            k += 4
-    tl = np.array(tl)
-    print(f"tiles {len(tl)} ({len(tl) / len(live):.2f}/CTA): issue + next A loads {tl[:, 0].mean():.2f}, "
-          f"MMA wait {tl[:, 1].mean():.2f}, epilogue + sync {tl[:, 2].mean():.2f} us")
-    print("CTA start quantiles (us):", np.round(np.quantile(start, [0, .1, .5, .9, 1]), 1))
-    sys.exit(0)
 # prologue: entry -> batch start -> prep done -> first planes-ready
 pro = np.array([tr[i, 4] - tr[i, 1] for i in live]) / 1e3
 print(f"prologue (entry -> first tile's planes ready) mean {pro.mean():.2f} us")
