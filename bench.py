@@ -367,7 +367,8 @@ def main():
                           "frac": (mma_flops / (bwd_ms * 1e-3) / 1e12 / bf16_peak) if (bwd_ms > 0 and bf16_peak) else None,
                           "traffic": _traffic(name, "k_tc_bwd"), "flops_per_launch": bwd_flops, "ms_per_launch": bwd_ms,
                           "note": "frac = issued BF16 MMA FLOPs (6 per algorithmic MAC of dG_F and dA) over the "
-                                  "dense BF16 peak; the N = K = 64 MMAs are shared-memory bound (DESIGN.md c2)"},
+                                  "dense BF16 peak; the kernel is bound by forming dC on the CUDA cores (latency of "
+                                  "the per-ID loads), not by the tensor pipe (DESIGN.md c2)"},
                       "gpu_launches": tc_run["launches"]}
         emb.set_path(a.path)
 
