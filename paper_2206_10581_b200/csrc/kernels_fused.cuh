@@ -574,10 +574,18 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
-  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-    const int p = __ldg(parentL + u);
-    const float* Gsrc = Gl + (int64_t)__ldg(a.digitL + u) * sliceL;
-    const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+  // the next ID's indices are loaded while this ID is processed (one L2 round
+  // trip per ID instead of two)
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int pn = 0, dn = 0, sn0 = 0, sn1 = 0;
+  if (u < U) { pn = __ldg(parentL + u); dn = __ldg(a.digitL + u); sn0 = __ldg(a.seg + u); sn1 = __ldg(a.seg + u + 1); }
+  for (; u < U; u += nwarps) {
+    const int p = pn, s0 = sn0, s1 = sn1;
+    const float* Gsrc = Gl + (int64_t)dn * sliceL;
+    if (u + nwarps < U) {
+      pn = __ldg(parentL + u + nwarps); dn = __ldg(a.digitL + u + nwarps);
+      sn0 = __ldg(a.seg + u + nwarps); sn1 = __ldg(a.seg + u + nwarps + 1);
+    }
     for (int i = lane; i < K * NL / 4; i += 32)
       reinterpret_cast<float4*>(Gs)[i] = __ldg(reinterpret_cast<const float4*>(Gsrc) + i);
     stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
@@ -638,8 +646,11 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
   float* Ys = buf + nrow * (K + 4);
   const int64_t npad = a.c.npad;
   const int r0 = lane * RPL;
-  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-    const int p = __ldg(parentL + u);
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int pn = u < U ? __ldg(parentL + u) : 0;
+  for (; u < U; u += nwarps) {
+    const int p = pn;
+    if (u + nwarps < U) pn = __ldg(parentL + u + nwarps);  // next ID's parent under this ID
     const float* Yp = a.dY + (int64_t)u * npad;
     for (int i = lane; i < nrow * NL / 4; i += 32)
       reinterpret_cast<float4*>(Ys)[i] = __ldg(reinterpret_cast<const float4*>(Yp) + i);
