@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
+#pragma unroll 4
       for (int kk = 0; kk < K; kk += 4) {
         float4 av[8];
 #pragma unroll
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         float a0[TK], b0[TN], a1[TK], b1[TN];
         ldA(0, a0);
         load_row_frag<BN>(Ds, lane, b0);
-#pragma unroll 1
+#pragma unroll 8
         for (int m = 0; m < BM; m += 2) {
           ldA(m + 1, a1);
           load_row_frag<BN>(Ds + (m + 1) * BN, lane, b1);
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         };
         float4 c0[TMA], e0[TKA], c1[TMA], e1[TKA];
         ldX(0, c0, e0);
-#pragma unroll 1
+#pragma unroll
         for (int n = 0; n < BN; n += 8) {
           ldX(n + 4, c1, e1);
           fmaX(c0, e0);
