@@ -796,8 +796,10 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
          h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
   const int per = f.RP * f.K;
   float* dst = f.F == 1 ? h->grads : h->L.dP[f.F - 1];
-  LAUNCH(k_fused_reduce_children, grid_for(h->capk[f.F - 1] * per), 256, 0, s, c, f.F, f.ncb, per, h->counts,
-         h->cstart + (f.F - 1) * (cap + 1), h->digit, h->F.dPc, dst, h->st);
+  // 128-thread blocks: twice the blocks of a parent-per-block grid, a smaller
+  // tail over the SMs (each block streams a contiguous run of partials)
+  LAUNCH(k_fused_reduce_children, grid_for(h->capk[f.F - 1] * per, 128, 148 * 64), 128, 0, s, c, f.F, f.ncb, per,
+         h->counts, h->cstart + (f.F - 1) * (cap + 1), h->digit, h->F.dPc, dst, h->st);
   for (int k = f.F - 1; k >= 1; --k) {
     const WideShape w = wide_shape(c, k);
     if (w.ok) {

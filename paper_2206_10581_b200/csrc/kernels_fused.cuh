@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
       float o[NL];
 #pragma unroll
       for (int jl = 0; jl < NL; ++jl) o[jl] = 0.f;
-#pragma unroll 4
+#pragma unroll
       for (int r = 0; r < K; r += 4) {
         const float4 c = *reinterpret_cast<const float4*>(crow + r);
         const float cv[4] = {c.x, c.y, c.z, c.w};
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
       for (int i = 0; i < RPL; ++i)
 #pragma unroll
         for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
-#pragma unroll 4
+#pragma unroll 8
       for (int q = 0; q < nrow; ++q) {
         float yv[NL], cv[RPL];
 #pragma unroll
@@ -754,8 +754,17 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
     const int p = (int)(t / per);
     const int e = (int)(t - (int64_t)p * per);
     const int n0 = cstart_pm1[p] * ncb, n1 = cstart_pm1[p + 1] * ncb;  // (child, cb) pairs are contiguous
+    // 32 loads in flight per thread (the loop is latency-bound; the adds stay
+    // in q order, so the sum is the same for any batch size)
     float acc = 0.f;
     int q = n0;
+    for (; q + 32 <= n1; q += 32) {
+      float x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = dPc[(int64_t)(q + i) * per + e];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc += x[i];
+    }
     for (; q + 8 <= n1; q += 8) {
       float x[8];
 #pragma unroll
