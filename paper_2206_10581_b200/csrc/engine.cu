@@ -98,7 +98,6 @@ struct tt_engine {
   int* d_B = nullptr;
   int* lflags = nullptr;
   int *digit = nullptr, *parent = nullptr, *first = nullptr, *cstart = nullptr;
-  int* prevF = nullptr;  // fused level F: A-row key per node in group order
   unsigned* gk[TT_MAXD][2] = {};
   int* gv[TT_MAXD][2] = {};
   int* order[TT_MAXD] = {};
@@ -174,7 +173,7 @@ struct Phase {
 
 void free_plan(tt_engine* h) {
   void* ptrs[] = {h->keys_a, h->keys_b, h->uniq, h->pos_a, h->pos_b, h->hist, h->flag, h->seg,
-                  h->lflags, h->digit, h->parent, h->first, h->cstart, h->partial, h->prevF};
+                  h->lflags, h->digit, h->parent, h->first, h->cstart, h->partial};
   for (void* p : ptrs) cudaFree(p);
   for (int k = 0; k < TT_MAXD; ++k) {
     for (int j = 0; j < 2; ++j) { cudaFree(h->gk[k][j]); cudaFree(h->gv[k][j]); h->gk[k][j] = nullptr; h->gv[k][j] = nullptr; }
@@ -186,7 +185,7 @@ void free_plan(tt_engine* h) {
   free_fused(h->F);
   h->keys_a = h->keys_b = h->uniq = nullptr;
   h->pos_a = h->pos_b = h->hist = h->flag = h->seg = h->lflags = nullptr;
-  h->digit = h->parent = h->first = h->cstart = h->partial = h->prevF = nullptr;
+  h->digit = h->parent = h->first = h->cstart = h->partial = nullptr;
   h->cap = 0;
 }
 
@@ -215,7 +214,6 @@ int ensure_plan(tt_engine* h, int64_t B) {
   CU(dalloc(&h->parent, (int64_t)d * cap));
   CU(dalloc(&h->first, (int64_t)d * cap));
   CU(dalloc(&h->cstart, (int64_t)d * (cap + 1)));
-  CU(dalloc(&h->prevF, cap));
   const int64_t nblk = (cap + SC_BLOCK - 1) / SC_BLOCK;
   h->partial_len = nblk;
   CU(dalloc(&h->partial, nblk * TT_MAXD));
@@ -447,17 +445,7 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
     ga.m[k] = (int)c.m[k];
     mmax = std::max<int64_t>(mmax, c.m[k]);
   }
-  int64_t gx = mmax + 1;
-  if (d >= 3) {
-    const int F = d - 2;
-    ga.F = F;
-    ga.orderF = h->order[F];
-    ga.parentF = h->parent + F * cap;
-    ga.digit0 = h->digit;
-    ga.prevF = h->prevF;
-    gx = std::max<int64_t>(gx, h->capk[F]);
-  }
-  LAUNCH(k_group_offsets_all, dim3(grid_for(gx, 256, INT_MAX), d + (d >= 3 ? 1 : 0)), 256, 0, s, ga, h->counts);
+  LAUNCH(k_group_offsets_all, dim3(grid_for(mmax + 1, 256, INT_MAX), d), 256, 0, s, ga, h->counts);
   return TT_OK;
 }
 
@@ -529,7 +517,6 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
   a.digit0 = h->digit;
   a.goffF = h->goff[f.F];
   a.orderF = h->order[f.F];
-  a.prevF = h->prevF;
   a.cstartF = h->cstart + f.F * (cap + 1);
   a.digitL = h->digit + (c.d - 1) * cap;
   a.seg = h->seg;

@@ -89,7 +89,6 @@ struct FusedArgs {
   const int* digit0;        // level-0 digits (F == 1)
   const int* goffF;         // group offsets over level-F digits
   const int* orderF;        // level-F nodes in digit order
-  const int* prevF;         // per orderF slot: level-0 digit (F == 1) or parent of the node
   const int* cstartF;       // level-F node -> range of distinct IDs
   const int* digitL;        // digits i_d of the distinct IDs
   const int* seg;           // distinct ID -> sorted batch slots

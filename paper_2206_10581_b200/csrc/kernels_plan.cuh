@@ -443,29 +443,12 @@ struct GroupOffArgs {
   const unsigned* sdig[TT_MAXD];
   int* goff[TT_MAXD];
   int m[TT_MAXD];
-  // fused level F (d >= 3): prevF[i] = A-row key of the i-th level-F node in
-  // group order -- its level-0 digit when F == 1, else its parent node --
-  // so the fused kernels' row gathers are one index load deep
-  int F;
-  const int* orderF;
-  const int* parentF;
-  const int* digit0;
-  int* prevF;
 };
 
-// all levels at once: blockIdx.y = level; the extra last slice (when prevF
-// is set) gathers prevF
+// all levels at once: blockIdx.y = level
 __global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ counts) {
   TT_PDL_ENTRY();
   const int k = blockIdx.y;
-  if (ga.prevF && k == (int)gridDim.y - 1) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < ld_count(&counts[ga.F])) {
-      const int p = ga.parentF[ga.orderF[i]];
-      ga.prevF[i] = ga.F == 1 ? ga.digit0[p] : p;
-    }
-    return;
-  }
   const int n = ld_count(&counts[k]);
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > ga.m[k]) return;

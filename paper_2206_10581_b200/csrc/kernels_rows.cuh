@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_dy_chunks(const float* __restrict__ up,
       acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  // rows are loaded 8 at a time (independent 16-byte loads in flight), then
+  // rows are loaded PF at a time (independent 16-byte loads in flight), then
   // summed in slot order
   constexpr int PF = NV <= 2 ? 8 : 4;
   for (int i0 = 0; i0 < hi - lo; i0 += PF) {
@@ -118,15 +118,20 @@ __global__ void __launch_bounds__(256) k_dy_groups(int B, int64_t npad, const in
   float4 acc[4];
   int cur = -1;
   // a run that holds all of u's continuation chunks is seeded with the tail
-  // partial of u's first chunk (strict chunk order) and completes dY[u]
-  auto complete = [&](int u) {
-    const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
-    return !(c0 + 1 < cbase) && !(c1 > cbase + 31);
-  };
+  // partial of u's first chunk (strict chunk order) and completes dY[u].
+  // Per lane (chunk), the run facts of its ID are loaded in parallel before
+  // the serial walk: whether a run here completes dY[u], whether u's
+  // continuations began before this group, and u's first chunk.
+  int my_first = 0, my_flags = 0;
+  if (my_u >= 0) {
+    const int c0 = seg[my_u] / DY_CHUNK, c1 = (seg[my_u + 1] - 1) / DY_CHUNK;
+    my_first = c0;
+    const bool complete = !(c0 + 1 < cbase) && !(c1 > cbase + 31);
+    my_flags = (complete ? 1 : 0) | (c0 + 1 < cbase ? 2 : 0);
+  }
+  int cur_flags = 0;
   auto emit = [&](int u) {
-    const int c0 = seg[u] / DY_CHUNK;
-    const bool before = c0 + 1 < cbase;
-    float* dst = complete(u) ? dY + (int64_t)u * npad : gpart + ((int64_t)G * 2 + (before ? 0 : 1)) * npad;
+    float* dst = (cur_flags & 1) ? dY + (int64_t)u * npad : gpart + ((int64_t)G * 2 + ((cur_flags & 2) ? 0 : 1)) * npad;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int64_t c = (int64_t)v * 128 + lane * 4;
@@ -135,13 +140,15 @@ __global__ void __launch_bounds__(256) k_dy_groups(int B, int64_t npad, const in
   };
   for (int i = 0; i < 32; ++i) {
     const int u = __shfl_sync(0xffffffffu, my_u, i);
+    const int fl = __shfl_sync(0xffffffffu, my_flags, i), first = __shfl_sync(0xffffffffu, my_first, i);
     if (u != cur) {
       if (cur >= 0) emit(cur);
       cur = u;
+      cur_flags = fl;
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u >= 0 && complete(u)) {
-        const float* head = part + ((int64_t)(seg[u] / DY_CHUNK) * 2 + 1) * npad;
+      if (u >= 0 && (fl & 1)) {
+        const float* head = part + ((int64_t)first * 2 + 1) * npad;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int64_t c = (int64_t)v * 128 + lane * 4;
@@ -174,11 +181,24 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
   const int U = ld_count(&counts[d - 1]);
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-    const int c0 = seg[u] / DY_CHUNK, c1 = (seg[u + 1] - 1) / DY_CHUNK;
-    if (c0 == c1) continue;
+  // each lane tests one ID (32 per step); the warp then finishes the IDs
+  // that span several chunk groups, in lane order
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int ub = warp * 32; ub < U; ub += nwarps * 32) {
+    const int mu = ub + lane;
+    int mc0 = 0, mc1 = 0;
+    if (mu < U) {
+      mc0 = seg[mu] / DY_CHUNK;
+      mc1 = (seg[mu + 1] - 1) / DY_CHUNK;
+    }
+    // k_dy_groups completes IDs within one chunk or one group
+    unsigned todo = __ballot_sync(0xffffffffu, mu < U && mc0 != mc1 && (mc0 + 1) / 32 != mc1 / 32);
+    while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int u = ub + src;
+    const int c0 = __shfl_sync(0xffffffffu, mc0, src), c1 = __shfl_sync(0xffffffffu, mc1, src);
     const int G0 = (c0 + 1) / 32, G1 = c1 / 32;
-    if (G0 == G1) continue;  // completed by k_dy_groups
     for (int64_t c = lane * 4; c < npad; c += 128) {
       float4 acc = *reinterpret_cast<const float4*>(part + ((int64_t)c0 * 2 + 1) * npad + c);
       float4 x = *reinterpret_cast<const float4*>(gpart + ((int64_t)G0 * 2 + 1) * npad + c);
@@ -188,6 +208,7 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
         acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
       }
       *reinterpret_cast<float4*>(dY + (int64_t)u * npad + c) = acc;
+    }
     }
   }
 }

@@ -273,8 +273,10 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
         const int nn = min(NPT, n - tb);
         float x[K];
         if (jm < nn && !(a.mode & 8)) {
-          const int pv = __ldg(a.prevF + g0 + tb + jm);
-          const int64_t aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)pv * a.c.slice[0] : (int64_t)pv * RP * a.c.R[a.F];
+          const int node = __ldg(a.orderF + g0 + tb + jm);
+          const int p = __ldg(a.parentF + node);
+          const int64_t aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
+                                        : (int64_t)p * RP * a.c.R[a.F];
           const float4* src = reinterpret_cast<const float4*>(a.Abase + aoff + am * K);
 #pragma unroll
           for (int v = 0; v < K / 4; ++v) {
