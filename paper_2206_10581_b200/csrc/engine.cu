@@ -707,7 +707,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
 #undef TT_LL_CASE
   }
   if (d_out)
-    LAUNCH(k_scatter_heavy, grid_for(h->B * (c.emb_dim / 4)), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
+    LAUNCH(k_scatter_heavy, grid_for((h->B + 31) / 32 * 32, 256, 148 * 8), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);
   return TT_OK;
 }

@@ -213,22 +213,49 @@ __global__ void __launch_bounds__(256) k_dy_spans(const int* __restrict__ counts
   }
 }
 
-// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS positions)
+// out[pos] = Yu[u] for the slots of heavy IDs (more than HEAVY_POS positions).
+// Warp per 32 sorted slots: the lanes look up their slot's ID, segment and
+// position in parallel, then the warp copies the ID's row (loaded once per run
+// of equal IDs; a heavy ID's slots are contiguous) to each heavy slot's
+// position, 16 bytes per lane.
 __global__ void __launch_bounds__(256) k_scatter_heavy(int B, int64_t emb, int64_t npad, const int* __restrict__ uid1,
                                                        const int* __restrict__ spos, const int* __restrict__ seg,
                                                        const float* __restrict__ Yu, float* __restrict__ out,
                                                        const DevStatus* st) {
   TT_PDL_ENTRY();
   if (tt_failed(st)) return;
-  const int64_t per = emb / 4;
-  const int64_t total = (int64_t)B * per;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int s = (int)(t / per);
-    const int64_t c = (t - (int64_t)s * per) * 4;
-    const int u = uid1[s] - 1;
-    if (seg[u + 1] - seg[u] <= HEAVY_POS) continue;
-    *reinterpret_cast<float4*>(out + (int64_t)spos[s] * emb + c) =
-        *reinterpret_cast<const float4*>(Yu + (int64_t)u * npad + c);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = (int)((emb + 127) / 128);  // float4 column groups per lane (emb <= 512)
+  for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < B; base += nwarps * 32) {
+    const int s = base + lane;
+    int u = -1, pos = 0;
+    if (s < B) {
+      u = uid1[s] - 1;
+      if (seg[u + 1] - seg[u] > HEAVY_POS) pos = spos[s];
+      else u = -1;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, u >= 0);
+    int cu = -1;
+    float4 row[4];
+    while (todo) {
+      const int i = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int uu = __shfl_sync(0xffffffffu, u, i), p = __shfl_sync(0xffffffffu, pos, i);
+      if (uu != cu) {
+        cu = uu;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int64_t c = (int64_t)v * 128 + lane * 4;
+          if (v < nv && c < emb) row[v] = *reinterpret_cast<const float4*>(Yu + (int64_t)uu * npad + c);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int64_t c = (int64_t)v * 128 + lane * 4;
+        if (v < nv && c < emb) *reinterpret_cast<float4*>(out + (int64_t)p * emb + c) = row[v];
+      }
+    }
   }
 }
 
