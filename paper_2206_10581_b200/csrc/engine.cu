@@ -103,8 +103,7 @@ struct tt_engine {
   int* order[TT_MAXD] = {};
   unsigned* sdig[TT_MAXD] = {};
   int* goff[TT_MAXD] = {};
-  int* partial = nullptr;
-  int64_t partial_len = 0;
+  unsigned long long* scan_status = nullptr;  // single-pass scan: [narr][nblk] status words + [narr] tickets
   LevelBufs L{};
   int64_t capk[TT_MAXD] = {};
   FusedBufs F{};
@@ -173,7 +172,7 @@ struct Phase {
 
 void free_plan(tt_engine* h) {
   void* ptrs[] = {h->keys_a, h->keys_b, h->uniq, h->pos_a, h->pos_b, h->hist, h->flag, h->seg,
-                  h->lflags, h->digit, h->parent, h->first, h->cstart, h->partial};
+                  h->lflags, h->digit, h->parent, h->first, h->cstart, h->scan_status};
   for (void* p : ptrs) cudaFree(p);
   for (int k = 0; k < TT_MAXD; ++k) {
     for (int j = 0; j < 2; ++j) { cudaFree(h->gk[k][j]); cudaFree(h->gv[k][j]); h->gk[k][j] = nullptr; h->gv[k][j] = nullptr; }
@@ -185,7 +184,8 @@ void free_plan(tt_engine* h) {
   free_fused(h->F);
   h->keys_a = h->keys_b = h->uniq = nullptr;
   h->pos_a = h->pos_b = h->hist = h->flag = h->seg = h->lflags = nullptr;
-  h->digit = h->parent = h->first = h->cstart = h->partial = nullptr;
+  h->digit = h->parent = h->first = h->cstart = nullptr;
+  h->scan_status = nullptr;
   h->cap = 0;
 }
 
@@ -215,8 +215,7 @@ int ensure_plan(tt_engine* h, int64_t B) {
   CU(dalloc(&h->first, (int64_t)d * cap));
   CU(dalloc(&h->cstart, (int64_t)d * (cap + 1)));
   const int64_t nblk = (cap + SC_BLOCK - 1) / SC_BLOCK;
-  h->partial_len = nblk;
-  CU(dalloc(&h->partial, nblk * TT_MAXD));
+  CU(dalloc(&h->scan_status, (nblk + 1) * TT_MAXD));
   int64_t prod = 1;
   for (int k = 0; k < d; ++k) {
     prod = (prod > (int64_t)1 << 40) ? prod : prod * c.m[k];
@@ -375,12 +374,14 @@ void sort_levels(tt_engine* h, cudaStream_t s) {
   LAUNCH(k_rs_scatter<unsigned>, dim3(ntiles, d - 1), RS_THREADS, smem, s, rb, 0, nbits);
 }
 
+// one memset (status words + tickets) and one single-pass scan kernel
 void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax,
                     const ScanFlags& sf) {
   const int nblk = (int)((nmax + SC_BLOCK - 1) / SC_BLOCK);
-  LAUNCH(k_scan_blocks, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk, sf);
-  LAUNCH(k_scan_partials, narr, 1024, 0, s, h->partial, nblk);
-  LAUNCH(k_scan_add, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, h->partial, nblk);
+  unsigned long long* status = h->scan_status;
+  unsigned long long* ticket = status + (int64_t)narr * nblk;
+  cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ((size_t)narr * nblk + narr), s);
+  LAUNCH(k_scan_onepass, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, status, ticket, nblk, sf);
 }
 
 __global__ void k_reset_status(DevStatus* st, int which) {

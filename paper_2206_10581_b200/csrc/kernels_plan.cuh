@@ -270,88 +270,101 @@ struct ScanFlags {
   unsigned long long div[TT_MAXD];
 };
 
-__global__ void __launch_bounds__(SC_THREADS) k_scan_blocks(int* __restrict__ a, int64_t stride,
-                                                            const int* n_dev, int* __restrict__ partial,
-                                                            int nblk, ScanFlags sf) {
+// Single-pass inclusive scan (chained scan with decoupled look-back): block
+// tickets in launch order, each block publishes its aggregate (state 1) and,
+// once its prefix is known, its inclusive prefix (state 2) in a 64-bit status
+// word; a block walks back over its predecessors' words until it meets an
+// inclusive prefix.  status[narr][nblk] and ticket[narr] are zeroed before
+// the launch.  Blocks only wait on lower tickets, which belong to blocks
+// already running, so the scan cannot deadlock.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_onepass(int* __restrict__ a, int64_t stride, const int* n_dev,
+                                                             unsigned long long* __restrict__ status,
+                                                             unsigned long long* __restrict__ ticket, int nblk,
+                                                             ScanFlags sf) {
   TT_PDL_ENTRY();
   __shared__ int wsum[SC_THREADS / 32];
+  __shared__ int s_blk, s_prefix;
+  if (threadIdx.x == 0) s_blk = (int)atomicAdd(ticket + blockIdx.y, 1ull);
+  __syncthreads();
+  const int blk = s_blk;
   const int n = ld_count(n_dev);
+  if (blk * SC_BLOCK >= n) return;  // later tickets are past n as well
   int* arr = a + blockIdx.y * stride;
-  const int i0 = blockIdx.x * SC_BLOCK + threadIdx.x * SC_ITEMS;
-  if (blockIdx.x * SC_BLOCK >= n) {
-    if (threadIdx.x == 0) partial[blockIdx.y * nblk + blockIdx.x] = 0;
-    return;
-  }
+  unsigned long long* stt = status + (int64_t)blockIdx.y * nblk;
+  const int i0 = blk * SC_BLOCK + threadIdx.x * SC_ITEMS;
   int v[SC_ITEMS];
   int t = 0;
+  const unsigned long long dv = sf.div[blockIdx.y];
+  if (sf.keys) {  // flags: key prefix (key / dv) differs from the previous slot's; one division per slot
+    auto q = [&](int s) { return dv == 1 ? sf.keys[s] : sf.keys[s] / dv; };
+    unsigned long long prev = (i0 > 0 && i0 - 1 < n) ? q(i0 - 1) : ~0ull;
 #pragma unroll
-  for (int j = 0; j < SC_ITEMS; ++j) {
-    const int s = i0 + j;
-    const unsigned long long dv = sf.div[blockIdx.y];
-    v[j] = s < n ? (sf.keys ? ((s == 0 || sf.keys[s] / dv != sf.keys[s - 1] / dv) ? 1 : 0) : arr[s]) : 0;
-    t += v[j];
-    v[j] = t;
+    for (int j = 0; j < SC_ITEMS; ++j) {
+      const int s = i0 + j;
+      int f = 0;
+      if (s < n) {
+        const unsigned long long cur = q(s);
+        f = (s == 0 || cur != prev) ? 1 : 0;
+        prev = cur;
+      }
+      t += f;
+      v[j] = t;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < SC_ITEMS; ++j) {
+      const int s = i0 + j;
+      t += s < n ? arr[s] : 0;
+      v[j] = t;
+    }
   }
   int total;
-  int off = block_excl_scan_256(t, wsum, total);
+  const int off = block_excl_scan_256(t, wsum, total);
+  if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
+    const int lane = threadIdx.x;
+    int prefix = 0;
+    if (blk == 0) {
+      if (lane == 0) st_release_u64(stt, (2ull << 62) | (unsigned)total);
+    } else {
+      if (lane == 0) st_release_u64(stt + blk, (1ull << 62) | (unsigned)total);
+      for (int hi = blk - 1; hi >= 0; hi -= 32) {
+        const int i = hi - lane;  // lane 0 = nearest predecessor
+        unsigned long long w = 2ull << 62;  // past block 0: contributes nothing
+        if (i >= 0) {
+          do {
+            w = ld_acquire_u64(stt + i);
+          } while ((w >> 62) == 0);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, i >= 0 && (w >> 62) == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive prefix in the window
+        int x = (lane <= stop && i >= 0) ? (int)(unsigned)(w & 0xffffffffull) : 0;
 #pragma unroll
-  for (int j = 0; j < SC_ITEMS; ++j)
-    if (i0 + j < n) arr[i0 + j] = v[j] + off;
-  if (threadIdx.x == 0) partial[blockIdx.y * nblk + blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_partials(int* __restrict__ partial, int nblk) {
-  TT_PDL_ENTRY();
-  // exclusive scan of partial[blockIdx.x * nblk ..]
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  int* p = partial + blockIdx.x * nblk;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nblk; base += 1024) {
-    int i = base + threadIdx.x;
-    int t = i < nblk ? p[i] : 0;
-    int x = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane_id() >= (unsigned)o) x += y;
-    }
-    if (lane_id() == 31) wsum[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int w = wsum[threadIdx.x];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane_id() >= (unsigned)o) w += y;
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        prefix += x;
+        if (incl) break;
       }
-      wsum[threadIdx.x] = w;
+      if (lane == 0) st_release_u64(stt + blk, (2ull << 62) | (unsigned)(prefix + total));
     }
-    __syncthreads();
-    int excl = carry + (x - t) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
-    if (i < nblk) p[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + t;
-    __syncthreads();
+    if (lane == 0) s_prefix = prefix;
   }
-}
-
-__global__ void __launch_bounds__(SC_THREADS) k_scan_add(int* __restrict__ a, int64_t stride, const int* n_dev,
-                                                         const int* __restrict__ partial, int nblk) {
-  TT_PDL_ENTRY();
-  const int n = ld_count(n_dev);
-  if (blockIdx.x == 0 || blockIdx.x * SC_BLOCK >= n) return;
-  int* arr = a + blockIdx.y * stride;
-  const int off = partial[blockIdx.y * nblk + blockIdx.x];
-  const int i0 = blockIdx.x * SC_BLOCK + threadIdx.x * SC_ITEMS;
+  __syncthreads();
+  const int base = off + s_prefix;
 #pragma unroll
   for (int j = 0; j < SC_ITEMS; ++j)
-    if (i0 + j < n) arr[i0 + j] += off;
+    if (i0 + j < n) arr[i0 + j] = v[j] + base;
 }
 
 // ---------------------------------------------------------------------------
-// unique IDs over the sorted keys (flags formed inside k_scan_blocks)
+// unique IDs over the sorted keys (flags formed inside k_scan_onepass)
 // After the inclusive scan: uniq[u] = key, seg[u] = first sorted slot.
 // counts[d-1] = U, seg[U] = B.
 __global__ void k_unique_emit(const unsigned long long* __restrict__ skey, int B, const int* __restrict__ scan,
