@@ -699,8 +699,13 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
 #define TT_LL_CASE(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
     const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (k_ + 4) + k_ * nl_); \
-    CU(cudaFuncSetAttribute((k_last_level<k_, nl_>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-    LAUNCH((k_last_level<k_, nl_>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+    if ((int64_t)f.RP * f.nF * k_ <= 2048) { \
+      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_last_level<k_, nl_, true>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+    } else { \
+      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_last_level<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+    } \
   }
     if (false) {
     }
@@ -773,8 +778,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
 #define TT_W_CASE(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
     const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (k_ + 4) + f.RP * f.nF * nl_); \
-    CU(cudaFuncSetAttribute((k_fused_w<k_, nl_>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-    LAUNCH((k_fused_w<k_, nl_>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
+    if ((int64_t)f.RP * f.nF * k_ <= 2048 && (int64_t)f.RP * f.nF * nl_ <= 256) { \
+      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_fused_w<k_, nl_, true>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
+    } else { \
+      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_fused_w<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
+    } \
   }
   if (false) {
   }

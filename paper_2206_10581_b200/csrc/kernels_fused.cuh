@@ -558,36 +558,72 @@ __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp,
 // out[(q, jl)] = sum_r P_F[prefix][q][r] G_{d-1}[r, i_d, jl]; a row's NL
 // outputs are contiguous, so a warp writes one contiguous output row per batch
 // position.  IDs with more than HEAVY_POS positions go to Yu (k_scatter_heavy).
-template <int K, int NL>
+// PIPE (prefix blocks of <= 2048 floats): the next ID's block and last-core
+// slice are loaded into registers while this ID is computed from shared
+// memory, so every warp keeps a block in flight; the indices run one ID ahead
+// of that.
+template <int K, int NL, bool PIPE>
 __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, const int* __restrict__ counts,
                                                               const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
+  constexpr int PB = 16;                      // block float4 per lane (PIPE)
+  constexpr int GV = (K * NL / 4 + 31) / 32;  // slice float4 per lane (PIPE)
   const int U = ld_count(&counts[a.c.d - 1]);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  const int n4 = nrow * (K / 4);
   float* buf = sk_smem + wib * (nrow * (K + 4) + K * NL);
   float* Gs = buf + nrow * (K + 4);
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
-  // the next ID's indices are loaded while this ID is processed (one L2 round
-  // trip per ID instead of two)
+  float4 pv[PIPE ? PB : 1], gr[PIPE ? GV : 1];
+  auto issue = [&](int p, int dg) {  // a block and slice into registers
+    const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
+#pragma unroll
+    for (int b = 0; b < PB; ++b)
+      if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+    const float4* gs = reinterpret_cast<const float4*>(Gl + (int64_t)dg * sliceL);
+#pragma unroll
+    for (int b = 0; b < GV; ++b)
+      if (b * 32 + lane < K * NL / 4) gr[b] = __ldg(gs + b * 32 + lane);
+  };
   int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int pn = 0, dn = 0, sn0 = 0, sn1 = 0;
   if (u < U) { pn = __ldg(parentL + u); dn = __ldg(a.digitL + u); sn0 = __ldg(a.seg + u); sn1 = __ldg(a.seg + u + 1); }
+  if constexpr (PIPE) {
+    if (u < U) issue(pn, dn);
+  }
   for (; u < U; u += nwarps) {
-    const int p = pn, s0 = sn0, s1 = sn1;
-    const float* Gsrc = Gl + (int64_t)dn * sliceL;
-    if (u + nwarps < U) {
-      pn = __ldg(parentL + u + nwarps); dn = __ldg(a.digitL + u + nwarps);
-      sn0 = __ldg(a.seg + u + nwarps); sn1 = __ldg(a.seg + u + nwarps + 1);
+    const int p = pn, dg = dn, s0 = sn0, s1 = sn1;
+    const int un = u + nwarps;
+    if (un < U) {  // the next ID's indices under this ID
+      pn = __ldg(parentL + un); dn = __ldg(a.digitL + un);
+      sn0 = __ldg(a.seg + un); sn1 = __ldg(a.seg + un + 1);
     }
-    for (int i = lane; i < K * NL / 4; i += 32)
-      reinterpret_cast<float4*>(Gs)[i] = __ldg(reinterpret_cast<const float4*>(Gsrc) + i);
-    stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    if constexpr (PIPE) {
+#pragma unroll
+      for (int b = 0; b < PB; ++b) {
+        const int i = b * 32 + lane;
+        if (i < n4) {
+          const int row = i / (K / 4), c4 = i - row * (K / 4);
+          *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < GV; ++b)
+        if (b * 32 + lane < K * NL / 4) reinterpret_cast<float4*>(Gs)[b * 32 + lane] = gr[b];
+      __syncwarp();
+      if (un < U) issue(pn, dn);  // lands while this ID is computed
+    } else {
+      const float* Gsrc = Gl + (int64_t)dg * sliceL;
+      for (int i = lane; i < K * NL / 4; i += 32)
+        reinterpret_cast<float4*>(Gs)[i] = __ldg(reinterpret_cast<const float4*>(Gsrc) + i);
+      stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    }
     const float* Gp = Gs;
     for (int q = lane; q < nrow; q += 32) {
       const float* crow = buf + q * (K + 4);
@@ -630,30 +666,64 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
 // W_u = P_F[prefix(u)]^T dY_u over all NC columns (K x n_d per distinct ID):
 // the last core's gradient contributions.  Lane owns RPL rank rows and sums
 // over the block's nrow rows (no cross-lane reduction).
-template <int K, int NL>
+template <int K, int NL, bool PIPE>
 __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const int* __restrict__ counts,
                                                            const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
   if (tt_failed(a.st)) return;
   constexpr int RPL = K >= 32 ? K / 32 : 1;
+  constexpr int PB = 16;  // block float4 per lane (PIPE: blocks of <= 2048 floats)
+  constexpr int YB = 2;   // dY float4 per lane (PIPE: nrow * NL <= 256)
   const int U = ld_count(&counts[a.c.d - 1]);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  const int n4 = nrow * (K / 4), y4 = nrow * NL / 4;
   float* buf = sk_smem + wib * (nrow * (K + 4) + nrow * NL);
   float* Ys = buf + nrow * (K + 4);
   const int64_t npad = a.c.npad;
   const int r0 = lane * RPL;
+  float4 pv[PIPE ? PB : 1], yr[PIPE ? YB : 1];
+  auto issue = [&](int u, int p) {  // ID u's prefix block and dY row into registers
+    const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
+#pragma unroll
+    for (int b = 0; b < PB; ++b)
+      if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+    const float4* ys = reinterpret_cast<const float4*>(a.dY + (int64_t)u * npad);
+#pragma unroll
+    for (int b = 0; b < YB; ++b)
+      if (b * 32 + lane < y4) yr[b] = __ldg(ys + b * 32 + lane);
+  };
   int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int pn = u < U ? __ldg(parentL + u) : 0;
+  if constexpr (PIPE) {
+    if (u < U) issue(u, pn);
+  }
   for (; u < U; u += nwarps) {
     const int p = pn;
-    if (u + nwarps < U) pn = __ldg(parentL + u + nwarps);  // next ID's parent under this ID
-    const float* Yp = a.dY + (int64_t)u * npad;
-    for (int i = lane; i < nrow * NL / 4; i += 32)
-      reinterpret_cast<float4*>(Ys)[i] = __ldg(reinterpret_cast<const float4*>(Yp) + i);
-    stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    const int un = u + nwarps;
+    if (un < U) pn = __ldg(parentL + un);  // next ID's parent under this ID
+    if constexpr (PIPE) {
+#pragma unroll
+      for (int b = 0; b < PB; ++b) {
+        const int i = b * 32 + lane;
+        if (i < n4) {
+          const int row = i / (K / 4), c4 = i - row * (K / 4);
+          *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < YB; ++b)
+        if (b * 32 + lane < y4) reinterpret_cast<float4*>(Ys)[b * 32 + lane] = yr[b];
+      __syncwarp();
+      if (un < U) issue(un, pn);  // lands while this ID is computed
+    } else {
+      const float* Yp = a.dY + (int64_t)u * npad;
+      for (int i = lane; i < y4; i += 32)
+        reinterpret_cast<float4*>(Ys)[i] = __ldg(reinterpret_cast<const float4*>(Yp) + i);
+      stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+    }
     if (r0 < K) {
       float wv[RPL][NL];
 #pragma unroll
