@@ -31,13 +31,22 @@ __global__ void k_check_finite(DevCfg c, const float* __restrict__ grads, int ve
   int bad = INT_MAX;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   if (vec4) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < c.nparams / 4; q += step) {
-      const float4 g = reinterpret_cast<const float4*>(grads)[q];
-      if (!(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w))) {
-        int k;
-        int64_t v;
-        locate(c, q * 4, k, v);
-        if (grads[c.tc_off[k] + v] > 0.f && k < bad) bad = k;
+    // four independent 16-byte loads per thread per step
+    const int64_t n4 = c.nparams / 4;
+    for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < n4; q0 += 4 * step) {
+      float4 g[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (q0 + i * step < n4) g[i] = reinterpret_cast<const float4*>(grads)[q0 + i * step];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t q = q0 + i * step;
+        if (q < n4 && !(isfinite(g[i].x) && isfinite(g[i].y) && isfinite(g[i].z) && isfinite(g[i].w))) {
+          int k;
+          int64_t v;
+          locate(c, q * 4, k, v);
+          if (grads[c.tc_off[k] + v] > 0.f && k < bad) bad = k;
+        }
       }
     }
   } else {
