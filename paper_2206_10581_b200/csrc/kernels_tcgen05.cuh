@@ -30,17 +30,8 @@ struct TcShape {
   size_t smem_fwd, smem_bwd;
 };
 
-// metadata area shared by both kernels (node batch of FB_NB)
+// metadata area of the backward (node batch of FB_NB)
 constexpr size_t TC_META = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 64;
-
-template <int K, int BN>
-constexpr size_t tc_fwd_smem() {
-  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + TC_META;
-}
-template <int K, int BN>
-constexpr size_t tc_bwd_smem() {
-  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + 3 * (size_t)TC_BM * BN * 2 + TC_META;
-}
 
 // Plane writers map 8 consecutive threads to the 8 rows of one core matrix
 // (unit u: row-in-core = u % 8), so each 16-byte store phase covers 128
@@ -168,8 +159,9 @@ constexpr int TCF_LOADERS = 8;   // two sets of four warps
 constexpr int TCF_EPI = 8;
 constexpr int TCF_THREADS = 32 * (TCF_LOADERS + TCF_EPI + 1);
 constexpr int TCF_ES = 132;  // epilogue staging row stride (floats): 128 columns + pad, conflict-free 16-byte stores
-template <int K, int BN>
-constexpr size_t tc_fwd_smem_bytes() {
+// dynamic shared memory: forward = S ring (2 stages x 3 slices of K x BN)
+// + the epilogue's staging rows; backward = S, A and dC planes + metadata
+inline size_t tc_fwd_smem(int K, int BN) {
   return 2 * 3 * (size_t)K * BN * 2 + (size_t)4 * 32 * TCF_ES * 4;
 }
 
@@ -419,6 +411,9 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
 // dependent L2 loads (ID digit -> last-core slice), so latency is hidden by
 // warps, and one CTA holds the whole 192 KB operand set per SM.
 constexpr int TCB_THREADS = 512;
+inline size_t tc_bwd_smem(int K, int BN) {
+  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + 3 * (size_t)TC_BM * BN * 2 + TC_META;
+}
 
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
@@ -620,8 +615,8 @@ inline bool tc_plan_shape(const FusedShape& f, TcShape* t) {
   t->ncbf = f.NC / 128;
   t->BNb = 128;
   t->ncbb = f.NC / 128;
-  t->smem_fwd = 2 * 3 * (size_t)f.K * 128 * 2 + (size_t)4 * 32 * TCF_ES * 4;
-  t->smem_bwd = 3 * (size_t)f.K * 128 * 2 + 3 * (size_t)TC_BM * f.K * 2 + 3 * (size_t)TC_BM * 128 * 2 + TC_META;
+  t->smem_fwd = tc_fwd_smem(f.K, 128);
+  t->smem_bwd = tc_bwd_smem(f.K, 128);
   t->ok = t->smem_bwd <= (size_t)FB_SMEM_MAX;
   return t->ok;
 }
