@@ -831,8 +831,13 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
 
 void touch_counters(tt_engine* h, cudaStream_t s) {
   const DevCfg& c = h->dc;
-  for (int k = 0; k < c.d; ++k)
-    LAUNCH(k_touch_counters, grid_for(c.m[k], 256, INT_MAX), 256, 0, s, c, k, h->goff[k], h->grads, 0, h->st);
+  GoffPtrs gp{};
+  int64_t mmax = 0;
+  for (int k = 0; k < c.d; ++k) {
+    gp.goff[k] = h->goff[k];
+    mmax = std::max<int64_t>(mmax, c.m[k]);
+  }
+  LAUNCH(k_touch_counters, dim3(grid_for(mmax, 256, INT_MAX), c.d), 256, 0, s, c, gp, h->grads, 0, h->st);
 }
 
 bool use_fused(tt_engine* h) { return h->path_pref != 1 && h->fused_ok; }

@@ -154,14 +154,20 @@ __global__ void k_gen_bwd_core0(DevCfg c, LevelBufs L, const int* __restrict__ c
   }
 }
 
-// touch counters: tc[k][v] = nodes with digit v at level k (0 = untouched)
-__global__ void k_touch_counters(DevCfg c, int k, const int* __restrict__ goff, float* __restrict__ grads,
-                                 int accumulate, const DevStatus* st) {
+// touch counters: tc[k][v] = nodes with digit v at level k (0 = untouched);
+// all levels in one launch (blockIdx.y = level)
+struct GoffPtrs {
+  const int* goff[TT_MAXD];
+};
+__global__ void k_touch_counters(DevCfg c, GoffPtrs gp, float* __restrict__ grads, int accumulate,
+                                 const DevStatus* st) {
   TT_PDL_ENTRY();
   if (tt_failed(st)) return;
-  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= c.m[k]) return;
-  float cnt = (float)(goff[v + 1] - goff[v]);
+  const int* goff = gp.goff[k];
+  const float cnt = (float)(goff[v + 1] - goff[v]);
   float* tc = grads + c.tc_off[k] + v;
   *tc = accumulate ? *tc + cnt : cnt;
 }
