@@ -851,9 +851,10 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 
 // The (K, BN, RP, NL) instantiations compiled into the library (engine.cu
 // FUSED_SWITCH): papers, products / sweep32, small, billion, sweep16,
-// sweep64, sweep128.
+// sweep64, sweep128, sweep8.
 #define TT_FUSED_SHAPES(X) \
-  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8)
+  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8) \
+  X(8, 32, 4, 8)
 #define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
@@ -871,6 +872,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   const int64_t K = c.R[F], NC = c.cols[F], R2 = c.R[F + 1], NL = c.n[c.d - 1], RP = c.rows[F];
   if (R2 != K) return false;
   int BN = 0;
+  if (K == 8 && NC % 32 == 0) BN = 32;
   if (K == 16 && NC % 64 == 0) BN = 64;
   if (K == 32 && NC % 128 == 0) BN = 128;
   if (K == 64 && NC % 128 == 0) BN = 128;

@@ -1,8 +1,9 @@
-# Round evidence in one call: bench lines (all measured configs, FFMA headline +
+# Round evidence in one call: bench lines (all BASELINE configs incl. the rank
+# sweep, FFMA headline +
 # tensor path), ncu launch lists (FFMA and tc paths at papers) and one
 # --set full capture of the four GEMM kernels.  Summaries go to gpurun_out/ev_*.
 set -x
-for cfg in ${CFGS:-papers products small billion}; do
+for cfg in ${CFGS:-papers products small billion sweep8 sweep16 sweep32 sweep64 sweep128}; do
   timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 > gpurun_out/ev_bench_$cfg.json 2> gpurun_out/ev_bench_$cfg.err
   python scripts/bench_summary.py gpurun_out/ev_bench_$cfg.json
 done

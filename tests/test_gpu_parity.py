@@ -72,6 +72,10 @@ SHAPES = {
 }
 
 
+# shapes the fused FFMA kernels cover (every BASELINE shape; the tiny, d2 and
+# ragged test shapes run the generic path)
+FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep128", "billion"}
+
 # shapes with tcgen05 kernels (rank >= 32, 128-column blocks)
 TC_SHAPES = ("products", "papers", "billion")
 
@@ -107,6 +111,8 @@ def test_forward_parity(name, path):
     emb.sync()
     if path == "tc" and name in TC_SHAPES:
         assert emb.last_path() == "fused-tc"  # the tcgen05 kernels ran, not the FFMA ones
+    if path == "auto" and name in FUSED_SHAPES:
+        assert emb.last_path() == "fused"  # a BASELINE shape never falls back to the generic path
     ref, bad = oracle.lookup_batch(cfg, cores, idx, 0)
     aref, _ = oracle.lookup_batch(cfg, abs_cores(cores), idx, 0)
     assert bad == -1
