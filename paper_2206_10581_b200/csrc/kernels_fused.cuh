@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 template <int K, int BN, int RP, int NL>
 __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fused_bwd(FusedArgs a) {
   TT_PDL_ENTRY();
-  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, BNJ = BN / K, NPT = BM / RP;
+  constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, NPT = BM / RP;
   constexpr int WE = K * NL;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
   using CM = ColMap<BN>;
@@ -398,8 +398,10 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
           const float* Yp = a.dY + (int64_t)u * npad;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            const int colb = CM::col(lane, q);
-            const int r0 = colb % K, jf = colb / K;
+            // global column of P_F: core-F column block jf, rank index r0
+            // (BN may be smaller than K: a block then covers part of one jf)
+            const int colg = cb * BN + CM::col(lane, q);
+            const int r0 = colg % K, jf = colg / K;
             float gv[W4][NL];
 #pragma unroll
             for (int t = 0; t < W4; ++t)
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
 #pragma unroll
             for (int ii = 0; ii < NR; ++ii) {
               float yv[NL];
-              const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + cb * BNJ + jf) * NL;
+              const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + jf) * NL;
 #pragma unroll
               for (int l4 = 0; l4 < NL; l4 += 4) {
                 const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
@@ -853,8 +855,8 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
 // FUSED_SWITCH): papers, products / sweep32, small, billion, sweep16,
 // sweep64, sweep128, sweep8.
 #define TT_FUSED_SHAPES(X) \
-  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 128, 4, 8) \
-  X(8, 32, 4, 8)
+  X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 64, 4, 8) \
+  X(128, 128, 4, 8) X(8, 32, 4, 8)
 #define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
@@ -876,7 +878,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   if (K == 16 && NC % 64 == 0) BN = 64;
   if (K == 32 && NC % 128 == 0) BN = 128;
   if (K == 64 && NC % 128 == 0) BN = 128;
-  if (K == 128 && NC % 128 == 0) BN = 128;
+  if (K == 128 && NC % 64 == 0) BN = 64;  // 64-column blocks: two CTAs per SM at rank 128
   if (!BN || !fused_shape_compiled((int)K, BN, (int)RP, (int)NL)) return false;
   if (c.emb_dim % 4 || c.npad % 4 || c.npad > 512) return false;
   for (int k = 0; k < c.d; ++k)
@@ -892,7 +894,9 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->nF = (int)c.n[F];
   s->BNj = (int)(BN / K);
   s->OUT = (int)(RP * (BN / K) * NL);
-  const int BNf = (int)std::min<int64_t>(BN, 128);  // 2 CTAs/SM without spills
+  // forward column block: up to 128 (2 CTAs/SM without spills); at rank 128
+  // the forward keeps 128-column blocks while the backward uses 64
+  const int BNf = (K == 128 && NC % 128 == 0) ? 128 : (int)std::min<int64_t>(BN, 128);
   s->BNf = BNf;
   s->ncbf = (int)(NC / BNf);
   s->BNjf = (int)(BNf / K);
