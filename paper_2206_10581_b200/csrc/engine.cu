@@ -790,8 +790,14 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   }
   TT_FUSED_SHAPES(TT_W_CASE)
 #undef TT_W_CASE
-  LAUNCH(k_fused_reduce_last, (int)c.m[d - 1], 256, 0, s, c, 1, WE,
-         h->goff[d - 1], h->order[d - 1], h->F.W, h->grads, h->st);
+  // wide W rows (one float4 column per thread already fills 256 threads): 1024
+  // threads, so several sub-groups split each digit group's rows
+  if (WE / 4 >= 256)
+    LAUNCH(k_fused_reduce_last<1024>, (int)c.m[d - 1], 1024, 0, s, c, 1, WE, h->goff[d - 1], h->order[d - 1], h->F.W,
+           h->grads, h->st);
+  else
+    LAUNCH(k_fused_reduce_last<256>, (int)c.m[d - 1], 256, 0, s, c, 1, WE, h->goff[d - 1], h->order[d - 1], h->F.W,
+           h->grads, h->st);
   const int per = f.RP * f.K;
   float* dst = f.F == 1 ? h->grads : h->L.dP[f.F - 1];
   // 128-thread blocks: twice the blocks of a parent-per-block grid, a smaller

@@ -762,21 +762,22 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
 // 256 threads = S sub-groups x (WE/4) float4 columns; sub-group sg sums the
 // (member, column block) pairs q = sg, sg+S, ... in order, and the S partials
 // are combined in sub-group order (a fixed tree: deterministic).
-__global__ void __launch_bounds__(256) k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __restrict__ goffL,
+template <int T>
+__global__ void __launch_bounds__(T) k_fused_reduce_last(DevCfg c, int ncb, int WE, const int* __restrict__ goffL,
                                                            const int* __restrict__ orderL, const float* __restrict__ W,
                                                            float* __restrict__ grads, const DevStatus* st) {
   TT_PDL_ENTRY();
-  __shared__ float4 red[256];
+  __shared__ float4 red[T];
   if (tt_failed(st)) return;
   const int v = blockIdx.x;
   const int g0 = goffL[v], g1 = goffL[v + 1];
   if (g0 == g1) return;
   const int cols = WE / 4;
-  const int S = cols >= 256 ? 1 : 256 / cols;
+  const int S = cols >= T ? 1 : T / cols;
   float* dst = grads + c.core_off[c.d - 1] + (int64_t)v * c.slice[c.d - 1];
   const int npair = (g1 - g0) * ncb;
-  for (int col0 = 0; col0 < cols; col0 += 256) {
-    const int sg = threadIdx.x / min(cols, 256), col = col0 + threadIdx.x % min(cols, 256);
+  for (int col0 = 0; col0 < cols; col0 += T) {
+    const int sg = threadIdx.x / min(cols, T), col = col0 + threadIdx.x % min(cols, T);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sg < S && col < cols) {
       int q = sg;
@@ -800,10 +801,10 @@ __global__ void __launch_bounds__(256) k_fused_reduce_last(DevCfg c, int ncb, in
     }
     red[threadIdx.x] = acc;
     __syncthreads();
-    if (threadIdx.x < min(cols, 256) && col0 + threadIdx.x < cols) {
+    if (threadIdx.x < min(cols, T) && col0 + threadIdx.x < cols) {
       float4 t = red[threadIdx.x];
       for (int s2 = 1; s2 < S; ++s2) {
-        const float4 y = red[s2 * min(cols, 256) + threadIdx.x];
+        const float4 y = red[s2 * min(cols, T) + threadIdx.x];
         t.x += y.x; t.y += y.y; t.z += y.z; t.w += y.w;
       }
       *reinterpret_cast<float4*>(dst + (col0 + threadIdx.x) * 4) = t;
