@@ -627,26 +627,38 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
       stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
     }
     const float* Gp = Gs;
-    for (int q = lane; q < nrow; q += 32) {
-      const float* crow = buf + q * (K + 4);
+    // KS lanes per output row, each over K / KS ranks (K >= 128: the two
+    // half-warps split the rank sum and combine it with one shuffle)
+    constexpr int KS = K >= 128 ? 2 : 1;
+    constexpr int KR = K / KS;
+    const int kpart = KS == 2 ? (lane >> 4) : 0, qlane = KS == 2 ? (lane & 15) : lane;
+    for (int q0 = 0; q0 < nrow; q0 += 32 / KS) {
+      const int q = q0 + qlane;
+      const float* crow = buf + (q < nrow ? q : 0) * (K + 4) + kpart * KR;
+      const float* Gk = Gp + kpart * KR * NL;
       float o[NL];
 #pragma unroll
       for (int jl = 0; jl < NL; ++jl) o[jl] = 0.f;
 #pragma unroll
-      for (int r = 0; r < K; r += 4) {
+      for (int r = 0; r < KR; r += 4) {
         const float4 c = *reinterpret_cast<const float4*>(crow + r);
         const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
           for (int l4 = 0; l4 < NL; l4 += 4) {
-            const float4 gv = *reinterpret_cast<const float4*>(Gp + (r + t) * NL + l4);
+            const float4 gv = *reinterpret_cast<const float4*>(Gk + (r + t) * NL + l4);
             o[l4] = fmaf(cv[t], gv.x, o[l4]);
             o[l4 + 1] = fmaf(cv[t], gv.y, o[l4 + 1]);
             o[l4 + 2] = fmaf(cv[t], gv.z, o[l4 + 2]);
             o[l4 + 3] = fmaf(cv[t], gv.w, o[l4 + 3]);
           }
       }
+      if constexpr (KS == 2) {
+#pragma unroll
+        for (int jl = 0; jl < NL; ++jl) o[jl] += __shfl_xor_sync(0xffffffffu, o[jl], 16);
+      }
+      if (q >= nrow || kpart != 0) continue;
       const int64_t col = (int64_t)q * NL;
       if (s1 - s0 > HEAVY_POS) {
 #pragma unroll
