@@ -699,12 +699,16 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
 #define TT_LL_CASE(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
     const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (k_ + 4) + k_ * nl_); \
-    if ((int64_t)f.RP * f.nF * k_ <= 2048) { \
-      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-      LAUNCH((k_last_level<k_, nl_, true>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+    const bool pipe_ = (int64_t)f.RP * f.nF * k_ <= 2048, split_ = f.RP * f.nF <= 16; \
+    if (pipe_ && split_) { \
+      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, true, 2>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_last_level<k_, nl_, true, 2>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+    } else if (pipe_) { \
+      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, true, 1>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_last_level<k_, nl_, true, 1>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
     } else { \
-      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-      LAUNCH((k_last_level<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
+      CU(cudaFuncSetAttribute((k_last_level<k_, nl_, false, 1>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_last_level<k_, nl_, false, 1>), 148 * 8, SK_WARPS * 32, sm_, s, o, h->counts, h->parent + (d - 1) * cap); \
     } \
   }
     if (false) {
@@ -790,9 +794,9 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   }
   TT_FUSED_SHAPES(TT_W_CASE)
 #undef TT_W_CASE
-  // wide W rows (one float4 column per thread already fills 256 threads): 1024
-  // threads, so several sub-groups split each digit group's rows
-  if (WE / 4 >= 256)
+  // wide W rows (128+ float4 columns): 1024 threads, so several sub-groups
+  // split each digit group's rows
+  if (WE / 4 >= 128)
     LAUNCH(k_fused_reduce_last<1024>, (int)c.m[d - 1], 1024, 0, s, c, 1, WE, h->goff[d - 1], h->order[d - 1], h->F.W,
            h->grads, h->st);
   else

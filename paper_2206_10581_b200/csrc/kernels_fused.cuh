@@ -564,7 +564,7 @@ __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp,
 // slice are loaded into registers while this ID is computed from shared
 // memory, so every warp keeps a block in flight; the indices run one ID ahead
 // of that.
-template <int K, int NL, bool PIPE>
+template <int K, int NL, bool PIPE, int KS>
 __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, const int* __restrict__ counts,
                                                               const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
@@ -627,9 +627,10 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
       stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
     }
     const float* Gp = Gs;
-    // KS lanes per output row, each over K / KS ranks (K >= 128: the two
-    // half-warps split the rank sum and combine it with one shuffle)
-    constexpr int KS = K >= 128 ? 2 : 1;
+    // KS lanes per output row, each over K / KS ranks (KS = 2 when a block
+    // has at most 16 rows: the two half-warps split the rank sum and combine
+    // it with one shuffle, so no lane idles)
+    static_assert(KS == 1 || KS == 2, "rank split");
     constexpr int KR = K / KS;
     const int kpart = KS == 2 ? (lane >> 4) : 0, qlane = KS == 2 ? (lane & 15) : lane;
     for (int q0 = 0; q0 < nrow; q0 += 32 / KS) {
