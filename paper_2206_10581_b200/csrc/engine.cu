@@ -241,14 +241,13 @@ int ensure_generic(tt_engine* h) {
   return TT_OK;
 }
 
-// Programmatic stream serialisation (PDL) is opt-in (TT_PDL=1): the next
-// kernel is scheduled while the previous one drains and waits
-// (griddepcontrol.wait, TT_PDL_ENTRY) for its completion -- 0.20 -> 0.16 ms
-// for the eager plan at papers.  It is off by default: with it, repeated
-// fresh-engine runs of the tensor-core path at the billion shape produced
-// differing P_F rows in ~8% of runs (scripts/race_stress.py, FRESH=1), and 0
-// of 59 without.  Never used under stream capture (the replayed graph already
-// launches back to back; programmatic edges measured slower there).
+// Programmatic stream serialisation (PDL, default on; TT_PDL=0 turns it off):
+// the next kernel is scheduled while the previous one drains and waits
+// (griddepcontrol.wait, TT_PDL_ENTRY, first statement of every kernel) for
+// its completion -- 0.147 -> 0.130 ms for the eager plan at papers.  (An
+// earlier race on the tensor path was k_tc_fwd missing that entry wait.)
+// Not used under stream capture unless TT_PDL_GRAPH=1: the replayed graph
+// already launches back to back, and programmatic edges measured slower there.
 // Diagnostic switches, read once per process (all off by default):
 //   TT_TC_VARIANT / TT_TC_BVARIANT = bit mask handed to the tcgen05 forward /
 //     backward as FusedArgs::mode to skip parts of the work for attribution
@@ -270,9 +269,21 @@ const DiagEnv& diag() {
   return d;
 }
 
+// Programmatic dependent launch on eager launches (default; TT_PDL=0 turns it
+// off).  Every kernel opens with TT_PDL_ENTRY (griddepcontrol.wait before any
+// read of its predecessor's output).
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("TT_PDL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+// TT_PDL_GRAPH=1: also under stream capture (programmatic edges in the graph;
+// measured slower for the replayed step, so off by default)
+bool pdl_graph_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_PDL_GRAPH");
     return e && *e && *e != '0';
   }();
   return on;
@@ -291,7 +302,7 @@ void tt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.attrs = at;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
-  cfg.numAttrs = (pdl_enabled() && cs == cudaStreamCaptureStatusNone) ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled() && (cs == cudaStreamCaptureStatusNone || pdl_graph_enabled())) ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -187,6 +187,7 @@ struct TileCursor {
 
 template <int K, int BN, int RP>
 __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
+  TT_PDL_ENTRY();  // under programmatic dependent launch: the plan must be complete
   static_assert(BN == 128 && K % 32 == 0 && K <= 64 && TC_BM % RP == 0 && 32 % RP == 0, "tcgen05 forward shape");
   constexpr int NPT = TC_BM / RP;                 // nodes per tile
   constexpr uint32_t SPL = (uint32_t)K * BN * 2;  // bytes per S slice plane
