@@ -253,8 +253,10 @@ int ensure_generic(tt_engine* h) {
 //     backward as FusedArgs::mode to skip parts of the work for attribution
 //     (2 MMAs, 4 epilogue stores, 8 A staging, 16 dC formation, 32 dC planes,
 //     64 one ID per node); results are wrong while set (scripts/tc_variants.sh);
-//   TT_TC_TRACE = per-CTA phase timestamps of the backward GEMM kernels
-//     (tt_debug_trace, scripts/tc_trace.py).
+//   TT_TC_TRACE = 1: per-CTA phase timestamps of the backward GEMM kernels,
+//     2: per-tile role stamps of the tcgen05 forward (tt_debug_trace,
+//     scripts/tc_trace.py).
+// The forward's variant bits are 2 MMAs, 4 P_F stores, 8 A loads.
 struct DiagEnv {
   int tc_fwd_variant = 0, tc_bwd_variant = 0;
   int trace = 0;  // 1: backward, 2: forward
