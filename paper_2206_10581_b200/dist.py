@@ -238,6 +238,14 @@ class OwnerShardedTT:
         emb.set_dense_grads(True)
         self._route = None
         self._recv_idx = None
+        # the replicated segments travel as one packed all-reduce (one NCCL call
+        # per step instead of one per segment)
+        if len(self.segments) > 1:
+            pos = np.concatenate([np.arange(o, o + n, dtype=np.int64) for o, n in self.segments])
+            self._pack_idx = torch.from_numpy(pos).to(self.buf.device)
+            self._pack = torch.empty(len(pos), dtype=torch.float32, device=self.buf.device)
+        else:
+            self._pack_idx = None
 
     def forward(self, indices, out=None):
         import torch
@@ -258,8 +266,14 @@ class OwnerShardedTT:
             self.emb.backward(up, self._recv_idx)
 
     def allreduce(self):
-        for o, n in self.segments:
-            self.dist.all_reduce(self.buf[o: o + n], group=self.group)
+        if self._pack_idx is None:
+            for o, n in self.segments:
+                self.dist.all_reduce(self.buf[o: o + n], group=self.group)
+            return
+        import torch
+        torch.index_select(self.buf, 0, self._pack_idx, out=self._pack)
+        self.dist.all_reduce(self._pack, group=self.group)
+        self.buf.index_copy_(0, self._pack_idx, self._pack)
 
     def step(self):
         self.allreduce()
