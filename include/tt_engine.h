@@ -83,6 +83,10 @@ int tt_get_cores_f32(tt_engine* h, float* const* cores);
  * (0.9, 0.999, 1e-8; Adagrad eps 1e-10). */
 int tt_opt_init(tt_engine* h, int kind, double lr, double beta1, double beta2, double eps);
 int tt_opt_get_step(tt_engine* h, int64_t* step); /* synchronises */
+/* Hyper-parameters only (apply_update reads opt.learning_rate etc. on every
+ * call, autodiff.cpp:147-173): moments and step are kept, so a learning-rate
+ * schedule does not reset the optimizer.  Takes effect for the next tt_step. */
+int tt_opt_set_hparams(tt_engine* h, double lr, double beta1, double beta2, double eps);
 
 /* ---- hot path: device buffers, stream-ordered, asynchronous ---------------
  * tt_forward  ~ lookup_batch (tt_embedding.cpp:110-125): d_out is
@@ -188,9 +192,10 @@ int64_t tt_launch_count(tt_engine* h);
 int64_t tt_debug_trace(long long* out, int64_t n);
 /* Selects the kernel family: 0 = auto (fused FFMA fast path where the shapes
  * allow), 1 = generic path only, 2 = fused with the optional tensor-core
- * 3xTF32 contraction where compiled for the shape (reported separately). */
+ * (tcgen05, BF16x3 split, FP32 accumulation) contraction where compiled for
+ * the shape (reported separately). */
 int tt_set_path(tt_engine* h, int path);
-/* Which path the last forward used (0 generic, 1 fused FFMA, 2 fused 3xTF32). */
+/* Which path the last forward used (0 generic, 1 fused FFMA, 2 fused tcgen05). */
 int tt_last_path(tt_engine* h);
 /* Batch position (TT_ERR_INDEX) or core (TT_ERR_NONFINITE) of the last error. */
 int64_t tt_last_error_position(void);

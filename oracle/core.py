@@ -39,6 +39,8 @@ def lib():
         _lib = _load(path)
         _lib.or_lookup_batch.restype = C.c_int64
         _lib.or_backward_lookup.restype = C.c_int64
+        _lib.or_lookup_batch_f32.restype = C.c_int64
+        _lib.or_backward_lookup_f32.restype = C.c_int64
         _lib.or_count_params.restype = C.c_int64
         _lib.or_padded_rows.restype = C.c_int64
         _lib.or_ttm_entry.restype = C.c_double
@@ -147,6 +149,56 @@ def apply_update(cfg, cores, grads, opt: OptState) -> int:
     rc = lib().or_apply_update(C.byref(to_c(cfg)), _ptrs(flat), _ptrs(g), C.c_int(opt.kind),
                                C.c_double(opt.lr), C.c_double(opt.beta1), C.c_double(opt.beta2),
                                C.c_double(opt.eps), C.byref(step), _ptrs(opt.s1), _ptrs(opt.s2))
+    opt.step = step.value
+    return rc
+
+
+# ---- fp32 variant (the multithreaded fp32 CPU
+# baseline; same loops as the fp64 restatement, float elements) ------------
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptrs32(arrs):
+    return (C.POINTER(C.c_float) * len(arrs))(*[a.ctypes.data_as(C.POINTER(C.c_float)) for a in arrs])
+
+
+def lookup_batch_f32(cfg, cores, idx, nthreads: int = 1):
+    idx = _i64(idx)
+    cores = [_f32(c).ravel() for c in cores]
+    out = np.zeros((len(idx), cfg.emb_dim), np.float32)
+    bad = lib().or_lookup_batch_f32(C.byref(to_c(cfg)), _ptrs32(cores), idx.ctypes.data_as(C.c_void_p),
+                                    C.c_int64(len(idx)), out.ctypes.data_as(C.c_void_p), C.c_int(nthreads))
+    return out, int(bad)
+
+
+def backward_lookup_f32(cfg, cores, idx, upstream, nthreads: int = 1):
+    idx = _i64(idx)
+    cores = [_f32(c).ravel() for c in cores]
+    up = _f32(upstream).reshape(len(idx), cfg.emb_dim)
+    grads = [np.zeros(cfg.core_size(k), np.float32) for k in range(cfg.d)]
+    bad = lib().or_backward_lookup_f32(C.byref(to_c(cfg)), _ptrs32(cores), idx.ctypes.data_as(C.c_void_p),
+                                       C.c_int64(len(idx)), up.ctypes.data_as(C.c_void_p), _ptrs32(grads),
+                                       C.c_int(nthreads))
+    return [g.reshape(cfg.core_shape(k)) for k, g in enumerate(grads)], int(bad)
+
+
+class OptState32(OptState):
+    def __init__(self, cfg, kind: int, lr: float, beta1=0.9, beta2=0.999, eps=None):
+        super().__init__(cfg, kind, lr, beta1, beta2, eps)
+        self.s1 = [np.zeros(cfg.core_size(k), np.float32) for k in range(cfg.d)]
+        self.s2 = [np.zeros(cfg.core_size(k), np.float32) for k in range(cfg.d)]
+
+
+def apply_update_f32(cfg, cores, grads, opt: OptState32) -> int:
+    flat = [c.reshape(-1) for c in cores]
+    for c in flat:
+        assert c.dtype == np.float32 and c.flags.c_contiguous
+    g = [_f32(x).ravel() for x in grads]
+    step = C.c_int64(opt.step)
+    rc = lib().or_apply_update_f32(C.byref(to_c(cfg)), _ptrs32(flat), _ptrs32(g), C.c_int(opt.kind),
+                                   C.c_double(opt.lr), C.c_double(opt.beta1), C.c_double(opt.beta2),
+                                   C.c_double(opt.eps), C.byref(step), _ptrs32(opt.s1), _ptrs32(opt.s2))
     opt.step = step.value
     return rc
 

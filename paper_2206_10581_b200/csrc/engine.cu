@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -314,12 +315,16 @@ void tt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
     ++h->launches;                                                              \
   } while (0)
 
+// The dynamic shared-memory opt-in is a per-device attribute of the function:
+// one bit per device that has it (an engine on a second GPU of the process
+// must set it again).
 template <class K>
-void rs_set_attrs() {
-  static bool done = false;
-  if (!done) {
+void rs_set_attrs(int device) {
+  static std::atomic<unsigned long long> done{0};  // bit per device (devices 0..63)
+  const unsigned long long bit = 1ull << (device & 63);
+  if (device >= 64 || !(done.load() & bit)) {
     cudaFuncSetAttribute(k_rs_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SCATTER_SMEM);
-    done = true;
+    done.fetch_or(bit);
   }
 }
 
@@ -333,7 +338,7 @@ K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, cons
   const int passes = (nbits + RS_MAXBITS - 1) / RS_MAXBITS;
   K* kin = ka; K* kout = kb;
   int* vin = va; int* vo = vb;
-  rs_set_attrs<K>();
+  rs_set_attrs<K>(h->device);
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (nbits - shift + (passes - p) - 1) / (passes - p);  // split evenly
@@ -365,7 +370,7 @@ void sort_levels(tt_engine* h, cudaStream_t s) {
   const int ntiles = (int)((cap + RS_TILE - 1) / RS_TILE);
   int nbits = 1;
   for (int k = 1; k < d; ++k) nbits = std::max<int>(nbits, (int)bitlen((uint64_t)(c.m[k] - 1)));
-  rs_set_attrs<unsigned>();
+  rs_set_attrs<unsigned>(h->device);
   RSBatch<unsigned> rb{};
   for (int k = 1; k < d; ++k) {
     const int y = k - 1;
@@ -1351,6 +1356,15 @@ int tt_opt_init(tt_engine* h, int kind, double lr, double beta1, double beta2, d
   return TT_OK;
 }
 
+int tt_opt_set_hparams(tt_engine* h, double lr, double beta1, double beta2, double eps) {
+  if (!h) return fail(TT_ERR_ARG, "tt_opt_set_hparams: null handle");
+  h->lr = lr;
+  h->beta1 = beta1 > 0 ? beta1 : 0.9;
+  h->beta2 = beta2 > 0 ? beta2 : 0.999;
+  h->eps = eps > 0 ? eps : (h->opt_kind == TT_OPT_ADAGRAD ? 1e-10 : 1e-8);
+  return TT_OK;
+}
+
 int tt_opt_get_step(tt_engine* h, int64_t* step) {
   if (!h || !step) return fail(TT_ERR_ARG, "tt_opt_get_step: null argument");
   CU(cudaSetDevice(h->device));
@@ -1495,19 +1509,35 @@ int tt_train_step_host(tt_engine* h, const int64_t* h_idx, int64_t B, const floa
   CU(cudaStreamWaitEvent(h->s_h2d, h->ev_in, 0));
   CU(cudaMemcpyAsync(h->st_up, h_up, rows, cudaMemcpyHostToDevice, h->s_h2d));  // under plan + forward
   CU(cudaEventRecord(h->ev_up, h->s_h2d));
+  // on any error below, the copies already queued (the upstream upload, the
+  // row download) may still be reading / writing the caller's host buffers:
+  // drain all three streams before returning
+  auto drained = [&](int code) {
+    cudaStreamSynchronize(h->s_h2d);
+    cudaStreamSynchronize(h->s_d2h);
+    cudaStreamSynchronize(s);
+    return code;
+  };
+#define CU_D(call)                                                                        \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return drained(fail(TT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
   rc = tt_forward(h, h->st_idx, B, h->st_out, s);
-  if (rc) return rc;
+  if (rc) return drained(rc);
   if (h_out) {  // rows go back under the backward + update
-    CU(cudaEventRecord(h->ev_fwd, s));
-    CU(cudaStreamWaitEvent(h->s_d2h, h->ev_fwd, 0));
-    CU(cudaMemcpyAsync(h_out, h->st_out, rows, cudaMemcpyDeviceToHost, h->s_d2h));
+    CU_D(cudaEventRecord(h->ev_fwd, s));
+    CU_D(cudaStreamWaitEvent(h->s_d2h, h->ev_fwd, 0));
+    CU_D(cudaMemcpyAsync(h_out, h->st_out, rows, cudaMemcpyDeviceToHost, h->s_d2h));
   }
-  CU(cudaStreamWaitEvent(s, h->ev_up, 0));
+  CU_D(cudaStreamWaitEvent(s, h->ev_up, 0));
   rc = tt_backward(h, nullptr, B, h->st_up, s);
-  if (rc) return rc;
+  if (rc) return drained(rc);
   rc = tt_step(h, s);
-  if (rc) return rc;
+  if (rc) return drained(rc);
+#undef CU_D
   CU(cudaStreamSynchronize(h->s_d2h));
+  CU(cudaStreamSynchronize(h->s_h2d));
   return read_status(h, s);
 }
 

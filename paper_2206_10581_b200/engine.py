@@ -57,7 +57,7 @@ SYMBOLS = [
     "tt_train_step_host", "tt_get_core_grads_f64", "tt_set_core_grads_f64", "tt_grad_buffer", "tt_set_dense_grads", "tt_bind_grad_buffer",
     "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
-    "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_debug_trace", "tt_set_permutation",
+    "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_opt_set_hparams", "tt_debug_trace", "tt_set_permutation",
     "tt_ortho_cores_f64",
 ]
 
@@ -80,6 +80,7 @@ def load_library(build_if_missing: bool = True):
         "tt_set_cores_f64": (i32, [vp, vp]), "tt_set_cores_f32": (i32, [vp, vp]),
         "tt_get_cores_f64": (i32, [vp, vp]), "tt_get_cores_f32": (i32, [vp, vp]),
         "tt_opt_init": (i32, [vp, i32, dbl, dbl, dbl, dbl]), "tt_opt_get_step": (i32, [vp, vp]),
+        "tt_opt_set_hparams": (i32, [vp, dbl, dbl, dbl, dbl]),
         "tt_forward": (i32, [vp, vp, i64, vp, vp]), "tt_backward": (i32, [vp, vp, i64, vp, vp]),
         "tt_step": (i32, [vp, vp]), "tt_sync": (i32, [vp, vp]),
         "tt_lookup_batch": (i32, [vp, vp, i64, vp]), "tt_backward_lookup": (i32, [vp, vp, i64, vp]),
@@ -255,6 +256,10 @@ class TTEmbedding:
         return arrs
 
     # ---- device-tensor path (torch CUDA tensors, current stream) -----------
+    def _check_device(self, t, what: str) -> None:
+        if not t.is_cuda or t.device.index != self.device:
+            raise InvalidArgument(f"{what} must be on cuda:{self.device}, got {t.device}")
+
     def _stream(self):
         torch = _torch()
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -263,9 +268,17 @@ class TTEmbedding:
         torch = _torch()
         if indices.dtype != torch.int64 or not indices.is_cuda or not indices.is_contiguous():
             raise InvalidArgument("forward: indices must be a contiguous int64 CUDA tensor")
+        self._check_device(indices, "forward: indices")
         B = indices.numel()
         if out is None:
             out = torch.empty((B, self.config.emb_dim), dtype=torch.float32, device=indices.device)
+        else:
+            if out.dtype != torch.float32 or not out.is_contiguous():
+                raise InvalidArgument("forward: out must be a contiguous float32 CUDA tensor")
+            if tuple(out.shape) != (B, self.config.emb_dim):
+                raise InvalidArgument(f"forward: out must have shape ({B}, {self.config.emb_dim}), "
+                                      f"got {tuple(out.shape)}")
+            self._check_device(out, "forward: out")
         _raise(self._lib.tt_forward(self._h, C.c_void_p(indices.data_ptr()), B, C.c_void_p(out.data_ptr()),
                                     self._stream()), "tt_forward")
         return out
@@ -275,6 +288,11 @@ class TTEmbedding:
         torch = _torch()
         if grad_out.dtype != torch.float32 or not grad_out.is_cuda or not grad_out.is_contiguous():
             raise InvalidArgument("backward: grad_out must be a contiguous float32 CUDA tensor")
+        self._check_device(grad_out, "backward: grad_out")
+        if indices is not None:
+            if indices.dtype != torch.int64 or not indices.is_cuda or not indices.is_contiguous():
+                raise InvalidArgument("backward: indices must be a contiguous int64 CUDA tensor")
+            self._check_device(indices, "backward: indices")
         B = grad_out.shape[0]
         if grad_out.dim() != 2 or grad_out.shape[1] != self.config.emb_dim:
             raise InvalidArgument("backward_lookup: upstream cols != emb_dim")
@@ -298,12 +316,28 @@ class TTEmbedding:
         _raise(self._lib.tt_sync(self._h, self._stream()), "tt_sync")
 
     def configure_optimizer(self, opt: OptimizerState) -> None:
-        sig = (opt.kind, opt.learning_rate, opt.beta1, opt.beta2, opt.epsilon)
-        if self._opt is not opt or self._opt_sig != sig:
+        """Binds `opt` to the engine's device-resident optimizer state.
+
+        In the reference the moments live in the OptimizerState object
+        (autodiff.hpp:43-56) and apply_update reads lr/betas/eps from it on
+        every call (autodiff.cpp:147-173).  Here the moments live on the device:
+        they are (re)initialised -- zero moments, step 0, as
+        OptimizerState::make produces them -- only when the optimizer kind
+        changes or a fresh state object (step 0) replaces the bound one.
+        Otherwise the hyper-parameters are pushed as they are now (a learning
+        rate schedule never resets the moments), and the device step follows
+        opt.step (a state object carried across rebuilds keeps counting)."""
+        fresh = self._opt is None or self._opt_sig != opt.kind or (self._opt is not opt and opt.step == 0)
+        if fresh:
             _raise(self._lib.tt_opt_init(self._h, opt.kind, opt.learning_rate, opt.beta1, opt.beta2, opt.epsilon),
                    "tt_opt_init")
-            self._opt, self._opt_sig = opt, sig
             opt.step = 0
+        else:
+            _raise(self._lib.tt_opt_set_hparams(self._h, opt.learning_rate, opt.beta1, opt.beta2, opt.epsilon),
+                   "tt_opt_set_hparams")
+            if self._opt is not opt and opt.step != self.opt_step():
+                _raise(self._lib.tt_opt_state_set_f64(self._h, None, None, int(opt.step)), "tt_opt_state_set")
+        self._opt, self._opt_sig = opt, opt.kind
 
     def train_step_host(self, indices: np.ndarray, upstream: np.ndarray, out: Optional[np.ndarray] = None):
         idx = np.ascontiguousarray(indices, dtype=np.int64)

@@ -66,6 +66,9 @@ SHAPES = {
     "products": (lambda: C.WORKLOADS["products"]["cfg"](), 2048, "zipf"),
     "papers": (lambda: C.WORKLOADS["papers"]["cfg"](), 1024, "zipf"),
     "sweep8": (lambda: C.WORKLOADS["sweep8"]["cfg"](), 2048, "locality"),
+    "sweep16": (lambda: C.WORKLOADS["sweep16"]["cfg"](), 2048, "locality"),
+    "sweep32": (lambda: C.WORKLOADS["sweep32"]["cfg"](), 2048, "locality"),
+    "sweep64": (lambda: C.WORKLOADS["sweep64"]["cfg"](), 1024, "locality"),
     "sweep128": (lambda: C.WORKLOADS["sweep128"]["cfg"](), 512, "locality"),
     "billion": (lambda: C.WORKLOADS["billion"]["cfg"](), 512, "zipf"),
     "ragged": (lambda: C.plan_factorization(1000, 30, [7, 11, 13], [2, 3, 5], [1, 5, 3, 1]), 700, "zipf"),
@@ -73,11 +76,13 @@ SHAPES = {
 
 
 # shapes the fused FFMA kernels cover (every BASELINE shape; the tiny, d2 and
-# ragged test shapes run the generic path)
-FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep128", "billion"}
+# ragged test shapes run the generic path).  tests/test_instantiations.py
+# checks that every compiled (K, BN, RP, NL) instantiation is reached by one
+# of these.
+FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep16", "sweep32", "sweep64", "sweep128", "billion"}
 
-# shapes with tcgen05 kernels (rank >= 32, 128-column blocks)
-TC_SHAPES = ("products", "papers", "billion")
+# shapes with tcgen05 kernels (rank >= 32)
+TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64")
 
 
 @pytest.mark.parametrize("name", list(SHAPES))
@@ -317,3 +322,45 @@ def test_200_sgd_steps_fit():  # test_autodiff.cpp:237-256 on the device
         e.apply_update(emb, e.backward_lookup(emb, allidx, (out - target).astype(np.float32)), opt)
     assert loss() <= initial / 100.0
     assert opt.step == 200
+
+
+def test_lr_schedule_keeps_optimizer_state():
+    """apply_update reads opt.learning_rate on every call (autodiff.cpp:147-173):
+    changing it on the same state object must not reset the Adagrad/Adam
+    moments or the step."""
+    e = eng()
+    cfg = SHAPES["products"][0]()
+    for kind, kid in (("adagrad", oracle.ADAGRAD), ("adam", oracle.ADAM)):
+        emb, cores = make(cfg, 23)
+        opt = e.OptimizerState.make(cfg, getattr(e.OptKind, kind), 0.01)
+        ost = oracle.OptState(cfg, kid, 0.01)
+        p64 = [c.astype(np.float64).copy() for c in cores]
+        for it, lr in enumerate((0.01, 0.005, 0.0025)):
+            idx = ids_for(cfg, 30 + it, 512, "zipf")
+            up = synth.normal(40 + it, 1, 512 * cfg.emb_dim).reshape(512, cfg.emb_dim)
+            gref, _ = oracle.backward_lookup(cfg, cores, idx, up, 0)
+            g32 = [g.astype(np.float32).astype(np.float64) for g in gref]
+            opt.learning_rate = lr
+            ost.lr = lr
+            e.apply_update(emb, e.CoreGradients(g32, 512), opt)
+            assert oracle.apply_update(cfg, p64, g32, ost) == -1
+        assert opt.step == ost.step == 3
+        got = emb.get_cores(np.float64)
+        for k in range(cfg.d):
+            err = np.abs(got[k] - p64[k]) / (np.abs(p64[k]) + 0.03)
+            assert float(err.max()) <= 1e-5, f"{kind} core {k}: {err.max():.3g}"
+
+
+def test_forward_rejects_bad_out_buffer():
+    import torch
+    cfg = SHAPES["tiny"][0]()
+    emb, _ = make(cfg, 24)
+    idx = torch.tensor([0, 1, 2], device="cuda")
+    for bad in (torch.empty((3, 8), dtype=torch.float64, device="cuda"),
+                torch.empty((2, 8), device="cuda"),
+                torch.empty((8, 3), device="cuda").t(),
+                torch.empty((3, 8))):
+        with pytest.raises(C.InvalidArgument):
+            emb.forward(idx, bad)
+    with pytest.raises(C.InvalidArgument):
+        emb.forward(idx.cpu())
