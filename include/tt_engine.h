@@ -168,6 +168,28 @@ int tt_set_dense_grads(tt_engine* h, int on);
  * engine's own buffer. */
 int tt_bind_grad_buffer(tt_engine* h, float* d_ptr, int64_t count);
 
+/* NCCL data parallelism, position sharding: the batch is
+ * sharded by position, cores are replicated, and the one exchange step is a
+ * sum all-reduce of the gradient buffer between tt_backward and tt_step.
+ *   tt_nccl_unique_id     ncclGetUniqueId into `out` (>= 128 bytes), on one
+ *                         rank; the caller ships it to the others;
+ *   tt_comm_init_rank     creates the handle's own ncclComm_t (ncclCommInitRank);
+ *   tt_comm_init          attaches a caller-owned ncclComm_t (NULL detaches);
+ *   tt_allreduce_grads    enqueues the all-reduce on the handle's comm stream,
+ *                         ordered after the backward on `stream` and before
+ *                         anything later on `stream`.  The level-F core's
+ *                         gradient (the fused GEMM's output, 63 of 64 MB at
+ *                         papers) is all-reduced as soon as that kernel ends,
+ *                         overlapping the backward's remaining kernels; the
+ *                         other cores and the touch counters follow.
+ * Attaching a communicator turns dense gradients on.  NCCL is resolved at run
+ * time (dlopen of libnccl.so.2, reusing a copy the process already loaded);
+ * without it these return TT_ERR_CUDA. */
+int tt_nccl_unique_id(void* out, int64_t nbytes);
+int tt_comm_init_rank(tt_engine* h, const void* unique_id, int rank, int nranks);
+int tt_comm_init(tt_engine* h, void* nccl_comm, int rank, int nranks);
+int tt_allreduce_grads(tt_engine* h, void* stream);
+
 /* ---- introspection -------------------------------------------------------- */
 /* Distinct prefixes (i_1..i_l), l = 1..d, of the last planned batch
  * (unique_per_level[d-1] = distinct IDs).  Synchronises. */

@@ -27,7 +27,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, os.path.join(SRC, "engine.cu")]
+    cmd = [NVCC, *FLAGS, "-o", LIB, os.path.join(SRC, "engine.cu"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

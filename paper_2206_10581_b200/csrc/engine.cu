@@ -17,6 +17,7 @@
 #include <utility>
 
 #include "../../include/tt_engine.h"
+#include "comm.cuh"
 #include "common.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_generic.cuh"
@@ -135,6 +136,18 @@ struct tt_engine {
   FusedShape fs{};
   bool tc_ok = false;  // tensor-core (tcgen05) kernels exist for this shape
   TcShape ts{};
+
+  // data parallelism (tt_comm_init*, tt_allreduce_grads): NCCL communicator,
+  // its stream, and the events that order the gradient all-reduce against
+  // the backward -- ev_gF is recorded right after the level-F GEMM kernel
+  // (which alone writes dG_F, 63 of the 64 MB at papers), so that segment's
+  // all-reduce overlaps the backward's remaining kernels
+  ncclComm_t comm = nullptr;
+  bool own_comm = false;
+  int rank = 0, nranks = 1;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_gF = nullptr, ev_bwd = nullptr, ev_comm = nullptr;
+  bool gF_ready = false;
 };
 
 namespace {
@@ -795,6 +808,10 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     }
   }
   if (rc) return rc;
+  if (h->comm) {  // dG_F is final here: its all-reduce may start (tt_allreduce_grads)
+    CU(cudaEventRecord(h->ev_gF, s));
+    h->gF_ready = true;
+  }
   Phase ph_aux(h, 3, s);
   const int WE = f.K * f.NL;
 #define TT_W_CASE(k_, bn_, rp_, nl_) \
@@ -890,6 +907,7 @@ int do_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, cuda
 }
 
 int do_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
+  h->gF_ready = false;
   if (h->dense) CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
   int rc;
   if (h->last_path >= 1)
@@ -1090,6 +1108,10 @@ void tt_engine_destroy(tt_engine* h) {
                   h->perm};
   for (void* p : ptrs) cudaFree(p);
   if (h->own) cudaStreamDestroy(h->own);
+  if (h->s_comm) { cudaStreamSynchronize(h->s_comm); cudaStreamDestroy(h->s_comm); }
+  for (cudaEvent_t e : {h->ev_gF, h->ev_bwd, h->ev_comm})
+    if (e) cudaEventDestroy(e);
+  if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   if (h->s_h2d) { cudaStreamSynchronize(h->s_h2d); cudaStreamDestroy(h->s_h2d); }
   if (h->s_d2h) { cudaStreamSynchronize(h->s_d2h); cudaStreamDestroy(h->s_d2h); }
   for (cudaEvent_t e : {h->ev_up, h->ev_fwd, h->ev_in})
@@ -1342,14 +1364,16 @@ int tt_opt_init(tt_engine* h, int kind, double lr, double beta1, double beta2, d
   h->beta1 = beta1 > 0 ? beta1 : 0.9;
   h->beta2 = beta2 > 0 ? beta2 : 0.999;
   h->eps = eps > 0 ? eps : (kind == TT_OPT_ADAGRAD ? 1e-10 : 1e-8);
-  cudaFree(h->s1); cudaFree(h->s2);
-  h->s1 = h->s2 = nullptr;
+  // state buffers are kept (zeroed) when the kind needs them, so device
+  // pointers captured in a CUDA graph stay valid across re-initialisation
+  if (kind == TT_OPT_SGD) { cudaFree(h->s1); h->s1 = nullptr; }
+  if (kind != TT_OPT_ADAM) { cudaFree(h->s2); h->s2 = nullptr; }
   if (kind != TT_OPT_SGD) {
-    CU(dalloc(&h->s1, h->dc.nparams));
+    if (!h->s1) CU(dalloc(&h->s1, h->dc.nparams));
     CU(cudaMemset(h->s1, 0, sizeof(float) * (size_t)h->dc.nparams));
   }
   if (kind == TT_OPT_ADAM) {
-    CU(dalloc(&h->s2, h->dc.nparams));
+    if (!h->s2) CU(dalloc(&h->s2, h->dc.nparams));
     CU(cudaMemset(h->s2, 0, sizeof(float) * (size_t)h->dc.nparams));
   }
   CU(cudaMemset(h->d_step, 0, sizeof(long long)));
@@ -1539,6 +1563,111 @@ int tt_train_step_host(tt_engine* h, const int64_t* h_idx, int64_t B, const floa
   CU(cudaStreamSynchronize(h->s_d2h));
   CU(cudaStreamSynchronize(h->s_h2d));
   return read_status(h, s);
+}
+
+// ---- data parallelism over NCCL ---------------------------
+namespace {
+int nccl_fail(const char* what, ncclResult_t r) {
+  return fail(TT_ERR_CUDA, std::string(what) + ": " + (nccl().ok ? nccl().GetErrorString(r) : nccl().why));
+}
+
+int comm_attach(tt_engine* h, ncclComm_t comm, bool own, int rank, int nranks) {
+  CU(cudaSetDevice(h->device));
+  if (!h->s_comm) {
+    CU(cudaStreamCreateWithFlags(&h->s_comm, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_gF, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_bwd, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+  }
+  if (h->comm && h->own_comm) nccl().CommDestroy(h->comm);
+  h->comm = comm;
+  h->own_comm = own;
+  h->rank = rank;
+  h->nranks = nranks;
+  h->dense = true;  // every rank's buffer holds its full local gradient: the sum is the global one
+  h->gF_ready = false;
+  return TT_OK;
+}
+}  // namespace
+
+int tt_nccl_unique_id(void* out, int64_t nbytes) {
+  if (!out || nbytes < (int64_t)sizeof(ncclUniqueId)) return fail(TT_ERR_ARG, "tt_nccl_unique_id: need 128 bytes");
+  if (!nccl().ok) return fail(TT_ERR_CUDA, nccl().why);
+  ncclUniqueId id;
+  const ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail("ncclGetUniqueId", r);
+  memcpy(out, &id, sizeof(id));
+  return TT_OK;
+}
+
+int tt_comm_init_rank(tt_engine* h, const void* unique_id, int rank, int nranks) {
+  if (!h || !unique_id) return fail(TT_ERR_ARG, "tt_comm_init_rank: null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(TT_ERR_ARG, "tt_comm_init_rank: bad rank / nranks");
+  if (!nccl().ok) return fail(TT_ERR_CUDA, nccl().why);
+  CU(cudaSetDevice(h->device));
+  CU(cudaDeviceSynchronize());
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = nccl().CommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) return nccl_fail("ncclCommInitRank", r);
+  return comm_attach(h, comm, true, rank, nranks);
+}
+
+int tt_comm_init(tt_engine* h, void* nccl_comm, int rank, int nranks) {
+  if (!h) return fail(TT_ERR_ARG, "tt_comm_init: null handle");
+  if (!nccl_comm) {  // detach
+    CU(cudaSetDevice(h->device));
+    CU(cudaDeviceSynchronize());
+    if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
+    h->comm = nullptr;
+    h->own_comm = false;
+    h->rank = 0;
+    h->nranks = 1;
+    h->dense = false;
+    return TT_OK;
+  }
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(TT_ERR_ARG, "tt_comm_init: bad rank / nranks");
+  if (!nccl().ok) return fail(TT_ERR_CUDA, nccl().why);
+  return comm_attach(h, (ncclComm_t)nccl_comm, false, rank, nranks);
+}
+
+int tt_allreduce_grads(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_allreduce_grads: null handle");
+  if (!h->comm) return fail(TT_ERR_STATE, "tt_allreduce_grads: no communicator (tt_comm_init first)");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevCfg& c = h->dc;
+  const size_t total = (size_t)(c.nparams + h->ntc);
+  const auto& api = nccl();
+  ncclResult_t r;
+  CU(cudaEventRecord(h->ev_bwd, s));
+  if (h->gF_ready && h->last_path >= 1) {
+    // dG_F (the fused level, written only by the GEMM kernel) was final at
+    // ev_gF: its all-reduce overlaps the backward's auxiliary kernels; the
+    // rest of the buffer (the other cores and the touch counters) follows
+    // the whole backward
+    const int F = h->fs.F;
+    const size_t o0 = (size_t)c.core_off[F], o1 = (size_t)(c.core_off[F] + c.m[F] * c.slice[F]);
+    CU(cudaStreamWaitEvent(h->s_comm, h->ev_gF, 0));
+    r = api.AllReduce(h->grads + o0, h->grads + o0, o1 - o0, ncclFloat32, ncclSum, h->comm, h->s_comm);
+    if (r != ncclSuccess) return nccl_fail("ncclAllReduce", r);
+    CU(cudaStreamWaitEvent(h->s_comm, h->ev_bwd, 0));
+    if (o0 > 0) {
+      r = api.AllReduce(h->grads, h->grads, o0, ncclFloat32, ncclSum, h->comm, h->s_comm);
+      if (r != ncclSuccess) return nccl_fail("ncclAllReduce", r);
+    }
+    r = api.AllReduce(h->grads + o1, h->grads + o1, total - o1, ncclFloat32, ncclSum, h->comm, h->s_comm);
+    if (r != ncclSuccess) return nccl_fail("ncclAllReduce", r);
+  } else {
+    CU(cudaStreamWaitEvent(h->s_comm, h->ev_bwd, 0));
+    r = api.AllReduce(h->grads, h->grads, total, ncclFloat32, ncclSum, h->comm, h->s_comm);
+    if (r != ncclSuccess) return nccl_fail("ncclAllReduce", r);
+  }
+  h->gF_ready = false;
+  CU(cudaEventRecord(h->ev_comm, h->s_comm));
+  CU(cudaStreamWaitEvent(s, h->ev_comm, 0));
+  return TT_OK;
 }
 
 int tt_grad_buffer(tt_engine* h, float** d_ptr, int64_t* count) {

@@ -81,9 +81,17 @@ def touch_counts(cfg: TTConfig, idx: np.ndarray) -> List[np.ndarray]:
 
 
 class DataParallelTT:
-    """Wraps a TTEmbedding for one rank of a torch.distributed job: binds the
-    gradient buffer to a torch tensor, turns on dense gradients and
-    all-reduces before every update."""
+    """Wraps a TTEmbedding for one rank of a torch.distributed job (position
+    sharding).
+
+    Under the NCCL backend the data plane is the engine's own: rank 0 draws an
+    NCCL unique id (tt_nccl_unique_id), torch.distributed only ships those 128
+    bytes to the other ranks (control plane), every engine creates its
+    communicator (tt_comm_init_rank), and each step's gradient all-reduce is
+    tt_allreduce_grads -- the level-F core's gradient is reduced as soon as
+    the GEMM kernel that writes it ends, overlapping the rest of the backward.
+    Under gloo (CPU tests) the gradient buffer is bound to a torch tensor and
+    all-reduced by torch.distributed."""
 
     def __init__(self, emb, group=None):
         import torch
@@ -91,6 +99,13 @@ class DataParallelTT:
         self.emb = emb
         self.group = group
         self.dist = dist
+        self.native = (dist.is_initialized() and dist.get_backend(group) == "nccl" and group is None)
+        if self.native:
+            obj = [emb_nccl_id() if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            emb.comm_init_rank(obj[0], dist.get_rank(), dist.get_world_size())
+            self.buf = None
+            return
         n = grad_buffer_len(emb.config)
         self.buf = torch.zeros(n, dtype=torch.float32, device=f"cuda:{emb.device}")
         emb.bind_grad_buffer(self.buf)
@@ -103,12 +118,19 @@ class DataParallelTT:
         self.emb.backward(grad_out, indices)
 
     def allreduce(self):
-        if self.dist.is_initialized() and self.dist.get_world_size() > 1:
+        if self.native:
+            self.emb.allreduce_grads()
+        elif self.dist.is_initialized() and self.dist.get_world_size() > 1:
             self.dist.all_reduce(self.buf, group=self.group)
 
     def step(self):
         self.allreduce()
         self.emb.step()
+
+
+def emb_nccl_id() -> bytes:
+    from .engine import nccl_unique_id
+    return nccl_unique_id()
 
 
 # ---------------------------------------------------------------------------

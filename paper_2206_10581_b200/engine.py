@@ -58,7 +58,7 @@ SYMBOLS = [
     "tt_cores_snapshot", "tt_cores_restore", "tt_plan_stats", "tt_plan_digits", "tt_plan_sorted", "tt_launch_count", "tt_set_profiling", "tt_profile_read", "tt_set_path", "tt_last_path",
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
     "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_opt_set_hparams", "tt_debug_trace", "tt_set_permutation",
-    "tt_ortho_cores_f64",
+    "tt_ortho_cores_f64", "tt_nccl_unique_id", "tt_comm_init_rank", "tt_comm_init", "tt_allreduce_grads",
 ]
 
 
@@ -99,6 +99,8 @@ def load_library(build_if_missing: bool = True):
         "tt_opt_state_get_f64": (i32, [vp, vp, vp, vp]), "tt_opt_state_set_f64": (i32, [vp, vp, vp, i64]),
         "tt_debug_trace": (i64, [vp, i64]), "tt_set_permutation": (i32, [vp, vp, i64]),
         "tt_ortho_cores_f64": (i32, [vp, i32, C.c_uint64, dbl, vp, vp]),
+        "tt_nccl_unique_id": (i32, [vp, i64]), "tt_comm_init_rank": (i32, [vp, vp, i32, i32]),
+        "tt_comm_init": (i32, [vp, vp, i32, i32]), "tt_allreduce_grads": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -446,6 +448,18 @@ class TTEmbedding:
         if self._opt is not None:
             self._opt.step = int(step)
 
+    # ---- NCCL data parallelism through the C-ABI (position sharding) --------
+    def comm_init_rank(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Creates the engine's own NCCL communicator (every rank passes the
+        same 128-byte id from nccl_unique_id())."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _raise(self._lib.tt_comm_init_rank(self._h, buf, rank, world), "tt_comm_init_rank")
+
+    def allreduce_grads(self) -> None:
+        """Sum all-reduce of the gradient buffer over the communicator,
+        stream-ordered between backward and step (tt_allreduce_grads)."""
+        _raise(self._lib.tt_allreduce_grads(self._h, self._stream()), "tt_allreduce_grads")
+
     def opt_step(self) -> int:
         s = C.c_int64()
         _raise(self._lib.tt_opt_get_step(self._h, C.byref(s)), "tt_opt_get_step")
@@ -500,6 +514,12 @@ def apply_update(emb: TTEmbedding, grads: CoreGradients, opt: OptimizerState) ->
         emb._grad_version += 1
     _raise(emb._lib.tt_apply_update(emb._h), "apply_update")
     opt.step = emb.opt_step()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _raise(load_library().tt_nccl_unique_id(buf, 128), "tt_nccl_unique_id")
+    return buf.raw
 
 
 def ffma_peak_tflops(device: int = 0, iters: int = 4096) -> float:
