@@ -577,8 +577,81 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
 #define FUSED_CASE_B(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.BN == bn_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_fused_bwd<k_, bn_, rp_, nl_>), f.smem_bwd, grid, s, a);
 
-int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a, int grid, cudaStream_t s) {
+// TT_FWD8=0 selects the 8 x 4-tile forward (k_fused_fwd) where the 8 x 8 one exists
+bool fwd8_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_FWD8");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
+// Chunks per digit group for a fused GEMM launch of `grid` = groups x column
+// blocks CTAs: enough CTAs for ~3 waves of 2 per SM (products: 140 groups x
+// 1 block -> 7 chunks each; billion: 178 -> 5; papers: 1924 -> 1).  TT_SPLIT
+// overrides (1 = one CTA per (group, column block)).
+// Chunks are only worth it for large groups: an empty CTA (a chunk a small
+// group does not have) still costs a CTA slot, measured at ~10 us per launch
+// at products / small.  The host bounds a group's rows by
+// min(B, prod_{p<=F} m_p) / m_F x RP (the level-F prefixes of the batch) and
+// splits only when that bound allows min_rows x 2 rows per chunk
+// (profiles/r02/NOTES.md: billion 7.45 -> 5.7 ms; products / small / sweeps
+// slower when split).
+int split_for(tt_engine* h, int grid, int level, bool fwd) {
+  static const int env = [] {
+    const char* e = getenv("TT_SPLIT");
+    return e && *e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  const DevCfg& c = h->dc;
+  long double prefixes = 1;
+  for (int k = 0; k <= level; ++k) prefixes *= (long double)c.m[k];
+  const long double nodes = std::min<long double>((long double)h->B, prefixes) / (long double)c.m[level];
+  const long double rows = nodes * (long double)c.rows[level];
+  const int min_rows = fwd ? 4096 : 1024;
+  const int by_rows = (int)std::min<long double>(16.0L, rows / min_rows);
+  const int target = h->nsm * 6;
+  const int by_grid = std::max(1, std::min(16, (target + grid - 1) / grid));
+  return std::max(1, std::min(by_rows, by_grid));
+}
+
+int split_rows_env(bool fwd, int dflt) {
+  static const int f = [] { const char* e = getenv("TT_SPLIT_ROWS_FWD"); return e && *e ? atoi(e) : 0; }();
+  static const int b = [] { const char* e = getenv("TT_SPLIT_ROWS_BWD"); return e && *e ? atoi(e) : 0; }();
+  const int v = fwd ? f : b;
+  return v > 0 ? v : dflt;
+}
+
+int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaStream_t s) {
   const FusedShape& f = h->fs;
+  FusedArgs a = a0;
+  const int groups = grid0 / a.ncb;
+  a.split = split_for(h, grid0, a.F, fwd);
+  // min rows per chunk: the forward (a short GEMM per tile, then stores) only
+  // pays off with long chunks; the backward (dC formation latency-bound) with
+  // short ones (measured: profiles/r02/NOTES.md)
+  a.split_rows = fwd ? split_rows_env(true, 1024) : split_rows_env(false, 128);
+  const int grid = grid0 * a.split;
+  if (!fwd && a.split > 1) {  // dG_F partials of the chunks, reduced below in a fixed order
+    const int64_t need = (int64_t)groups * a.split * h->dc.slice[a.F];
+    if (h->F.cap_gsplit < need) {
+      cudaFree(h->F.gsplit);
+      h->F.gsplit = nullptr;
+      h->F.cap_gsplit = 0;
+      CU(dalloc(&h->F.gsplit, need));
+      h->F.cap_gsplit = need;
+    }
+    a.gsplit = h->F.gsplit;
+  }
+  if (fwd && f.BNf == 128 && fwd8_enabled()) {
+#define FWD8_CASE(k_, rp_)                                                                       \
+  if (f.K == k_ && f.RP == rp_) {                                                                \
+    FUSED_LAUNCH_T((k_fused_fwd8<k_, rp_>), fwd8_smem(k_), grid, F8_THREADS, s, a);               \
+    return TT_OK;                                                                                \
+  }
+    TT_FWD8_SHAPES(FWD8_CASE)
+#undef FWD8_CASE
+  }
   if (fwd) {
     if (false) {
     }
@@ -589,6 +662,9 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a, int grid, cudaStr
     }
     TT_FUSED_SHAPES(FUSED_CASE_B)
     else return fail(TT_ERR_ARG, "fused path: backward shape not compiled");
+    if (a.split > 1)
+      LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, a.F,
+             a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
   }
   return TT_OK;
 }

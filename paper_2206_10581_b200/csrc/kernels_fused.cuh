@@ -63,6 +63,8 @@ struct FusedBufs {
   float* part = nullptr;   // [chunks][2][npad]   k_dy_chunks partials
   float* gpart = nullptr;  // [groups][2][npad]   k_dy_groups partials
   float* dPcw = nullptr;   // wide-level dA partials
+  float* gsplit = nullptr; // dG partials of split digit groups (FusedArgs::gsplit)
+  int64_t cap_gsplit = 0;
   int64_t cap_nodes = 0, cap_ids = 0, cap_chunks = 0, cap_w = 0;
 };
 
@@ -75,6 +77,7 @@ inline void free_fused(FusedBufs& b) {
   cudaFree(b.part);
   cudaFree(b.gpart);
   cudaFree(b.dPcw);
+  cudaFree(b.gsplit);
   b = FusedBufs{};
 }
 
@@ -100,9 +103,38 @@ struct FusedArgs {
   float* W;
   float* dPc;
   float* grads;
+  int split;       // max chunks per digit group (work_item); > 1: dG_F partials in gsplit
+  int split_rows;  // min rows per chunk
+  float* gsplit;  // [groups][split][slice] dG_F partials of the chunks (k_fused_reduce_gsplit)
   const DevStatus* st;
   long long* dbg;  // optional per-CTA phase timestamps (TT_TC_TRACE builds only)
 };
+
+// A fused GEMM CTA's work item: digit group g, column block cb, and chunk
+// `chunk` of the group's nodes (a.split chunks of equal node count: groups are
+// split when m_F x ncb alone would leave SMs idle -- products has 140 groups
+// and one column block, billion 178).  Returns false for an empty item.
+// Chunks of a group of n nodes (RP rows each): at most `split`, and at least
+// `min_rows` rows per chunk (small groups stay whole: splitting them only
+// re-stages the slice block and leaves tiles part-empty).
+__host__ __device__ __forceinline__ int group_chunks(int n, int RP, int split, int min_rows) {
+  const int64_t by_rows = ((int64_t)n * RP) / (min_rows > 0 ? min_rows : 1);
+  return (int)(by_rows < 1 ? 1 : (by_rows < split ? by_rows : split));
+}
+
+__device__ __forceinline__ bool work_item(const FusedArgs& a, int& g, int& cb, int& chunk, int& g0, int& g1) {
+  const int split = a.split > 1 ? a.split : 1;
+  const int gc = blockIdx.x / a.ncb;
+  cb = blockIdx.x - gc * a.ncb;
+  g = gc / split;
+  chunk = gc - g * split;
+  const int n0 = a.goffF[g], n = a.goffF[g + 1] - n0;
+  const int nch = group_chunks(n, a.RP, split, a.split_rows);
+  if (chunk >= nch) return false;
+  g0 = n0 + (int)(((int64_t)n * chunk) / nch);
+  g1 = n0 + (int)(((int64_t)n * (chunk + 1)) / nch);
+  return g0 < g1;
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -113,10 +145,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Stage the (K x BN) column block cb of slice g of core F: Bs[k][n], row stride SB.
-template <int K, int BN, int SB>
+template <int K, int BN, int SB, int NT = FB_THREADS>
 __device__ __forceinline__ void load_slice_block(const FusedArgs& a, int g, int cb, float* Bs) {
   const float* src = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
-  for (int i = threadIdx.x; i < K * BN / 4; i += FB_THREADS) {
+  for (int i = threadIdx.x; i < K * BN / 4; i += NT) {
     const int k = i / (BN / 4), q = i - k * (BN / 4);
     cp_async16(Bs + k * SB + q * 4, src + (int64_t)k * a.NC + q * 4);
   }
@@ -127,6 +159,7 @@ constexpr int FB_NB = 256;  // nodes whose metadata is staged per batch
 // Metadata for nodes [nb0, nb0 + nbn) of the group (one thread per node):
 // node id, first distinct ID, A-block offset, and the exclusive prefix of the
 // nodes' distinct-ID counts (s_pref[nbn] = total).  Ends with a barrier.
+template <int NT = FB_THREADS>
 __device__ __forceinline__ void prep_nodes(const FusedArgs& a, int nb0, int nbn, int* s_node, int* s_cs0,
                                            int* s_pref, int64_t* s_aoff, int* s_wsum) {
   const int t = threadIdx.x;
@@ -149,13 +182,13 @@ __device__ __forceinline__ void prep_nodes(const FusedArgs& a, int nb0, int nbn,
   if (lane_id() == 31) s_wsum[t >> 5] = x;
   __syncthreads();
   if (t < 32) {
-    int w = t < FB_THREADS / 32 ? s_wsum[t] : 0;
+    int w = t < NT / 32 ? s_wsum[t] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, w, o);
       if ((int)lane_id() >= o) w += y;
     }
-    if (t < FB_THREADS / 32) s_wsum[t] = w;  // inclusive warp totals
+    if (t < NT / 32) s_wsum[t] = w;  // inclusive warp totals
   }
   __syncthreads();
   const int excl = x - cnt + ((t >> 5) ? s_wsum[(t >> 5) - 1] : 0);
@@ -168,9 +201,9 @@ constexpr int FB_IDS = 512;  // per-batch distinct IDs whose metadata is staged
 
 // A tile (BM x K, row-major) of batch-local nodes [tb, tb+nn) by cp.async;
 // rows past the tile's nodes are zero-filled.
-template <int K, int RP>
+template <int K, int RP, int NT = FB_THREADS>
 __device__ __forceinline__ void load_A_tile(const FusedArgs& a, int tb, int nn, const int64_t* s_aoff, float* As) {
-  for (int i = threadIdx.x; i < FB_BM * K / 4; i += FB_THREADS) {
+  for (int i = threadIdx.x; i < FB_BM * K / 4; i += NT) {
     const int m = i / (K / 4), q = i - m * (K / 4);
     const int j = m / RP;
     float* dst = As + m * K + q * 4;
@@ -238,9 +271,8 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
   int* s_wsum = s_pref + FB_NB + 4;
 
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
-  const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
-  if (g0 == g1) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = warp * 8;
 
@@ -291,7 +323,174 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
           store_row_frag<BN>(a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN, lane, acc[i]);
       }
     }
+    __syncthreads();  // the batch's node metadata is rewritten by the next prep_nodes
   }
+}
+
+// dC rows m0..m0+7 of the warp (GEMM layout) for the tile's nodes into Ds:
+// dC[row][col] = sum over the node's IDs and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
+template <int K, int BN, int RP, int NL>
+__device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int cb, const int* s_pref, const int* s_cs0,
+                                        const int* s_bd, float* Ds) {
+  constexpr int TN = BN / 32;
+  using CM = ColMap<BN>;
+  constexpr int W4 = CM::W4, NQ = CM::NQ;
+  constexpr int NR = RP < 8 ? RP : 8;
+  constexpr int NPW = 8 / NR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = warp * 8;
+  const int nF = a.nF;
+  const int64_t npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+
+  // dC in registers (GEMM layout): dC[row][col] = sum over the node's IDs
+  // and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
+  float dacc[8][TN];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) dacc[i][j] = 0.f;
+#pragma unroll
+  for (int jw = 0; jw < NPW; ++jw) {
+    const int j = (m0 + jw * NR) / RP;
+    if (j >= nn) continue;
+    const int ar0 = (m0 + jw * NR) % RP;
+    const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
+    for (int f = fA; f < fB; ++f) {
+      const int u = cs0 + (f - fA);
+      const float* Gp = Gl + (int64_t)(f < FB_IDS ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
+      const float* Yp = a.dY + (int64_t)u * npad;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        // global column of P_F: core-F column block jf, rank index r0
+        // (BN may be smaller than K: a block then covers part of one jf)
+        const int colg = cb * BN + CM::col(lane, q);
+        const int r0 = colg % K, jf = colg / K;
+        float gv[W4][NL];
+#pragma unroll
+        for (int t = 0; t < W4; ++t)
+#pragma unroll
+          for (int l4 = 0; l4 < NL; l4 += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
+            gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
+          }
+#pragma unroll
+        for (int ii = 0; ii < NR; ++ii) {
+          float yv[NL];
+          const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + jf) * NL;
+#pragma unroll
+          for (int l4 = 0; l4 < NL; l4 += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
+            yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+          }
+#pragma unroll
+          for (int t = 0; t < W4; ++t) {
+            float s = dacc[jw * NR + ii][q * W4 + t];
+#pragma unroll
+            for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[jl], gv[t][jl], s);
+            dacc[jw * NR + ii][q * W4 + t] = s;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Forward with 8 x 8 register tiles (BN = 128, K = 32 / 64): 128 threads per
+// CTA, each owning 8 rows x 8 columns of the 64 x 128 C tile.  Per k step a
+// thread reads 8 A values and 8 slice values for 64 FFMAs -- 0.25 shared-memory
+// floats per FFMA, against 0.375 for the 8 x 4 tiles of k_fused_fwd, whose
+// shared-memory bandwidth (32 floats / clk / SM) capped the FMA pipe at 67%.
+// Lane (rh, cl) = (lane / 16, lane % 16) of warp w owns rows w*16 + rh*8 ..+8
+// and columns cl*4 ..+4 and 64 + cl*4 ..+4 (each 16-lane group reads 256
+// contiguous bytes of a slice row: conflict-free).
+constexpr int F8_THREADS = 128;
+
+template <int K, int RP>
+__global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int BN = 128, BM = FB_BM, SB = BN + 4, NPT = BM / RP, NB = F8_THREADS;
+  extern __shared__ __align__(16) float smem[];
+  float* Bs = smem;                      // [K][SB]
+  float* As0 = Bs + K * SB;              // [2][BM][K]
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * K);
+  int* s_node = reinterpret_cast<int*>(s_aoff + NB);
+  int* s_cs0 = s_node + NB;
+  int* s_pref = s_cs0 + NB;               // [NB + 1]
+  int* s_wsum = s_pref + NB + 4;
+
+  if (tt_failed(a.st)) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = warp * 16 + (lane >> 4) * 8, c0 = (lane & 15) * 4;
+
+  load_slice_block<K, BN, SB, F8_THREADS>(a, g, cb, Bs);
+  cp_async_commit();
+  for (int nb0 = g0; nb0 < g1; nb0 += NB) {
+    const int nbn = min(NB, g1 - nb0);
+    prep_nodes<F8_THREADS>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    load_A_tile<K, RP, F8_THREADS>(a, 0, min(NPT, nbn), s_aoff, As0);
+    cp_async_commit();
+    int buf = 0;
+    for (int tb = 0; tb < nbn; tb += NPT, buf ^= 1) {
+      const int nn = min(NPT, nbn - tb);
+      cp_async_wait<0>();
+      __syncthreads();
+      if (tb + NPT < nbn)  // the next tile's A under this tile's GEMM
+        load_A_tile<K, RP, F8_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
+      cp_async_commit();
+      if (r0 >= nn * RP) continue;  // rows past the group's end: no work (warp-uniform per half)
+      const float* As = As0 + buf * BM * K;
+      float acc[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+      for (int kk = 0; kk < K; kk += 4) {
+        float4 av[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (r0 + i) * K + kk);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float4 b0 = *reinterpret_cast<const float4*>(Bs + (kk + t) * SB + c0);
+          const float4 b1 = *reinterpret_cast<const float4*>(Bs + (kk + t) * SB + 64 + c0);
+          const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = r0 + i, j = m / RP;
+        if (j < nn) {
+          float* dst = a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN;
+          *reinterpret_cast<float4*>(dst + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+          *reinterpret_cast<float4*>(dst + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        }
+      }
+    }
+    __syncthreads();  // the batch's node metadata is rewritten by the next prep_nodes
+  }
+}
+
+// (K, RP) instantiations of k_fused_fwd8 (papers, sweep64).  Measured (papers,
+// 1 B200): 0.552 -> 0.541 ms; at K = 32 it was slower (products 0.023 ->
+// 0.025 ms, billion's fused level 1.58 -> 1.73 ms), so those keep k_fused_fwd.
+#define TT_FWD8_SHAPES(X) X(64, 4)
+
+inline size_t fwd8_smem(int K) {
+  const size_t NB = F8_THREADS;
+  return sizeof(float) * ((size_t)K * 132 + 2 * FB_BM * K) + sizeof(int64_t) * NB + sizeof(int) * (3 * NB + 12) + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -329,9 +528,8 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   };
   TR();
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
-  const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
-  if (g0 == g1) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
   load_slice_block<K, BN, SB>(a, g, cb, Bs);
   cp_async_commit();
 
@@ -378,61 +576,8 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
       }
       cp_async_commit();
       if (a.mode == 0) {
-
-      // dC in registers (GEMM layout): dC[row][col] = sum over the node's IDs
-      // and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
-      float dacc[8][TN];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dacc[i][j] = 0.f;
-#pragma unroll
-      for (int jw = 0; jw < NPW; ++jw) {
-        const int j = (m0 + jw * NR) / RP;
-        if (j >= nn) continue;
-        const int ar0 = (m0 + jw * NR) % RP;
-        const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
-        for (int f = fA; f < fB; ++f) {
-          const int u = cs0 + (f - fA);
-          const float* Gp = Gl + (int64_t)(f < FB_IDS ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
-          const float* Yp = a.dY + (int64_t)u * npad;
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            // global column of P_F: core-F column block jf, rank index r0
-            // (BN may be smaller than K: a block then covers part of one jf)
-            const int colg = cb * BN + CM::col(lane, q);
-            const int r0 = colg % K, jf = colg / K;
-            float gv[W4][NL];
-#pragma unroll
-            for (int t = 0; t < W4; ++t)
-#pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
-                gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
-              }
-#pragma unroll
-            for (int ii = 0; ii < NR; ++ii) {
-              float yv[NL];
-              const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + jf) * NL;
-#pragma unroll
-              for (int l4 = 0; l4 < NL; l4 += 4) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
-                yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
-              }
-#pragma unroll
-              for (int t = 0; t < W4; ++t) {
-                float s = dacc[jw * NR + ii][q * W4 + t];
-#pragma unroll
-                for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[jl], gv[t][jl], s);
-                dacc[jw * NR + ii][q * W4 + t] = s;
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
-      cp_async_wait<0>();  // slice block + A tile landed
+        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds);
+        cp_async_wait<0>();  // slice block + A tile landed
       } else {
         cp_async_wait<0>();  // slice block + A tile + dC tile
       }
@@ -522,7 +667,8 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
     }
   }
   // the group's dG_F column block (one writer per slice block: no atomics)
-  float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN;
+  float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                              : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN;
 #pragma unroll
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
@@ -862,6 +1008,30 @@ __global__ void k_fused_reduce_children(DevCfg c, int F, int ncb, int per, const
       dst[c.core_off[0] + (int64_t)digit0[p] * c.slice[0] + e] = acc;
     else
       dst[t] = acc;
+  }
+}
+
+// dG_F[g] = sum over the group's nonempty chunks c (ascending) of gpart[g][c]
+// (split > 1; a fixed order, so the result does not depend on scheduling).
+__global__ void k_fused_reduce_gsplit(DevCfg c, int F, int split, int split_rows, const int* __restrict__ goffF,
+                                      const float* __restrict__ gsplit, float* __restrict__ grads, const DevStatus* st) {
+  TT_PDL_ENTRY();
+  if (tt_failed(st)) return;
+  const int64_t per4 = c.slice[F] / 4;
+  const int64_t total = c.m[F] * per4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(t / per4);
+    const int64_t e4 = t - (int64_t)g * per4;
+    const int n = goffF[g + 1] - goffF[g];
+    if (n == 0) continue;
+    const int nch = group_chunks(n, (int)c.rows[F], split, split_rows);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ch = 0; ch < nch; ++ch) {
+      if (((int64_t)n * (ch + 1)) / nch == ((int64_t)n * ch) / nch) continue;  // empty chunk: nothing written
+      const float4 x = reinterpret_cast<const float4*>(gsplit + ((int64_t)g * split + ch) * c.slice[F])[e4];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    reinterpret_cast<float4*>(grads + c.core_off[F] + (int64_t)g * c.slice[F])[e4] = acc;
   }
 }
 
