@@ -615,6 +615,17 @@ int split_for(tt_engine* h, int grid, int level, bool fwd) {
   return std::max(1, std::min(by_rows, by_grid));
 }
 
+// TT_BWDK32 = bit mask of the RP values using k_fused_bwd_k32 (1: RP 4, 2: RP 16);
+// default 2: billion's level-F backward 2.75 -> 2.44 ms, while at RP 4
+// (products 0.068 -> 0.087 ms, sweep32 0.262 -> 0.324) k_fused_bwd is faster
+bool bwdk32_enabled(int rp) {
+  static const int mask = [] {
+    const char* e = getenv("TT_BWDK32");
+    return e && *e ? atoi(e) : 2;
+  }();
+  return (rp == 4 && (mask & 1)) || (rp == 16 && (mask & 2));
+}
+
 int split_rows_env(bool fwd, int dflt) {
   static const int f = [] { const char* e = getenv("TT_SPLIT_ROWS_FWD"); return e && *e ? atoi(e) : 0; }();
   static const int b = [] { const char* e = getenv("TT_SPLIT_ROWS_BWD"); return e && *e ? atoi(e) : 0; }();
@@ -642,6 +653,18 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
       h->F.cap_gsplit = need;
     }
     a.gsplit = h->F.gsplit;
+  }
+  if (!fwd && f.K == 32 && f.BN == 128 && bwdk32_enabled(f.RP)) {
+#define BWDK32_CASE(rp_, nl_)                                                                    \
+  if (f.RP == rp_ && f.NL == nl_) {                                                              \
+    FUSED_LAUNCH_T((k_fused_bwd_k32<rp_, nl_>), bwd_k32_smem(), grid, K32_THREADS, s, a);         \
+    if (a.split > 1)                                                                             \
+      LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
+             a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
+    return TT_OK;                                                                                \
+  }
+    TT_BWDK32_SHAPES(BWDK32_CASE)
+#undef BWDK32_CASE
   }
   if (fwd && f.BNf == 128 && fwd8_enabled()) {
 #define FWD8_CASE(k_, rp_)                                                                       \

@@ -331,14 +331,13 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 // dC[row][col] = sum over the node's IDs and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
 template <int K, int BN, int RP, int NL>
 __device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int cb, const int* s_pref, const int* s_cs0,
-                                        const int* s_bd, float* Ds) {
+                                        const int* s_bd, float* Ds, int m0) {
   constexpr int TN = BN / 32;
   using CM = ColMap<BN>;
   constexpr int W4 = CM::W4, NQ = CM::NQ;
   constexpr int NR = RP < 8 ? RP : 8;
   constexpr int NPW = 8 / NR;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = warp * 8;
+  const int lane = threadIdx.x & 31;
   const int nF = a.nF;
   const int64_t npad = a.c.npad;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
@@ -576,7 +575,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
       }
       cp_async_commit();
       if (a.mode == 0) {
-        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds);
+        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds, (threadIdx.x >> 5) * 8);
         cp_async_wait<0>();  // slice block + A tile landed
       } else {
         cp_async_wait<0>();  // slice block + A tile + dC tile
@@ -672,6 +671,158 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
 #pragma unroll
   for (int i = 0; i < TK; ++i) store_row_frag<BN>(gdst + (int64_t)(warp * TK + i) * a.NC, lane, gacc[i]);
 }
+
+// ---------------------------------------------------------------------------
+// Backward for rank 32 (K = 32, BN = 128): 128-thread CTAs, 3 per SM, the two
+// GEMMs on separate warp pairs.  With 256 threads k_fused_bwd's tiles at
+// K = 32 are 4 x 4 (dG_F) and 4 x 2 (dA): 0.5 and 0.75 shared-memory floats per
+// FFMA, which bounds it well below the FMA pipe (billion: 26-37% of peak).
+// Here, after all 4 warps have formed the tile's dC (16 rows each):
+//   warps 0-1: dG_F += A^T dC with 8 x 8 tiles (thread t: k rows (t/16)*8 ..+8,
+//     columns (t%16)*4 ..+4 and 64 + (t%16)*4 ..+4): 0.25 floats / FFMA;
+//   warps 2-3: dA = dC S^T with 8 x 4 tiles (rows (t/8)*8 ..+8, k = t%8 + 8j):
+//     0.375 floats / FFMA;
+// one 64-entry accumulator array is the persistent dG_F tile in warps 0-1 and
+// the per-tile dA tile in warps 2-3.  mode 1 (a wide level) loads dC.
+constexpr int K32_THREADS = 128, K32_NB = 128;
+
+template <int RP, int NL>
+__global__ void __launch_bounds__(K32_THREADS, 3) k_fused_bwd_k32(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int K = 32, BN = 128, BM = FB_BM, SB = BN + 4, NPT = BM / RP, NB = K32_NB;
+  extern __shared__ __align__(16) float smem[];
+  float* Bs = smem;               // [K][SB]
+  float* As = Bs + K * SB;        // [BM][K]
+  float* Ds = As + BM * K;        // [BM][BN]  dC
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Ds + BM * BN);
+  int* s_node = reinterpret_cast<int*>(s_aoff + NB);
+  int* s_cs0 = s_node + NB;
+  int* s_pref = s_cs0 + NB;
+  int* s_wsum = s_pref + NB + 4;
+  int* s_bd = s_wsum + 8;  // [FB_IDS]
+
+  if (tt_failed(a.st)) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
+  load_slice_block<K, BN, SB, K32_THREADS>(a, g, cb, Bs);
+  cp_async_commit();
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const bool gw = warp < 2;
+  const int kb = (tid >> 4) * 8, c0 = (tid & 15) * 4;        // dG role (tid < 64)
+  const int t2 = tid - 64, mg8 = (t2 >> 3) * 8, kg = t2 & 7;  // dA role (tid >= 64)
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  for (int nb0 = g0; nb0 < g1; nb0 += NB) {
+    const int nbn = min(NB, g1 - nb0);
+    prep_nodes<K32_THREADS>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    if (a.mode == 0) {  // digits of the batch's IDs: one L2 round trip per batch, not per ID
+      const int tot = min(s_pref[nbn], FB_IDS);
+      for (int f = tid; f < tot; f += K32_THREADS) {
+        int lo = 0, hi = nbn - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_pref[mid] <= f) lo = mid; else hi = mid - 1;
+        }
+        s_bd[f] = __ldg(a.digitL + s_cs0[lo] + (f - s_pref[lo]));
+      }
+      __syncthreads();
+    }
+    for (int tb = 0; tb < nbn; tb += NPT) {
+      const int nn = min(NPT, nbn - tb);
+      const int mlim = nn * RP;
+      load_A_tile<K, RP, K32_THREADS>(a, tb, nn, s_aoff, As);
+      if (a.mode == 1) {  // the materialised dC tile
+        for (int i = tid; i < BM * BN / 4; i += K32_THREADS) {
+          const int m = i / (BN / 4), q = i - m * (BN / 4);
+          const int j = m / RP;
+          float* dst = Ds + m * BN + q * 4;
+          if (j < nn) cp_async16(dst, a.dPin + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
+          else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      cp_async_commit();
+      if (a.mode == 0) {
+        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds, warp * 16);
+        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds, warp * 16 + 8);
+      }
+      cp_async_wait<0>();  // slice block + A tile (+ dC tile)
+      __syncthreads();
+      if (gw) {
+#pragma unroll 2
+        for (int m = 0; m < BM; ++m) {
+          if (m >= mlim) break;
+          const float4 a0 = *reinterpret_cast<const float4*>(As + m * K + kb);
+          const float4 a1 = *reinterpret_cast<const float4*>(As + m * K + kb + 4);
+          const float4 d0 = *reinterpret_cast<const float4*>(Ds + m * BN + c0);
+          const float4 d1 = *reinterpret_cast<const float4*>(Ds + m * BN + 64 + c0);
+          const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+          const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], dv[j], acc[i][j]);
+        }
+      } else if (mg8 < mlim) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+        for (int n = 0; n < BN; n += 4) {
+          float4 cv[8], bv[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg8 + i) * BN + n);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + 8 * j) * SB + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc[i][j] = fmaf(cv[i].x, bv[j].x, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].y, bv[j].y, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].z, bv[j].z, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].w, bv[j].w, acc[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = mg8 + i;
+          const int j = m / RP;
+          if (j >= nn) continue;
+          float* dst = a.dPc + ((int64_t)s_node[tb + j] * a.ncb + cb) * RP * K + (m - j * RP) * K;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) dst[kg + 8 * jj] = acc[i][jj];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (gw) {  // the group's (chunk's) dG_F column block
+    float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float* row = gdst + (int64_t)(kb + i) * a.NC;
+      *reinterpret_cast<float4*>(row + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      *reinterpret_cast<float4*>(row + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+  }
+}
+
+inline size_t bwd_k32_smem() {
+  return sizeof(float) * (32 * 132 + FB_BM * 32 + FB_BM * 128) + sizeof(int64_t) * K32_NB +
+         sizeof(int) * (3 * K32_NB + 12 + 8 + FB_IDS) + 16;
+}
+
+// (RP, NL) instantiations of k_fused_bwd_k32 (billion's level F; the RP = 4
+// variant measured slower than k_fused_bwd, profiles/r02/NOTES.md)
+#define TT_BWDK32_SHAPES(X) X(16, 4)
 
 // Streaming kernels over the saved P_F, one warp per distinct ID
 // (grid-stride).  The ID's prefix block P_F[p] (RP x NC floats, contiguous)

@@ -91,6 +91,18 @@ def test_every_fwd8_instantiation_has_a_parity_case():
     assert not missing, f"compiled 8x8-tile forward instantiations with no parity case: {missing}"
 
 
+def test_every_bwdk32_instantiation_has_a_parity_case():
+    src = open(os.path.join(CSRC, "kernels_fused.cuh")).read()
+    m = re.search(r"#define\s+TT_BWDK32_SHAPES\(X\)([^\n]*)", src)
+    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+)\)", m.group(1))}
+    covered = set()
+    for name in FUSED_SHAPES:
+        ffma, _ = reached(SHAPES[name][0]())
+        covered |= {(t[2], t[3]) for t in ffma if t[0] == 32 and t[1] == 128 and t[3] != "*"}
+    missing = sorted(t for t in compiled if t not in covered)
+    assert not missing, f"compiled rank-32 backward instantiations with no parity case: {missing}"
+
+
 def test_every_tcgen05_instantiation_has_a_parity_case():
     compiled = _macro_tuples("kernels_tcgen05.cuh", "TT_TC_SHAPES")
     covered = set()
