@@ -4,6 +4,7 @@
 // stream-ordered and host-sync free (counts that depend on the batch stay on
 // the device), so a whole training step can be captured in a CUDA graph.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -148,6 +149,11 @@ struct tt_engine {
   cudaStream_t s_comm = nullptr;
   cudaEvent_t ev_gF = nullptr, ev_bwd = nullptr, ev_comm = nullptr;
   bool gF_ready = false;
+
+  // TMA tensor maps of the cores for the fused forward (level k -> [m_k R_k] x
+  // [n_k R_{k+1}] fp32 view of core k, box {128, R_k})
+  CUtensorMap tmap[TT_MAXD] = {};
+  bool tmap_ok[TT_MAXD] = {};
 };
 
 namespace {
@@ -633,6 +639,40 @@ int split_rows_env(bool fwd, int dflt) {
   return v > 0 ? v : dflt;
 }
 
+// TT_TMA=0 stages the forward's slice block by cp.async instead of TMA
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_TMA");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
+// The tensor map of core k for TMA loads of (K x 128) slice blocks; false
+// when the driver entry point is unavailable (the cp.async kernel runs).
+bool core_tmap(tt_engine* h, int k) {
+  if (h->tmap_ok[k]) return true;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const DevCfg& c = h->dc;
+  const cuuint64_t dims[2] = {(cuuint64_t)c.cols[k], (cuuint64_t)(c.m[k] * c.R[k])};
+  const cuuint64_t strides[1] = {(cuuint64_t)c.cols[k] * sizeof(float)};
+  const cuuint32_t box[2] = {128, (cuuint32_t)c.R[k]};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&h->tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, h->params + c.core_off[k], dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  h->tmap_ok[k] = r == CUDA_SUCCESS;
+  return h->tmap_ok[k];
+}
+
 int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaStream_t s) {
   const FusedShape& f = h->fs;
   FusedArgs a = a0;
@@ -669,7 +709,16 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
   if (fwd && f.BNf == 128 && fwd8_enabled()) {
 #define FWD8_CASE(k_, rp_)                                                                       \
   if (f.K == k_ && f.RP == rp_) {                                                                \
-    FUSED_LAUNCH_T((k_fused_fwd8<k_, rp_>), fwd8_smem(k_), grid, F8_THREADS, s, a);               \
+    if (tma_enabled() && core_tmap(h, a.F)) {                                                    \
+      CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)fwd8_smem(k_)));                                               \
+      tt_launch((k_fused_fwd8<k_, rp_, true>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
+    } else {                                                                                     \
+      CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)fwd8_smem(k_)));                                               \
+      tt_launch((k_fused_fwd8<k_, rp_, false>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
+    }                                                                                            \
+    ++h->launches;                                                                               \
     return TT_OK;                                                                                \
   }
     TT_FWD8_SHAPES(FWD8_CASE)

@@ -28,6 +28,8 @@
 // are reduced by sorted segmented reductions in a fixed order
 // (k_fused_reduce_last, k_fused_reduce_children).
 #pragma once
+#include <cuda.h>  // CUtensorMap (types only: the encoder comes from cudaGetDriverEntryPoint)
+
 #include "common.cuh"
 #include "kernels_rows.cuh"
 
@@ -409,11 +411,39 @@ __device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int 
 // contiguous bytes of a slice row: conflict-free).
 constexpr int F8_THREADS = 128;
 
-template <int K, int RP>
-__global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(FusedArgs a) {
+// TMA (cp.async.bulk.tensor.2d) of the K x 128 slice block: the tensor map
+// views core F as a [m_F K] x [NC] fp32 matrix (slice g = rows g K ..+K), box
+// {128 columns, K rows}; it lands dense in shared memory (row stride 128
+// floats -- the 16-lane row fragments this kernel reads stay conflict-free)
+// and completes on an mbarrier with the byte count.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(map), "r"(x), "r"(y),
+      "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "W:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra W;\n\t}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+template <int K, int RP, bool TMA>
+__global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
+    k_fused_fwd8(FusedArgs a, const __grid_constant__ CUtensorMap tmS) {
   TT_PDL_ENTRY();
-  constexpr int BN = 128, BM = FB_BM, SB = BN + 4, NPT = BM / RP, NB = F8_THREADS;
-  extern __shared__ __align__(16) float smem[];
+  constexpr int BN = 128, BM = FB_BM, SB = TMA ? BN : BN + 4, NPT = BM / RP, NB = F8_THREADS;
+  extern __shared__ __align__(128) float smem[];
   float* Bs = smem;                      // [K][SB]
   float* As0 = Bs + K * SB;              // [2][BM][K]
   int64_t* s_aoff = reinterpret_cast<int64_t*>(As0 + 2 * BM * K);
@@ -421,6 +451,7 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(Fu
   int* s_cs0 = s_node + NB;
   int* s_pref = s_cs0 + NB;               // [NB + 1]
   int* s_wsum = s_pref + NB + 4;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_wsum + 12);  // 8-byte aligned (s_wsum is)
 
   if (tt_failed(a.st)) return;
   int g, cb, g0, g1, chunk;
@@ -428,8 +459,18 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(Fu
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * 16 + (lane >> 4) * 8, c0 = (lane & 15) * 4;
 
-  load_slice_block<K, BN, SB, F8_THREADS>(a, g, cb, Bs);
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(s_bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_expect_tx(s_bar, K * BN * 4);
+      tma_load_2d(Bs, &tmS, s_bar, cb * BN, g * K);
+    }
+  } else {
+    load_slice_block<K, BN, SB, F8_THREADS>(a, g, cb, Bs);
+  }
   cp_async_commit();
+  bool s_ready = !TMA;
   for (int nb0 = g0; nb0 < g1; nb0 += NB) {
     const int nbn = min(NB, g1 - nb0);
     prep_nodes<F8_THREADS>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
@@ -443,6 +484,12 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(Fu
       if (tb + NPT < nbn)  // the next tile's A under this tile's GEMM
         load_A_tile<K, RP, F8_THREADS>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, As0 + (buf ^ 1) * BM * K);
       cp_async_commit();
+      if constexpr (TMA) {
+        if (!s_ready) {  // (every thread passed the barrier above after thread 0 armed it)
+          mbar_wait_parity(s_bar, 0);
+          s_ready = true;
+        }
+      }
       if (r0 >= nn * RP) continue;  // rows past the group's end: no work (warp-uniform per half)
       const float* As = As0 + buf * BM * K;
       float acc[8][8];
@@ -489,7 +536,8 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3) k_fused_fwd8(Fu
 
 inline size_t fwd8_smem(int K) {
   const size_t NB = F8_THREADS;
-  return sizeof(float) * ((size_t)K * 132 + 2 * FB_BM * K) + sizeof(int64_t) * NB + sizeof(int) * (3 * NB + 12) + 16;
+  return sizeof(float) * ((size_t)K * 132 + 2 * FB_BM * K) + sizeof(int64_t) * NB + sizeof(int) * (3 * NB + 12) + 16 +
+         16;
 }
 
 // ---------------------------------------------------------------------------
