@@ -123,6 +123,21 @@ int tt_apply_update(tt_engine* h);
 int tt_train_step_host(tt_engine* h, const int64_t* h_indices, int64_t batch,
                        const float* h_upstream, float* h_out);
 
+/* The same step, pipelined across calls: tt_train_step_submit enqueues one
+ * step (uploads on a copy stream, compute on the handle's stream, the row
+ * download on a second copy stream) into one of two staging slots and returns
+ * at once; tt_train_step_wait retires the oldest submitted step and returns
+ * its status (TT_ERR_INDEX / TT_ERR_NONFINITE as tt_sync would).  With two
+ * steps in flight, step t+1's host-to-device copies run under step t's compute
+ * and device-to-host copy (as a data loader feeding a training loop would);
+ * steps still run in submission order on the cores.  Host buffers must stay
+ * valid until the step is retired; a third submit retires the oldest first. */
+int tt_train_step_submit(tt_engine* h, const int64_t* h_indices, int64_t batch, const float* h_upstream,
+                         float* h_out);
+int tt_train_step_wait(tt_engine* h);
+/* The handle's own CUDA stream (the host-buffer calls run on it). */
+void* tt_engine_stream(tt_engine* h);
+
 /* Dense gradients in the reference layout (CoreGradients, autodiff.hpp:29-34);
  * untouched slices read as exactly 0.  batch_count may be NULL. */
 int tt_get_core_grads_f64(tt_engine* h, double* const* grads, int64_t* batch_count);

@@ -121,6 +121,20 @@ struct tt_engine {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_up = nullptr, ev_fwd = nullptr, ev_in = nullptr;
 
+  // pipelined host-buffer steps (tt_train_step_submit / _wait): two staging
+  // slots, so step t+1's uploads run under step t's compute and download
+  struct HostSlot {
+    int64_t cap = 0, B = 0;
+    int64_t* idx = nullptr;
+    float* up = nullptr;
+    float* out = nullptr;
+    const int64_t* h_idx = nullptr;
+    DevStatus* h_st = nullptr;  // pinned: the device status right after the step
+    cudaEvent_t ev_idx = nullptr, ev_up = nullptr, ev_fwd = nullptr, ev_done = nullptr, ev_out = nullptr;
+    bool busy = false, has_out = false;
+  } hs[2];
+  int hs_next = 0, hs_head = 0, hs_count = 0;
+
   // profiling (tt_set_profiling): event pairs per slot
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[8];
@@ -1255,6 +1269,14 @@ void tt_engine_destroy(tt_engine* h) {
   void* ptrs[] = {h->params, h->own_grads, h->snap, h->s1, h->s2, h->d_step, h->st, h->counts, h->st_idx, h->st_out, h->st_up,
                   h->perm};
   for (void* p : ptrs) cudaFree(p);
+  for (auto& sl : h->hs) {
+    for (cudaEvent_t e : {sl.ev_done, sl.ev_out})
+      if (e) cudaEventSynchronize(e);
+    cudaFree(sl.idx); cudaFree(sl.up); cudaFree(sl.out);
+    if (sl.h_st) cudaFreeHost(sl.h_st);
+    for (cudaEvent_t e : {sl.ev_idx, sl.ev_up, sl.ev_fwd, sl.ev_done, sl.ev_out})
+      if (e) cudaEventDestroy(e);
+  }
   if (h->own) cudaStreamDestroy(h->own);
   if (h->s_comm) { cudaStreamSynchronize(h->s_comm); cudaStreamDestroy(h->s_comm); }
   for (cudaEvent_t e : {h->ev_gF, h->ev_bwd, h->ev_comm})
@@ -1817,6 +1839,97 @@ int tt_allreduce_grads(tt_engine* h, void* stream) {
   CU(cudaStreamWaitEvent(s, h->ev_comm, 0));
   return TT_OK;
 }
+
+// ---- pipelined host-buffer steps ------------------------------------------
+int tt_train_step_wait(tt_engine* h) {
+  if (!h) return fail(TT_ERR_ARG, "tt_train_step_wait: null handle");
+  if (h->hs_count == 0) return TT_OK;
+  CU(cudaSetDevice(h->device));
+  auto& sl = h->hs[h->hs_head];
+  h->hs_head ^= 1;
+  --h->hs_count;
+  sl.busy = false;
+  CU(cudaEventSynchronize(sl.ev_done));
+  if (sl.has_out) CU(cudaEventSynchronize(sl.ev_out));  // (ev_done follows the slot's uploads)
+  const DevStatus st = *sl.h_st;
+  if (st.bad_pos != TT_NO_POS) {
+    const int64_t val = sl.h_idx ? sl.h_idx[st.bad_pos] : 0;
+    h->plan_valid = false;
+    return fail(TT_ERR_INDEX,
+                "lookup_batch: index " + std::to_string(val) + " at batch position " +
+                    std::to_string((long long)st.bad_pos) + " out of [0, " + std::to_string(h->dc.num_nodes) + ")",
+                (int64_t)st.bad_pos, val);
+  }
+  if (st.bad_core != INT_MAX)
+    return fail(TT_ERR_NONFINITE,
+                "apply_update: non-finite gradient in core " + std::to_string(st.bad_core) + "; update rejected",
+                st.bad_core);
+  return TT_OK;
+}
+
+int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const float* h_up, float* h_out) {
+  if (!h) return fail(TT_ERR_ARG, "tt_train_step_submit: null handle");
+  if (B <= 0 || !h_idx || !h_up) return fail(TT_ERR_ARG, "tt_train_step_submit: empty batch or null buffer");
+  CU(cudaSetDevice(h->device));
+  if (h->hs_count == 2) {  // both slots in flight: retire the oldest first
+    int rc = tt_train_step_wait(h);
+    if (rc) return rc;
+  }
+  if (!h->s_h2d) {
+    CU(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  }
+  auto& sl = h->hs[h->hs_next];
+  const int64_t N = h->dc.emb_dim;
+  if (sl.cap < B) {
+    cudaFree(sl.idx); cudaFree(sl.up); cudaFree(sl.out);
+    sl.idx = nullptr; sl.up = nullptr; sl.out = nullptr; sl.cap = 0;
+    CU(dalloc(&sl.idx, B));
+    CU(dalloc(&sl.up, B * N));
+    CU(dalloc(&sl.out, B * N));
+    sl.cap = B;
+  }
+  if (!sl.ev_idx) {
+    for (cudaEvent_t* e : {&sl.ev_idx, &sl.ev_up, &sl.ev_fwd, &sl.ev_done, &sl.ev_out})
+      CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CU(cudaMallocHost(&sl.h_st, sizeof(DevStatus)));
+  }
+  cudaStream_t s = h->own;
+  const size_t rows = sizeof(float) * (size_t)B * (size_t)N;
+  // uploads on the copy stream: the indices first (the plan needs them), the
+  // upstream behind them -- both may run under the previous step's compute
+  CU(cudaMemcpyAsync(sl.idx, h_idx, sizeof(int64_t) * B, cudaMemcpyHostToDevice, h->s_h2d));
+  CU(cudaEventRecord(sl.ev_idx, h->s_h2d));
+  CU(cudaMemcpyAsync(sl.up, h_up, rows, cudaMemcpyHostToDevice, h->s_h2d));
+  CU(cudaEventRecord(sl.ev_up, h->s_h2d));
+  CU(cudaStreamWaitEvent(s, sl.ev_idx, 0));
+  int rc = tt_forward(h, sl.idx, B, sl.out, s);
+  if (rc) { cudaStreamSynchronize(h->s_h2d); cudaStreamSynchronize(s); return rc; }
+  sl.has_out = h_out != nullptr;
+  if (h_out) {  // rows go back under the backward + update (and the next step's upload)
+    CU(cudaEventRecord(sl.ev_fwd, s));
+    CU(cudaStreamWaitEvent(h->s_d2h, sl.ev_fwd, 0));
+    CU(cudaMemcpyAsync(h_out, sl.out, rows, cudaMemcpyDeviceToHost, h->s_d2h));
+    CU(cudaEventRecord(sl.ev_out, h->s_d2h));
+  }
+  CU(cudaStreamWaitEvent(s, sl.ev_up, 0));
+  rc = tt_backward(h, nullptr, B, sl.up, s);
+  if (!rc) rc = tt_step(h, s);
+  if (rc) { cudaStreamSynchronize(h->s_h2d); cudaStreamSynchronize(h->s_d2h); cudaStreamSynchronize(s); return rc; }
+  CU(cudaMemcpyAsync(sl.h_st, h->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(sl.ev_done, s));
+  sl.B = B;
+  sl.h_idx = h_idx;
+  sl.busy = true;
+  h->hs_next ^= 1;
+  ++h->hs_count;
+  return TT_OK;
+}
+
+void* tt_engine_stream(tt_engine* h) { return h ? (void*)h->own : nullptr; }
 
 int tt_grad_buffer(tt_engine* h, float** d_ptr, int64_t* count) {
   if (!h || !d_ptr || !count) return fail(TT_ERR_ARG, "tt_grad_buffer: null argument");

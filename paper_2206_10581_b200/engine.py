@@ -59,6 +59,7 @@ SYMBOLS = [
     "tt_last_error_position", "tt_last_error_value", "tt_last_error", "tt_ffma_peak_tflops", "tt_ffma_outer_tflops",
     "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_opt_set_hparams", "tt_debug_trace", "tt_set_permutation",
     "tt_ortho_cores_f64", "tt_nccl_unique_id", "tt_comm_init_rank", "tt_comm_init", "tt_allreduce_grads",
+    "tt_train_step_submit", "tt_train_step_wait", "tt_engine_stream",
 ]
 
 
@@ -101,6 +102,8 @@ def load_library(build_if_missing: bool = True):
         "tt_ortho_cores_f64": (i32, [vp, i32, C.c_uint64, dbl, vp, vp]),
         "tt_nccl_unique_id": (i32, [vp, i64]), "tt_comm_init_rank": (i32, [vp, vp, i32, i32]),
         "tt_comm_init": (i32, [vp, vp, i32, i32]), "tt_allreduce_grads": (i32, [vp, vp]),
+        "tt_train_step_submit": (i32, [vp, vp, i64, vp, vp]), "tt_train_step_wait": (i32, [vp]),
+        "tt_engine_stream": (vp, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -347,6 +350,27 @@ class TTEmbedding:
         op = out.ctypes.data if out is not None else None
         _raise(self._lib.tt_train_step_host(self._h, idx.ctypes.data, len(idx), up.ctypes.data, op),
                "tt_train_step_host")
+
+    def train_step_submit(self, indices, upstream, out=None) -> None:
+        """Pipelined host-buffer step (tt_train_step_submit): returns at once;
+        the buffers (numpy arrays or pinned torch CPU tensors) must stay alive
+        until train_step_wait() retires the step."""
+        ip = indices.ctypes.data if isinstance(indices, np.ndarray) else indices.data_ptr()
+        up = upstream.ctypes.data if isinstance(upstream, np.ndarray) else upstream.data_ptr()
+        op = None if out is None else (out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr())
+        B = len(indices)
+        _raise(self._lib.tt_train_step_submit(self._h, C.c_void_p(ip), B, C.c_void_p(up),
+                                              None if op is None else C.c_void_p(op)), "tt_train_step_submit")
+
+    def train_step_wait(self) -> None:
+        _raise(self._lib.tt_train_step_wait(self._h), "tt_train_step_wait")
+
+    def engine_stream(self) -> int:
+        return self._lib.tt_engine_stream(self._h) or 0
+
+    def restore_cores_on_engine_stream(self) -> None:
+        """tt_cores_restore ordered with the host-buffer calls (the handle's stream)."""
+        _raise(self._lib.tt_cores_restore(self._h, C.c_void_p(self.engine_stream())), "tt_cores_restore")
 
     def grad_buffer(self):
         p, n = C.c_void_p(), C.c_int64()
