@@ -872,7 +872,11 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       }
-      const int grid = (int)std::min<int64_t>(c.m[f.F] * h->ts.ncbf, sms);
+      // chunks of large digit groups as in the FFMA kernels (billion: 178 items
+      // alone leave the persistent CTAs unevenly loaded)
+      a.split = split_for(h, (int)(c.m[f.F] * h->ts.ncbf), f.F, true);
+      a.split_rows = split_rows_env(true, 1024);
+      const int grid = (int)std::min<int64_t>(c.m[f.F] * h->ts.ncbf * a.split, sms);
       if (false) {
       }
 #define TT_TC_FWD_CASE(k_, bn_, rp_, nl_) \
@@ -950,7 +954,20 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
         a.dbg = trace_buf;
         g_trace_buf = trace_buf;
       }
-      const int grid = (int)(c.m[f.F] * h->ts.ncbb);
+      a.split = split_for(h, (int)(c.m[f.F] * h->ts.ncbb), f.F, false);
+      a.split_rows = split_rows_env(false, 128);
+      if (a.split > 1) {
+        const int64_t need = c.m[f.F] * a.split * c.slice[f.F];
+        if (h->F.cap_gsplit < need) {
+          cudaFree(h->F.gsplit);
+          h->F.gsplit = nullptr;
+          h->F.cap_gsplit = 0;
+          CU(dalloc(&h->F.gsplit, need));
+          h->F.cap_gsplit = need;
+        }
+        a.gsplit = h->F.gsplit;
+      }
+      const int grid = (int)(c.m[f.F] * h->ts.ncbb * a.split);
       rc = TT_OK;
       if (false) {
       }
@@ -958,6 +975,9 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, TCB_THREADS, s, a);
       TT_TC_SHAPES(TT_TC_BWD_CASE)
 #undef TT_TC_BWD_CASE
+      if (a.split > 1)
+        LAUNCH(k_fused_reduce_gsplit, grid_for(c.m[f.F] * c.slice[f.F] / 4, 256, 148 * 8), 256, 0, s, c, f.F, a.split,
+               a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
     } else {
       static long long* trace_buf2 = nullptr;
       if (diag().trace == 1) {

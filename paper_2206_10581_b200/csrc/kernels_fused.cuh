@@ -125,7 +125,15 @@ __host__ __device__ __forceinline__ int group_chunks(int n, int RP, int split, i
 }
 
 __device__ __forceinline__ bool work_item(const FusedArgs& a, int& g, int& cb, int& chunk, int& g0, int& g1) {
-  const int split = a.split > 1 ? a.split : 1;
+  if (a.split <= 1) {
+    g = blockIdx.x / a.ncb;
+    cb = blockIdx.x - g * a.ncb;
+    chunk = 0;
+    g0 = a.goffF[g];
+    g1 = a.goffF[g + 1];
+    return g0 < g1;
+  }
+  const int split = a.split;
   const int gc = blockIdx.x / a.ncb;
   cb = blockIdx.x - gc * a.ncb;
   g = gc / split;

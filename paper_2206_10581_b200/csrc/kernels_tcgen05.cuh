@@ -165,15 +165,38 @@ inline size_t tc_fwd_smem(int K, int BN) {
   return 2 * 3 * (size_t)K * BN * 2 + (size_t)4 * 32 * TCF_ES * 4;
 }
 
+// Work item `it` of the persistent forward: (digit group g, column block cb,
+// chunk of the group's nodes) -- the same chunking as the FFMA kernels'
+// work_item (a.split chunks at most, a.split_rows rows at least); g0 / n =
+// the chunk's first node (in group order) and node count (0: empty item).
+__device__ __forceinline__ void tc_item(const FusedArgs& a, int it, int& g, int& cb, int& g0, int& n) {
+  if (a.split <= 1) {  // (the common case: no chunk arithmetic, no 64-bit divisions)
+    g = it / a.ncb;
+    cb = it - g * a.ncb;
+    g0 = a.goffF[g];
+    n = a.goffF[g + 1] - g0;
+    return;
+  }
+  const int split = a.split;
+  const int gc = it / a.ncb;
+  cb = it - gc * a.ncb;
+  g = gc / split;
+  const int chunk = gc - g * split;
+  const int n0 = a.goffF[g], ng = a.goffF[g + 1] - n0;
+  const int nch = group_chunks(ng, a.RP, split, a.split_rows);
+  if (chunk >= nch) { g0 = n0; n = 0; return; }
+  g0 = n0 + (int)(((int64_t)ng * chunk) / nch);
+  n = n0 + (int)(((int64_t)ng * (chunk + 1)) / nch) - g0;
+}
+
 // A CTA's static tile schedule: items it = blockIdx.x + k * gridDim.x, tiles
-// of npt nodes (tb = first node of the tile within the item's group)
+// of npt nodes (tb = first node of the tile within the item's node range)
 struct TileCursor {
   int it, g0, n, tb;
   __device__ __forceinline__ void seek(const FusedArgs& a, int nitems) {
     while (it < nitems) {
-      const int g = it / a.ncb;
-      g0 = a.goffF[g];
-      n = a.goffF[g + 1] - g0;
+      int g, cb;
+      tc_item(a, it, g, cb, g0, n);
       if (tb < n) return;
       it += gridDim.x;
       tb = 0;
@@ -217,7 +240,7 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
   tc::after_sync();
   const uint32_t tm = tslot;
   const uint32_t tacc = tm, ta = tm + 2 * BN;
-  const int nitems = (int)a.c.m[a.F] * a.ncb;
+  const int nitems = (int)a.c.m[a.F] * a.ncb * (a.split > 1 ? a.split : 1);
   // TT_TC_TRACE=2: per-tile %globaltimer stamps, 256 per role and CTA:
   // [0] MMA issued, [1] epilogue has the accumulator, [2] epilogue done,
   // [3] A stage handed over by the loaders
@@ -238,8 +261,8 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
     const int su = (int)(threadIdx.x & 127);  // thread within the set
     uint32_t t = 0, i = 0;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const int g = it / a.ncb, cb = it - g * a.ncb;
-      const int g0 = a.goffF[g], n = a.goffF[g + 1] - g0;
+      int g, cb, g0, n;
+      tc_item(a, it, g, cb, g0, n);
       if (n == 0) continue;
       {  // half of the S block (rows k of the set's half) into S stage i % 2
         const int s = i & 1;
@@ -314,7 +337,7 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
     // one tile: accumulator stage t % 2 -> Psave rows of the tile's nodes
     // (node ids in `mynode`, one per lane, loaded a tile ahead)
     auto drain = [&](uint32_t t, const TileCursor& c, int mynode) {
-      const int cb = c.it % a.ncb;
+      const int cb = c.it % a.ncb;  // (it = (g * split + chunk) * ncb + cb)
       const int nn = min(NPT, c.n - c.tb);
       const int st = t & 1;
       tc::mbar_wait(&c_full[st], (t >> 1) & 1);
@@ -380,8 +403,8 @@ __global__ void __launch_bounds__(TCF_THREADS, 1) k_tc_fwd(FusedArgs a) {
     const uint32_t idesc = tc::idesc_bf16(TC_BM, BN, 0, 1);
     uint32_t t = 0, i = 0;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const int g = it / a.ncb;
-      const int n = a.goffF[g + 1] - a.goffF[g];
+      int g, cb, g0, n;
+      tc_item(a, it, g, cb, g0, n);
       if (n == 0) continue;
       const int s = i & 1;
       tc::mbar_wait(&s_full[s], (i >> 1) & 1);
@@ -445,9 +468,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   __shared__ uint32_t tslot;
 
   if (tt_failed(a.st)) return;
-  const int g = blockIdx.x / a.ncb, cb = blockIdx.x - g * a.ncb;
-  const int g0 = a.goffF[g], g1 = a.goffF[g + 1];
-  if (g0 == g1) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quadrant of this warp
   const int eslice = (warp >> 2) * EC;
@@ -589,7 +611,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   {
     const uint32_t tm = tslot;
     const int col = 32 * (warp & 3) + lane;
-    float* gdst = a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F] + cb * BN + col;
+    float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN + col;
     float v[EC];
     if constexpr (EC == 16) tc::tmem_ld16(tm + lane_base + eslice, v);
     else tc::tmem_ld8(tm + lane_base + eslice, v);
