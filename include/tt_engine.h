@@ -205,6 +205,31 @@ int tt_comm_init_rank(tt_engine* h, const void* unique_id, int rank, int nranks)
 int tt_comm_init(tt_engine* h, void* nccl_comm, int rank, int nranks);
 int tt_allreduce_grads(tt_engine* h, void* stream);
 
+/* NCCL data parallelism, ID-owner sharding (keeps the dedupe that
+ * position sharding loses across ranks): rank r owns the level-F digits
+ * [floor(m_F r / P), floor(m_F (r+1) / P)) of core F = d-2 -- every ID,
+ * level-F prefix and G_F slice with such a digit.
+ *   tt_owner_forward   buckets this rank's batch by owner (stable radix
+ *                      sort), exchanges the IDs (ncclSend/Recv groups), runs
+ *                      the owner's forward on what it received (every prefix
+ *                      once in the job) and sends the rows back to their
+ *                      batch positions.  One host round trip per call: the
+ *                      P x P count matrix the point-to-point calls size from.
+ *                      An out-of-range index on any rank fails the batch on
+ *                      every rank (TT_ERR_INDEX).
+ *   tt_owner_backward  routes the upstream rows to the owners, runs the
+ *                      owner's backward on the forward's plan, and sum
+ *                      all-reduces the replicated cores' gradients (every
+ *                      core but F, with their touch counters); the owned G_F
+ *                      slices and their optimizer state never cross NVLink.
+ *   tt_owner_step      tt_step with the non-finite verdict min-reduced over
+ *                      the ranks first (all apply or all reject).
+ *   tt_owner_rows      IDs this rank received in the last tt_owner_forward. */
+int tt_owner_forward(tt_engine* h, const int64_t* d_indices, int64_t batch, float* d_out, void* stream);
+int tt_owner_backward(tt_engine* h, const float* d_grad_out, void* stream);
+int tt_owner_step(tt_engine* h, void* stream);
+int64_t tt_owner_rows(tt_engine* h);
+
 /* ---- introspection -------------------------------------------------------- */
 /* Distinct prefixes (i_1..i_l), l = 1..d, of the last planned batch
  * (unique_per_level[d-1] = distinct IDs).  Synchronises. */

@@ -166,6 +166,13 @@ class DeviceTT {
   }
   void allreduce_grads(void* stream) { check(tt_allreduce_grads(h_, stream)); }
 
+  // NCCL ID-owner sharding (device buffers, stream-ordered)
+  void owner_forward(const int64_t* d_idx, int64_t B, float* d_out, void* stream) {
+    check(tt_owner_forward(h_, d_idx, B, d_out, stream));
+  }
+  void owner_backward(const float* d_up, void* stream) { check(tt_owner_backward(h_, d_up, stream)); }
+  void owner_step(void* stream) { check(tt_owner_step(h_, stream)); }
+
  private:
   Config cfg_;
   tt_engine* h_ = nullptr;

@@ -24,6 +24,11 @@ struct NcclApi {
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
   decltype(&ncclGetVersion) GetVersion = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
 };
 
 inline const NcclApi& nccl() {
@@ -50,6 +55,11 @@ inline const NcclApi& nccl() {
     TT_NCCL_SYM(AllReduce)
     TT_NCCL_SYM(GetErrorString)
     TT_NCCL_SYM(GetVersion)
+    TT_NCCL_SYM(AllGather)
+    TT_NCCL_SYM(Send)
+    TT_NCCL_SYM(Recv)
+    TT_NCCL_SYM(GroupStart)
+    TT_NCCL_SYM(GroupEnd)
 #undef TT_NCCL_SYM
     api.ok = true;
   });

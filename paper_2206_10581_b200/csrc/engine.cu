@@ -23,6 +23,7 @@
 #include "kernels_fused.cuh"
 #include "kernels_generic.cuh"
 #include "kernels_init.cuh"
+#include "kernels_owner.cuh"
 #include "kernels_plan.cuh"
 #include "kernels_rows.cuh"
 #include "kernels_tcgen05.cuh"
@@ -163,6 +164,24 @@ struct tt_engine {
   cudaStream_t s_comm = nullptr;
   cudaEvent_t ev_gF = nullptr, ev_bwd = nullptr, ev_comm = nullptr;
   bool gF_ready = false;
+
+  // ID-owner sharding (tt_owner_*): the last owner-routed batch
+  struct Owner {
+    int64_t cap = 0, cap_r = 0;
+    unsigned *ka = nullptr, *kb = nullptr;
+    int *va = nullptr, *vb = nullptr;
+    int* perm = nullptr;      // local positions in owner order (va or vb)
+    int64_t* sid = nullptr;   // local IDs in owner order
+    int* d_counts = nullptr;  // [P] local IDs per owner
+    int* d_all = nullptr;     // [P][P] all ranks' counts
+    unsigned long long* d_gbad = nullptr;
+    int* h_all = nullptr;     // pinned [P][P] + 2 ints of the global bad position
+    int64_t* rid = nullptr;   // received IDs (owner side)
+    float *rout = nullptr, *back = nullptr, *sup = nullptr, *rup = nullptr;
+    std::vector<int64_t> soff, roff, send, recv;
+    int64_t B = 0, Bown = 0;
+    bool valid = false;
+  } ow;
 
   // TMA tensor maps of the cores for the fused forward (level k -> [m_k R_k] x
   // [n_k R_{k+1}] fp32 view of core k, box {128, R_k})
@@ -1297,6 +1316,12 @@ void tt_engine_destroy(tt_engine* h) {
     for (cudaEvent_t e : {sl.ev_idx, sl.ev_up, sl.ev_fwd, sl.ev_done, sl.ev_out})
       if (e) cudaEventDestroy(e);
   }
+  {
+    auto& o = h->ow;
+    void* ptrs2[] = {o.ka, o.kb, o.va, o.vb, o.sid, o.d_counts, o.d_all, o.d_gbad, o.rid, o.rout, o.back, o.sup, o.rup};
+    for (void* p : ptrs2) cudaFree(p);
+    if (o.h_all) cudaFreeHost(o.h_all);
+  }
   if (h->own) cudaStreamDestroy(h->own);
   if (h->s_comm) { cudaStreamSynchronize(h->s_comm); cudaStreamDestroy(h->s_comm); }
   for (cudaEvent_t e : {h->ev_gF, h->ev_bwd, h->ev_comm})
@@ -1619,10 +1644,19 @@ int tt_backward(tt_engine* h, const int64_t* d_idx, int64_t B, const float* d_up
   return do_backward(h, d_up, s);
 }
 
+static int step_impl(tt_engine* h, cudaStream_t s, bool global_reject);
+
 int tt_step(tt_engine* h, void* stream) {
   if (!h) return fail(TT_ERR_ARG, "tt_step: null handle");
   CU(cudaSetDevice(h->device));
-  cudaStream_t s = (cudaStream_t)stream;
+  return step_impl(h, (cudaStream_t)stream, false);
+}
+
+// the update kernels; global_reject: the non-finite check's verdict is
+// min-reduced over the communicator before any core changes, so every rank
+// applies or rejects the step together (owner sharding: a rank's gradient
+// covers its own G_F slices only)
+static int step_impl(tt_engine* h, cudaStream_t s, bool global_reject) {
   const DevCfg& c = h->dc;
   Phase ph(h, 4, s);
   LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 2);
@@ -1630,6 +1664,10 @@ int tt_step(tt_engine* h, void* stream) {
   for (int k = 0; k < c.d; ++k) vec4 = vec4 && c.core_off[k] % 4 == 0 && c.slice[k] % 4 == 0;
   const int64_t work = vec4 ? c.nparams / 4 : c.nparams;
   LAUNCH(k_check_finite, grid_for(work), 256, 0, s, c, h->grads, vec4 ? 1 : 0, h->st);
+  if (global_reject && h->comm) {
+    const ncclResult_t r = nccl().AllReduce(&h->st->bad_core, &h->st->bad_core, 1, ncclInt32, ncclMin, h->comm, s);
+    if (r != ncclSuccess) return fail(TT_ERR_CUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+  }
   const float lr = (float)h->lr, b1 = (float)h->beta1, b2 = (float)h->beta2, ep = (float)h->eps;
   if (h->opt_kind == TT_OPT_SGD)
     LAUNCH(k_update<0>, grid_for(work), 256, 0, s, c, h->params, h->grads, h->s1, h->s2, vec4 ? 1 : 0, lr, b1, b2,
@@ -1950,6 +1988,189 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const fl
 }
 
 void* tt_engine_stream(tt_engine* h) { return h ? (void*)h->own : nullptr; }
+
+// ---- ID-owner sharding over the handle's NCCL communicator ------------------
+namespace {
+int owner_alloc(tt_engine* h, int64_t B) {
+  auto& o = h->ow;
+  const int P = h->nranks;
+  const int64_t N = h->dc.emb_dim;
+  if (!o.d_counts) {
+    CU(dalloc(&o.d_counts, P));
+    CU(dalloc(&o.d_all, (int64_t)P * P));
+    CU(dalloc(&o.d_gbad, 1));
+    CU(cudaMallocHost(&o.h_all, sizeof(int) * ((size_t)P * P + 2)));
+  }
+  if (o.cap < B) {
+    void* ptrs[] = {o.ka, o.kb, o.va, o.vb, o.sid, o.back, o.sup};
+    for (void* p : ptrs) cudaFree(p);
+    o.ka = o.kb = nullptr; o.va = o.vb = nullptr; o.sid = nullptr; o.back = o.sup = nullptr; o.cap = 0;
+    CU(dalloc(&o.ka, B)); CU(dalloc(&o.kb, B)); CU(dalloc(&o.va, B)); CU(dalloc(&o.vb, B));
+    CU(dalloc(&o.sid, B)); CU(dalloc(&o.back, B * N)); CU(dalloc(&o.sup, B * N));
+    o.cap = B;
+  }
+  return TT_OK;
+}
+
+int owner_recv_alloc(tt_engine* h, int64_t R) {
+  auto& o = h->ow;
+  if (o.cap_r >= R) return TT_OK;
+  const int64_t N = h->dc.emb_dim;
+  cudaFree(o.rid); cudaFree(o.rout); cudaFree(o.rup);
+  o.rid = nullptr; o.rout = o.rup = nullptr; o.cap_r = 0;
+  CU(dalloc(&o.rid, R)); CU(dalloc(&o.rout, R * N)); CU(dalloc(&o.rup, R * N));
+  o.cap_r = R;
+  return TT_OK;
+}
+
+// grouped point-to-point exchange: send counts[p] elements at offsets soff to
+// every p, receive rcounts[p] at roff (elem = `width` values of `type`)
+int owner_exchange(tt_engine* h, const void* sbuf, const std::vector<int64_t>& soff, const std::vector<int64_t>& scnt,
+                   void* rbuf, const std::vector<int64_t>& roff, const std::vector<int64_t>& rcnt, size_t esize,
+                   int64_t width, ncclDataType_t type, cudaStream_t s) {
+  const auto& api = nccl();
+  ncclResult_t r = api.GroupStart();
+  for (int p = 0; p < h->nranks && r == ncclSuccess; ++p) {
+    if (scnt[p]) r = api.Send((const char*)sbuf + soff[p] * width * esize, (size_t)(scnt[p] * width), type, p, h->comm, s);
+    if (r == ncclSuccess && rcnt[p])
+      r = api.Recv((char*)rbuf + roff[p] * width * esize, (size_t)(rcnt[p] * width), type, p, h->comm, s);
+  }
+  const ncclResult_t e = api.GroupEnd();
+  if (r != ncclSuccess || e != ncclSuccess)
+    return fail(TT_ERR_CUDA, std::string("owner exchange: ") + api.GetErrorString(r != ncclSuccess ? r : e));
+  return TT_OK;
+}
+}  // namespace
+
+int tt_owner_forward(tt_engine* h, const int64_t* d_idx, int64_t B, float* d_out, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_owner_forward: null handle");
+  if (!h->comm) return fail(TT_ERR_STATE, "tt_owner_forward: no communicator (tt_comm_init first)");
+  if (B < 0 || B > INT_MAX / 2) return fail(TT_ERR_ARG, "tt_owner_forward: batch size out of range");
+  if (B > 0 && (!d_idx || !d_out)) return fail(TT_ERR_ARG, "tt_owner_forward: null device buffer");
+  if (h->dc.emb_dim % 4) return fail(TT_ERR_ARG, "tt_owner_forward: emb_dim must be a multiple of 4");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  auto& o = h->ow;
+  o.valid = false;
+  const int P = h->nranks, F = std::max(h->dc.d - 2, 0);
+  int rc = ensure_plan(h, std::max<int64_t>(B, 1));  // (the radix sort's histogram slots)
+  if (rc) return rc;
+  rc = owner_alloc(h, std::max<int64_t>(B, 1));
+  if (rc) return rc;
+  const int64_t N = h->dc.emb_dim;
+  LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 1);
+  if (B > 0) {
+    LAUNCH(k_owner_of, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, h->dc, F, P, h->rank, o.ka, o.va, h->st);
+    const int nbits = std::max<int>(1, (int)bitlen((uint64_t)(P - 1)));
+    unsigned* sk = radix_sort<unsigned>(h, s, o.ka, o.va, o.kb, o.vb, nullptr, (int)B, B, nbits, &o.perm);
+    LAUNCH(k_owner_counts, 1, 32 * ((P + 31) / 32), 0, s, (const unsigned*)sk, (int)B, P, o.d_counts);
+  } else {
+    CU(cudaMemsetAsync(o.d_counts, 0, sizeof(int) * P, s));
+  }
+  const auto& api = nccl();
+  ncclResult_t r = api.AllGather(o.d_counts, o.d_all, (size_t)P, ncclInt32, h->comm, s);
+  if (r == ncclSuccess) r = api.AllReduce(&h->st->bad_pos, o.d_gbad, 1, ncclUint64, ncclMin, h->comm, s);
+  if (r != ncclSuccess) return fail(TT_ERR_CUDA, std::string("owner counts: ") + api.GetErrorString(r));
+  // the one host round trip of a routed step: NCCL's point-to-point calls take
+  // host-side counts (the P x P matrix, 4 P^2 bytes)
+  CU(cudaMemcpyAsync(o.h_all, o.d_all, sizeof(int) * P * P, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(o.h_all + P * P, o.d_gbad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  unsigned long long gbad;
+  memcpy(&gbad, o.h_all + P * P, sizeof(gbad));
+  if (gbad != TT_NO_POS) {
+    DevStatus st;
+    CU(cudaMemcpy(&st, h->st, sizeof(st), cudaMemcpyDeviceToHost));
+    LAUNCH(k_reset_status, 1, 1, 0, s, h->st, 1);
+    CU(cudaStreamSynchronize(s));
+    if (st.bad_pos != TT_NO_POS) {
+      int64_t val = 0;
+      cudaMemcpy(&val, d_idx + st.bad_pos, sizeof(val), cudaMemcpyDeviceToHost);
+      return fail(TT_ERR_INDEX,
+                  "lookup_batch: index " + std::to_string(val) + " at batch position " +
+                      std::to_string((long long)st.bad_pos) + " out of [0, " + std::to_string(h->dc.num_nodes) + ")",
+                  (int64_t)st.bad_pos, val);
+    }
+    return fail(TT_ERR_INDEX, "lookup_batch: an index out of range on another rank; batch rejected", -1, 0);
+  }
+  o.send.assign(P, 0); o.recv.assign(P, 0); o.soff.assign(P + 1, 0); o.roff.assign(P + 1, 0);
+  for (int p = 0; p < P; ++p) {
+    o.send[p] = o.h_all[h->rank * P + p];
+    o.recv[p] = o.h_all[p * P + h->rank];
+    o.soff[p + 1] = o.soff[p] + o.send[p];
+    o.roff[p + 1] = o.roff[p] + o.recv[p];
+  }
+  o.B = B;
+  o.Bown = o.roff[P];
+  rc = owner_recv_alloc(h, std::max<int64_t>(o.Bown, 1));
+  if (rc) return rc;
+  if (B > 0) LAUNCH(k_gather_ids, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, (const int*)o.perm, (int)B, o.sid);
+  rc = owner_exchange(h, o.sid, o.soff, o.send, o.rid, o.roff, o.recv, sizeof(int64_t), 1, ncclInt64, s);
+  if (rc) return rc;
+  if (o.Bown > 0) {
+    rc = do_forward(h, o.rid, o.Bown, o.rout, s, true);
+    if (rc) return rc;
+  } else {
+    h->plan_valid = false;
+  }
+  // rows back to the ranks that asked, then to their batch positions
+  rc = owner_exchange(h, o.rout, o.roff, o.recv, o.back, o.soff, o.send, sizeof(float), N, ncclFloat32, s);
+  if (rc) return rc;
+  if (B > 0)
+    LAUNCH(k_permute_rows<true>, grid_for(B * 32, 256, 148 * 8), 256, 0, s, (const float*)o.back, (const int*)o.perm,
+           (int)B, N, d_out);
+  o.valid = true;
+  CU(cudaGetLastError());
+  return TT_OK;
+}
+
+int tt_owner_backward(tt_engine* h, const float* d_up, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_owner_backward: null handle");
+  auto& o = h->ow;
+  if (!h->comm || !o.valid) return fail(TT_ERR_STATE, "tt_owner_backward: no matching tt_owner_forward");
+  if (o.B > 0 && !d_up) return fail(TT_ERR_ARG, "tt_owner_backward: null upstream buffer");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t N = h->dc.emb_dim;
+  const DevCfg& c = h->dc;
+  if (o.B > 0)
+    LAUNCH(k_permute_rows<false>, grid_for(o.B * 32, 256, 148 * 8), 256, 0, s, d_up, (const int*)o.perm, (int)o.B, N,
+           o.sup);
+  int rc = owner_exchange(h, o.sup, o.soff, o.send, o.rup, o.roff, o.recv, sizeof(float), N, ncclFloat32, s);
+  if (rc) return rc;
+  if (o.Bown > 0) {
+    if (!h->plan_valid || h->plan_version != h->cores_version)
+      return fail(TT_ERR_STATE, "tt_owner_backward: the cores changed since tt_owner_forward");
+    rc = do_backward(h, o.rup, s);
+    if (rc) return rc;
+  } else {  // nothing owned this step: CoreGradients::zeros (autodiff.cpp:40-46)
+    CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(c.nparams + h->ntc), s));
+    h->batch_count = 0;
+  }
+  // the replicated cores' gradients (every core but F, and their touch
+  // counters) are summed over the ranks; the owned G_F slices never move
+  const int F = std::max(c.d - 2, 0);
+  const int64_t g0 = c.core_off[F], g1 = c.core_off[F] + c.m[F] * c.slice[F];
+  const int64_t t0 = c.tc_off[F], t1 = c.tc_off[F] + c.m[F], tend = c.nparams + h->ntc;
+  const int64_t spans[3][2] = {{0, g0}, {g1, t0}, {t1, tend}};
+  for (auto& sp : spans) {
+    if (sp[1] <= sp[0]) continue;
+    const ncclResult_t r =
+        nccl().AllReduce(h->grads + sp[0], h->grads + sp[0], (size_t)(sp[1] - sp[0]), ncclFloat32, ncclSum, h->comm, s);
+    if (r != ncclSuccess) return fail(TT_ERR_CUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+  }
+  CU(cudaGetLastError());
+  return TT_OK;
+}
+
+int tt_owner_step(tt_engine* h, void* stream) {
+  if (!h) return fail(TT_ERR_ARG, "tt_owner_step: null handle");
+  if (!h->comm) return fail(TT_ERR_STATE, "tt_owner_step: no communicator");
+  CU(cudaSetDevice(h->device));
+  return step_impl(h, (cudaStream_t)stream, true);
+}
+
+int64_t tt_owner_rows(tt_engine* h) { return h ? h->ow.Bown : -1; }
 
 int tt_grad_buffer(tt_engine* h, float** d_ptr, int64_t* count) {
   if (!h || !d_ptr || !count) return fail(TT_ERR_ARG, "tt_grad_buffer: null argument");

@@ -255,6 +255,17 @@ class OwnerShardedTT:
         self.rank = dist.get_rank(group)
         self.bounds = owner_bounds(cfg, self.world)
         self.segments = replicated_segments(cfg)
+        # Under the NCCL backend the data plane is the engine's own
+        # (tt_owner_forward / _backward / _step over its communicator): no torch
+        # ops on the rows; torch.distributed ships only the 128-byte NCCL id
+        self.native = (comm is None and group is None and dist.is_initialized()
+                       and dist.get_backend() == "nccl")
+        if self.native:
+            obj = [emb_nccl_id() if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            emb.comm_init_rank(obj[0], self.rank, self.world)
+            self.buf = None
+            return
         self.buf = torch.zeros(grad_buffer_len(cfg), dtype=torch.float32, device=f"cuda:{emb.device}")
         emb.bind_grad_buffer(self.buf)
         emb.set_dense_grads(True)
@@ -271,6 +282,8 @@ class OwnerShardedTT:
 
     def forward(self, indices, out=None):
         import torch
+        if self.native:
+            return self.emb.owner_forward(indices, out)
         cfg = self.emb.config
         recv, self._route = route_to_owners(cfg, indices, self.group, self.dist)
         self._recv_idx = recv
@@ -279,6 +292,9 @@ class OwnerShardedTT:
         return route_back(rows, self._route, out, self.group, self.dist)
 
     def backward(self, grad_out):
+        if self.native:
+            self.emb.owner_backward(grad_out)
+            return
         if self._route is None:
             raise RuntimeError("OwnerShardedTT.backward: no forward on this rank")
         up = route_rows(grad_out, self._route, self.group, self.dist)
@@ -298,6 +314,9 @@ class OwnerShardedTT:
         self.buf.index_copy_(0, self._pack_idx, self._pack)
 
     def step(self):
+        if self.native:
+            self.emb.owner_step()
+            return
         self.allreduce()
         self.emb.step()
 

@@ -60,6 +60,7 @@ SYMBOLS = [
     "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_opt_set_hparams", "tt_debug_trace", "tt_set_permutation",
     "tt_ortho_cores_f64", "tt_nccl_unique_id", "tt_comm_init_rank", "tt_comm_init", "tt_allreduce_grads",
     "tt_train_step_submit", "tt_train_step_wait", "tt_engine_stream",
+    "tt_owner_forward", "tt_owner_backward", "tt_owner_step", "tt_owner_rows",
 ]
 
 
@@ -104,6 +105,8 @@ def load_library(build_if_missing: bool = True):
         "tt_comm_init": (i32, [vp, vp, i32, i32]), "tt_allreduce_grads": (i32, [vp, vp]),
         "tt_train_step_submit": (i32, [vp, vp, i64, vp, vp]), "tt_train_step_wait": (i32, [vp]),
         "tt_engine_stream": (vp, [vp]),
+        "tt_owner_forward": (i32, [vp, vp, i64, vp, vp]), "tt_owner_backward": (i32, [vp, vp, vp]),
+        "tt_owner_step": (i32, [vp, vp]), "tt_owner_rows": (i64, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -478,6 +481,35 @@ class TTEmbedding:
         same 128-byte id from nccl_unique_id())."""
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _raise(self._lib.tt_comm_init_rank(self._h, buf, rank, world), "tt_comm_init_rank")
+
+    def owner_forward(self, indices, out=None):
+        """ID-owner-sharded forward over the NCCL communicator (tt_owner_forward):
+        this rank's batch in, its rows out (in batch order)."""
+        torch = _torch()
+        if indices.dtype != torch.int64 or not indices.is_cuda or not indices.is_contiguous():
+            raise InvalidArgument("owner_forward: indices must be a contiguous int64 CUDA tensor")
+        self._check_device(indices, "owner_forward: indices")
+        B = indices.numel()
+        if out is None:
+            out = torch.empty((B, self.config.emb_dim), dtype=torch.float32, device=indices.device)
+        _raise(self._lib.tt_owner_forward(self._h, C.c_void_p(indices.data_ptr()), B, C.c_void_p(out.data_ptr()),
+                                          self._stream()), "tt_owner_forward")
+        return out
+
+    def owner_backward(self, grad_out) -> None:
+        torch = _torch()
+        if grad_out.dtype != torch.float32 or not grad_out.is_cuda or not grad_out.is_contiguous():
+            raise InvalidArgument("owner_backward: grad_out must be a contiguous float32 CUDA tensor")
+        self._check_device(grad_out, "owner_backward: grad_out")
+        _raise(self._lib.tt_owner_backward(self._h, C.c_void_p(grad_out.data_ptr()), self._stream()),
+               "tt_owner_backward")
+        self._grad_version += 1
+
+    def owner_step(self) -> None:
+        _raise(self._lib.tt_owner_step(self._h, self._stream()), "tt_owner_step")
+
+    def owner_rows(self) -> int:
+        return int(self._lib.tt_owner_rows(self._h))
 
     def allreduce_grads(self) -> None:
         """Sum all-reduce of the gradient buffer over the communicator,

@@ -76,3 +76,47 @@ def test_native_nccl_step_equals_single_engine(nccl_world1, name, path):
     np.testing.assert_array_equal(outs[0], outs[1])
     for a, b in zip(cs[0], cs[1]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,path", [("products", "auto"), ("papers", "auto"), ("billion", "auto"), ("papers", "tc")])
+def test_native_owner_step_equals_single_engine(nccl_world1, name, path):
+    """tt_owner_forward / _backward / _step (ID-owner sharding in the engine,
+    NCCL point-to-point routing) on a 1-rank communicator == the plain step,
+    bit for bit; an out-of-range index fails the routed batch."""
+    import torch
+    from paper_2206_10581_b200 import config as Cf
+    from paper_2206_10581_b200 import engine as E
+    from paper_2206_10581_b200.dist import OwnerShardedTT
+    cfg = C.WORKLOADS[name]["cfg"]()
+    B = 4096
+    idx = torch.tensor(synth.zipf_ids(13, B, 1.1, cfg.num_nodes), device="cuda")
+    up = torch.tensor(synth.normal(14, 1, B * cfg.emb_dim).reshape(B, cfg.emb_dim), device="cuda")
+    cores = synth.gaussian_cores(cfg, 15)
+    kind = getattr(E.OptKind, C.WORKLOADS[name]["opt"])
+    res = []
+    for native in (False, True):
+        emb = E.TTEmbedding(cfg, 0)
+        emb.set_cores(cores)
+        emb.set_path(path)
+        emb.configure_optimizer(E.OptimizerState.make(cfg, kind, 0.01))
+        if native:
+            dp = OwnerShardedTT(emb)
+            assert dp.native
+            o = dp.forward(idx)
+            assert emb.owner_rows() == B
+            dp.backward(up)
+            dp.step()
+        else:
+            o = emb.forward(idx)
+            emb.backward(up)
+            emb.step()
+        emb.sync()
+        res.append((o.cpu().numpy(), emb.get_cores(np.float32)))
+        if native:
+            bad = idx.clone()
+            bad[7] = cfg.num_nodes
+            with pytest.raises(Cf.OutOfRange, match="position 7"):
+                dp.forward(bad)
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        np.testing.assert_array_equal(a, b)
