@@ -665,6 +665,17 @@ bool bwdk32_enabled(int rp) {
   return (rp == 4 && (mask & 1)) || (rp == 16 && (mask & 2));
 }
 
+// TT_BWDWS = bit mask of the level-F shapes using the warp-specialised
+// backward (1: K = 32 with RP = 16, 2: K = 32 with RP = 4; default 1); 0
+// selects k_fused_bwd_k32 / k_fused_bwd
+bool bwdws_enabled(int K, int RP) {
+  static const int mask = [] {
+    const char* e = getenv("TT_BWDWS");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return K == 32 && ((RP == 16 && (mask & 1)) || (RP == 4 && (mask & 2)));
+}
+
 int split_rows_env(bool fwd, int dflt) {
   static const int f = [] { const char* e = getenv("TT_SPLIT_ROWS_FWD"); return e && *e ? atoi(e) : 0; }();
   static const int b = [] { const char* e = getenv("TT_SPLIT_ROWS_BWD"); return e && *e ? atoi(e) : 0; }();
@@ -726,6 +737,18 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
       h->F.cap_gsplit = need;
     }
     a.gsplit = h->F.gsplit;
+  }
+  if (!fwd && f.BN == 128 && a.mode == 0 && bwdws_enabled(f.K, f.RP)) {
+#define BWDWS_CASE(k_, rp_, nl_)                                                                 \
+  if (f.K == k_ && f.RP == rp_ && f.NL == nl_) {                                                 \
+    FUSED_LAUNCH_T((k_fused_bwd_ws<k_, rp_, nl_>), bwd_ws_smem(k_), grid, WsRoles<k_>::T, s, a);  \
+    if (a.split > 1)                                                                             \
+      LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
+             a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
+    return TT_OK;                                                                                \
+  }
+    TT_BWDWS_SHAPES(BWDWS_CASE)
+#undef BWDWS_CASE
   }
   if (!fwd && f.K == 32 && f.BN == 128 && bwdk32_enabled(f.RP)) {
 #define BWDK32_CASE(rp_, nl_)                                                                    \

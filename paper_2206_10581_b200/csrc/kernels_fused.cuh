@@ -880,6 +880,263 @@ inline size_t bwd_k32_smem() {
 // variant measured slower than k_fused_bwd, profiles/r02/NOTES.md)
 #define TT_BWDK32_SHAPES(X) X(16, 4)
 
+// ---------------------------------------------------------------------------
+// Warp-specialised rank-32 backward (billion's level F).  The profile of
+// k_fused_bwd_k32 puts ~21% of its stall samples on the dC formation's L2
+// loads (last-core slices, upstream rows) and ~12% on the barriers around it:
+// every warp waited for the slowest warp's dC before the GEMMs could start.
+// Here dC and the A tile are produced one tile ahead into double buffers:
+//   warps 0-3 (producers): A tile by cp.async + dC (16 rows each) -> buffer t%2,
+//     then bar.arrive FULL[t%2]; before reusing a buffer they bar.sync on
+//     EMPTY[t%2] (the consumers' release of tile t-2);
+//   warps 4-5: dG_F += A^T dC (8 x 8 tiles, persistent), warps 6-7: dA (8 x 4),
+//     each bar.sync FULL[t%2] -> GEMM -> bar.arrive EMPTY[t%2].
+// Named barriers 1-2 (FULL) and 3-4 (EMPTY), 256 threads each.
+constexpr int WS_THREADS = 256, WS_NB = 256;
+
+template <int ID, int N>
+__device__ __forceinline__ void named_sync() { asm volatile("bar.sync %0, %1;\n" ::"n"(ID), "n"(N) : "memory"); }
+template <int ID, int N>
+__device__ __forceinline__ void named_arrive() { asm volatile("bar.arrive %0, %1;\n" ::"n"(ID), "n"(N) : "memory"); }
+// barrier (base + buf) with a run-time buffer index 0 / 1
+template <int BASE, int N>
+__device__ __forceinline__ void named_sync2(int buf) { if (buf) named_sync<BASE + 1, N>(); else named_sync<BASE, N>(); }
+template <int BASE, int N>
+__device__ __forceinline__ void named_arrive2(int buf) { if (buf) named_arrive<BASE + 1, N>(); else named_arrive<BASE, N>(); }
+
+// dC rows m0..m0+7 (one node: RP % 8 == 0) x the lane's 4 columns: per ID
+// all twelve loads (4 slice rows + 8 upstream rows) are issued before the FMAs
+template <int K, int RP, int NL>
+__device__ __forceinline__ void form_dC8(const FusedArgs& a, int tb, int nn, int cb, const int* s_pref,
+                                         const int* s_cs0, const int* s_bd, float* Ds, int m0, int lane) {
+  constexpr int BN = 128;
+  const int j = m0 / RP;
+  float dacc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) dacc[i][t] = 0.f;
+  if (j < nn) {
+    const int ar0 = m0 - j * RP;
+    const int fA = s_pref[tb + j], fB = s_pref[tb + j + 1], cs0 = s_cs0[tb + j];
+    const int colg = cb * BN + lane * 4, r0 = colg % K, jf = colg / K;
+    const int nF = a.nF;
+    const int64_t npad = a.c.npad;
+    const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+    const int64_t sliceL = a.c.slice[a.c.d - 1];
+    for (int f = fA; f < fB; ++f) {
+      const int u = cs0 + (f - fA);
+      const float* Gp = Gl + (int64_t)(f < FB_IDS ? s_bd[f] : __ldg(a.digitL + u)) * sliceL;
+      const float* Yp = a.dY + (int64_t)u * npad + ((int64_t)ar0 * nF + jf) * NL;
+#pragma unroll
+      for (int l4 = 0; l4 < NL; l4 += 4) {
+        float4 gv[4], y[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) gv[t] = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) y[ii] = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)ii * nF * NL + l4));
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float x = dacc[ii][t];
+            x = fmaf(y[ii].x, gv[t].x, x);
+            x = fmaf(y[ii].y, gv[t].y, x);
+            x = fmaf(y[ii].z, gv[t].z, x);
+            x = fmaf(y[ii].w, gv[t].w, x);
+            dacc[ii][t] = x;
+          }
+      }
+    }
+  }
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii)
+    *reinterpret_cast<float4*>(Ds + (m0 + ii) * BN + lane * 4) = make_float4(dacc[ii][0], dacc[ii][1], dacc[ii][2], dacc[ii][3]);
+}
+
+struct WsSmem {
+  float *Bs, *As0, *Ds0;
+  int64_t* s_aoff;
+  int *s_node, *s_cs0, *s_pref, *s_wsum, *s_bd;
+};
+
+// the batch prologue every role runs in step (prep_nodes' barriers + the
+// digit staging barrier: the same __syncthreads sequence in both roles)
+template <int T>
+__device__ __forceinline__ void ws_batch_prologue(const FusedArgs& a, const WsSmem& m, int nb0, int nbn) {
+  prep_nodes<T>(a, nb0, nbn, m.s_node, m.s_cs0, m.s_pref, m.s_aoff, m.s_wsum);
+  const int tot = min(m.s_pref[nbn], FB_IDS);
+  for (int f = threadIdx.x; f < tot; f += T) {
+    int lo = 0, hi = nbn - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (m.s_pref[mid] <= f) lo = mid; else hi = mid - 1;
+    }
+    m.s_bd[f] = __ldg(a.digitL + m.s_cs0[lo] + (f - m.s_pref[lo]));
+  }
+  __syncthreads();
+}
+
+// thread counts of the warp-specialised backward: 4 producer warps, then the
+// dG_F warps (8 x 8 tiles over K x 128) and the dA warps (8 x 4 tiles over
+// 64 x K)
+template <int K>
+struct WsRoles {
+  static constexpr int PROD = 128, DG = K * 128 / 64, DA = FB_BM * K / 32, T = PROD + DG + DA;
+};
+
+template <int K, int RP, int NL>
+__device__ __forceinline__ void ws_producer(const FusedArgs& a, const WsSmem& m, int g0, int g1, int cb) {
+  constexpr int BM = FB_BM, BN = 128, NPT = BM / RP, NB = WS_NB, T = WsRoles<K>::T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int nb0 = g0; nb0 < g1; nb0 += NB) {
+    const int nbn = min(NB, g1 - nb0);
+    ws_batch_prologue<T>(a, m, nb0, nbn);
+    const int TT = (nbn + NPT - 1) / NPT;
+    for (int t = 0; t < TT; ++t) {
+      const int buf = t & 1, tb = t * NPT, nn = min(NPT, nbn - tb);
+      if (t >= 2) named_sync2<3, T>(buf);  // the consumers released tile t - 2
+      load_A_tile<K, RP, 128>(a, tb, nn, m.s_aoff, m.As0 + buf * BM * K);
+      cp_async_commit();
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        if constexpr (RP % 8 == 0)
+          form_dC8<K, RP, NL>(a, tb, nn, cb, m.s_pref, m.s_cs0, m.s_bd, m.Ds0 + buf * BM * BN, warp * 16 + q * 8, lane);
+        else
+          form_dC<K, BN, RP, NL>(a, tb, nn, cb, m.s_pref, m.s_cs0, m.s_bd, m.Ds0 + buf * BM * BN, warp * 16 + q * 8);
+      }
+      cp_async_wait<0>();  // the A tile (and this thread's share of the slice block)
+      named_arrive2<1, T>(buf);
+    }
+    for (int t = TT < 2 ? 2 : TT; t < TT + 2; ++t) named_sync2<3, T>(t & 1);  // the last releases
+    __syncthreads();  // the batch's node metadata is rewritten by the next prologue
+  }
+}
+
+template <int K, int RP, int NL>
+__device__ __forceinline__ void ws_consumer(const FusedArgs& a, const WsSmem& m, int g0, int g1, int g, int cb,
+                                            int chunk) {
+  constexpr int BM = FB_BM, BN = 128, SB = BN + 4, NPT = BM / RP, NB = WS_NB;
+  using R = WsRoles<K>;
+  constexpr int T = R::T, KG = K / 4;
+  const int tc = threadIdx.x - R::PROD;
+  const bool gw = tc < R::DG;                                    // dG role
+  const int kb = (tc >> 4) * 8, c0 = (tc & 15) * 4;             // dG role
+  const int t2 = tc - R::DG, mg8 = (t2 / KG) * 8, kg = t2 % KG;  // dA role: k = kg + KG j
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  cp_async_wait<0>();  // this thread's share of the slice block
+  for (int nb0 = g0; nb0 < g1; nb0 += NB) {
+    const int nbn = min(NB, g1 - nb0);
+    ws_batch_prologue<T>(a, m, nb0, nbn);
+    const int TT = (nbn + NPT - 1) / NPT;
+    for (int t = 0; t < TT; ++t) {
+      const int buf = t & 1, tb = t * NPT, nn = min(NPT, nbn - tb), mlim = nn * RP;
+      const float* As = m.As0 + buf * BM * K;
+      const float* Ds = m.Ds0 + buf * BM * BN;
+      named_sync2<1, T>(buf);
+      if (gw) {
+#pragma unroll 2
+        for (int mm = 0; mm < BM; ++mm) {
+          if (mm >= mlim) break;
+          const float4 a0 = *reinterpret_cast<const float4*>(As + mm * K + kb);
+          const float4 a1 = *reinterpret_cast<const float4*>(As + mm * K + kb + 4);
+          const float4 d0 = *reinterpret_cast<const float4*>(Ds + mm * BN + c0);
+          const float4 d1 = *reinterpret_cast<const float4*>(Ds + mm * BN + 64 + c0);
+          const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+          const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], dv[j], acc[i][j]);
+        }
+      } else if (mg8 < mlim) {
+        // (the dA tile reuses the accumulator array: dA threads hold no dG_F)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+        for (int n = 0; n < BN; n += 4) {
+          float4 cv[8], bv[4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg8 + i) * BN + n);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const float4*>(m.Bs + (kg + KG * j) * SB + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc[i][j] = fmaf(cv[i].x, bv[j].x, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].y, bv[j].y, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].z, bv[j].z, acc[i][j]);
+              acc[i][j] = fmaf(cv[i].w, bv[j].w, acc[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int mm = mg8 + i;
+          const int j = mm / RP;
+          if (j >= nn) continue;
+          float* dst = a.dPc + ((int64_t)m.s_node[tb + j] * a.ncb + cb) * RP * K + (mm - j * RP) * K;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) dst[kg + KG * jj] = acc[i][jj];
+        }
+      }
+      named_arrive2<3, T>(buf);
+    }
+    __syncthreads();  // (matches the producers' end-of-batch barrier)
+  }
+  if (gw) {  // the group's (chunk's) dG_F column block
+    float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float* row = gdst + (int64_t)(kb + i) * a.NC;
+      *reinterpret_cast<float4*>(row + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      *reinterpret_cast<float4*>(row + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+  }
+}
+
+template <int K, int RP, int NL>
+__global__ void __launch_bounds__(WsRoles<K>::T, K <= 32 ? 2 : 1) k_fused_bwd_ws(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int BN = 128, BM = FB_BM, SB = BN + 4, NB = WS_NB;
+  static_assert(K == 32 || K == 64, "warp-specialised backward: K = 32 / 64");
+  extern __shared__ __align__(16) float smem[];
+  WsSmem m;
+  m.Bs = smem;                       // [K][SB]
+  m.As0 = m.Bs + K * SB;             // [2][BM][K]
+  m.Ds0 = m.As0 + 2 * BM * K;        // [2][BM][BN]
+  m.s_aoff = reinterpret_cast<int64_t*>(m.Ds0 + 2 * BM * BN);
+  m.s_node = reinterpret_cast<int*>(m.s_aoff + NB);
+  m.s_cs0 = m.s_node + NB;
+  m.s_pref = m.s_cs0 + NB;
+  m.s_wsum = m.s_pref + NB + 4;
+  m.s_bd = m.s_wsum + 16;  // [FB_IDS]
+  if (tt_failed(a.st)) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
+  load_slice_block<K, BN, SB, WsRoles<K>::T>(a, g, cb, m.Bs);
+  cp_async_commit();
+  if (threadIdx.x < WsRoles<K>::PROD) ws_producer<K, RP, NL>(a, m, g0, g1, cb);
+  else ws_consumer<K, RP, NL>(a, m, g0, g1, g, cb, chunk);
+}
+
+inline size_t bwd_ws_smem(int K) {
+  return sizeof(float) * ((size_t)K * 132 + 2 * FB_BM * K + 2 * FB_BM * 128) + sizeof(int64_t) * WS_NB +
+         sizeof(int) * (3 * WS_NB + 12 + 16 + FB_IDS) + 16;
+}
+
+// (K, RP, NL) instantiations of k_fused_bwd_ws (billion's level F; products /
+// sweep32).  At K = 64 (one 384-thread CTA per SM) it measured slower than
+// k_fused_bwd: papers 1.204 -> 1.283 ms, sweep64 0.468 -> 0.589 ms.
+#define TT_BWDWS_SHAPES(X) X(32, 16, 4) X(32, 4, 8)
+
 // Streaming kernels over the saved P_F, one warp per distinct ID
 // (grid-stride).  The ID's prefix block P_F[p] (RP x NC floats, contiguous)
 // is staged into the warp's shared buffer with coalesced 16-byte loads (all
