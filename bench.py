@@ -397,7 +397,8 @@ def main():
         torch.cuda.synchronize()
         phase_ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
         return {"t_max": t_max, "per_step": per_step, "launches": launches, "phase_ms": phase_ms,
-                "path": emb.last_path(), "graph": graph is not None}
+                "path": emb.last_path(), "graph": graph is not None,
+                "kernels": {"fwd": emb.main_kernel(False), "bwd": emb.main_kernel(True)}}
 
     props = torch.cuda.get_device_properties(local)
     uuid = getattr(props, "uuid", None)
@@ -468,9 +469,10 @@ def main():
     uf_cf = U[-2] * costs[-2] if len(costs) >= 2 else 0
     ud_cd = U[-1] * costs[-1]
     if fused:
-        dom = "k_fused_bwd" if phase_ms["bwd_main"] >= phase_ms["fwd_main"] else "k_fused_fwd"
-        dom_flops = (4.0 * uf_cf + 2.0 * ud_cd) if dom == "k_fused_bwd" else 2.0 * uf_cf
-        dom_ms = phase_ms["bwd_main" if dom == "k_fused_bwd" else "fwd_main"]
+        bwd_dom = phase_ms["bwd_main"] >= phase_ms["fwd_main"]
+        dom = main_run["kernels"]["bwd" if bwd_dom else "fwd"] or ("k_fused_bwd" if bwd_dom else "k_fused_fwd")
+        dom_flops = (4.0 * uf_cf + 2.0 * ud_cd) if bwd_dom else 2.0 * uf_cf
+        dom_ms = phase_ms["bwd_main" if bwd_dom else "fwd_main"]
     else:
         dom, dom_flops, dom_ms = "whole step (generic path)", flops, ms_per_step
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0

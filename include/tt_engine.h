@@ -137,6 +137,9 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_indices, int64_t batch, 
 int tt_train_step_wait(tt_engine* h);
 /* The handle's own CUDA stream (the host-buffer calls run on it). */
 void* tt_engine_stream(tt_engine* h);
+/* Name of the level-F GEMM kernel the last forward (backward != 0: backward)
+ * launched, e.g. "k_fused_fwd8", "k_fused_bwd_ws", "k_tc_bwd" ("" if none). */
+const char* tt_main_kernel(tt_engine* h, int backward);
 
 /* Dense gradients in the reference layout (CoreGradients, autodiff.hpp:29-34);
  * untouched slices read as exactly 0.  batch_count may be NULL. */

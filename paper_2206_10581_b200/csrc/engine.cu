@@ -187,6 +187,10 @@ struct tt_engine {
   // [n_k R_{k+1}] fp32 view of core k, box {128, R_k})
   CUtensorMap tmap[TT_MAXD] = {};
   bool tmap_ok[TT_MAXD] = {};
+
+  // the level-F GEMM kernels of the last forward / backward (tt_main_kernels)
+  const char* fwd_kernel = "";
+  const char* bwd_kernel = "";
 };
 
 namespace {
@@ -742,6 +746,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
 #define BWDWS_CASE(k_, rp_, nl_)                                                                 \
   if (f.K == k_ && f.RP == rp_ && f.NL == nl_) {                                                 \
     FUSED_LAUNCH_T((k_fused_bwd_ws<k_, rp_, nl_>), bwd_ws_smem(k_), grid, WsRoles<k_>::T, s, a);  \
+    h->bwd_kernel = "k_fused_bwd_ws";                                                            \
     if (a.split > 1)                                                                             \
       LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
              a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
@@ -754,6 +759,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
 #define BWDK32_CASE(rp_, nl_)                                                                    \
   if (f.RP == rp_ && f.NL == nl_) {                                                              \
     FUSED_LAUNCH_T((k_fused_bwd_k32<rp_, nl_>), bwd_k32_smem(), grid, K32_THREADS, s, a);         \
+    h->bwd_kernel = "k_fused_bwd_k32";                                                           \
     if (a.split > 1)                                                                             \
       LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
              a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
@@ -775,6 +781,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
       tt_launch((k_fused_fwd8<k_, rp_, false>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
     }                                                                                            \
     ++h->launches;                                                                               \
+    if (a.mode == 0) h->fwd_kernel = "k_fused_fwd8";                                             \
     return TT_OK;                                                                                \
   }
     TT_FWD8_SHAPES(FWD8_CASE)
@@ -785,11 +792,13 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
     }
     TT_FUSED_FWD_SHAPES(FUSED_CASE_F)
     else return fail(TT_ERR_ARG, "fused path: forward shape not compiled");
+    if (a.mode == 0) h->fwd_kernel = "k_fused_fwd";
   } else {
     if (false) {
     }
     TT_FUSED_SHAPES(FUSED_CASE_B)
     else return fail(TT_ERR_ARG, "fused path: backward shape not compiled");
+    if (a.mode == 0) h->bwd_kernel = "k_fused_bwd";
     if (a.split > 1)
       LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, a.F,
              a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
@@ -925,6 +934,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_fwd<k_, bn_, rp_>), h->ts.smem_fwd, grid, TCF_THREADS, s, a);
       TT_TC_SHAPES(TT_TC_FWD_CASE)
 #undef TT_TC_FWD_CASE
+      h->fwd_kernel = "k_tc_fwd";
       h->last_path = 2;
     } else {
       rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
@@ -1017,6 +1027,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, TCB_THREADS, s, a);
       TT_TC_SHAPES(TT_TC_BWD_CASE)
 #undef TT_TC_BWD_CASE
+      h->bwd_kernel = "k_tc_bwd";
       if (a.split > 1)
         LAUNCH(k_fused_reduce_gsplit, grid_for(c.m[f.F] * c.slice[f.F] / 4, 256, 148 * 8), 256, 0, s, c, f.F, a.split,
                a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
@@ -2011,6 +2022,11 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const fl
 }
 
 void* tt_engine_stream(tt_engine* h) { return h ? (void*)h->own : nullptr; }
+
+const char* tt_main_kernel(tt_engine* h, int backward) {
+  if (!h) return "";
+  return backward ? h->bwd_kernel : h->fwd_kernel;
+}
 
 // ---- ID-owner sharding over the handle's NCCL communicator ------------------
 namespace {

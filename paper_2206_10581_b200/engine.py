@@ -60,7 +60,7 @@ SYMBOLS = [
     "tt_opt_state_get_f64", "tt_opt_state_set_f64", "tt_opt_set_hparams", "tt_debug_trace", "tt_set_permutation",
     "tt_ortho_cores_f64", "tt_nccl_unique_id", "tt_comm_init_rank", "tt_comm_init", "tt_allreduce_grads",
     "tt_train_step_submit", "tt_train_step_wait", "tt_engine_stream",
-    "tt_owner_forward", "tt_owner_backward", "tt_owner_step", "tt_owner_rows",
+    "tt_owner_forward", "tt_owner_backward", "tt_owner_step", "tt_owner_rows", "tt_main_kernel",
 ]
 
 
@@ -107,6 +107,7 @@ def load_library(build_if_missing: bool = True):
         "tt_engine_stream": (vp, [vp]),
         "tt_owner_forward": (i32, [vp, vp, i64, vp, vp]), "tt_owner_backward": (i32, [vp, vp, vp]),
         "tt_owner_step": (i32, [vp, vp]), "tt_owner_rows": (i64, [vp]),
+        "tt_main_kernel": (C.c_char_p, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -367,6 +368,10 @@ class TTEmbedding:
 
     def train_step_wait(self) -> None:
         _raise(self._lib.tt_train_step_wait(self._h), "tt_train_step_wait")
+
+    def main_kernel(self, backward: bool) -> str:
+        """The level-F GEMM kernel of the last forward / backward."""
+        return (self._lib.tt_main_kernel(self._h, 1 if backward else 0) or b"").decode()
 
     def engine_stream(self) -> int:
         return self._lib.tt_engine_stream(self._h) or 0
