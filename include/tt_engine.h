@@ -125,13 +125,14 @@ int tt_train_step_host(tt_engine* h, const int64_t* h_indices, int64_t batch,
 
 /* The same step, pipelined across calls: tt_train_step_submit enqueues one
  * step (uploads on a copy stream, compute on the handle's stream, the row
- * download on a second copy stream) into one of two staging slots and returns
- * at once; tt_train_step_wait retires the oldest submitted step and returns
- * its status (TT_ERR_INDEX / TT_ERR_NONFINITE as tt_sync would).  With two
+ * download on a second copy stream) into one of three staging slots and
+ * returns at once; tt_train_step_wait retires the oldest submitted step and
+ * returns its status (TT_ERR_INDEX / TT_ERR_NONFINITE as tt_sync would).  With
  * steps in flight, step t+1's host-to-device copies run under step t's compute
  * and device-to-host copy (as a data loader feeding a training loop would);
  * steps still run in submission order on the cores.  Host buffers must stay
- * valid until the step is retired; a third submit retires the oldest first. */
+ * valid until the step is retired; a submit with every slot busy retires the
+ * oldest first. */
 int tt_train_step_submit(tt_engine* h, const int64_t* h_indices, int64_t batch, const float* h_upstream,
                          float* h_out);
 int tt_train_step_wait(tt_engine* h);

@@ -34,6 +34,10 @@ using namespace tt;
 namespace {
 
 thread_local std::string g_err;
+// staging slots of the pipelined host-buffer steps: three, so the host can keep
+// a step's upload queued while it waits for the download of the step before
+// (with two, that wait coupled the copy engines: 3.12 vs 2.8 ms at papers)
+constexpr int TT_HOST_SLOTS = 3;
 long long* g_trace_buf = nullptr;  // TT_TC_TRACE: last backward's per-CTA timestamps
 thread_local int64_t g_err_pos = -1;
 thread_local int64_t g_err_val = 0;
@@ -122,8 +126,8 @@ struct tt_engine {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_up = nullptr, ev_fwd = nullptr, ev_in = nullptr;
 
-  // pipelined host-buffer steps (tt_train_step_submit / _wait): two staging
-  // slots, so step t+1's uploads run under step t's compute and download
+  // pipelined host-buffer steps (tt_train_step_submit / _wait): staging slots
+  // so that later steps' uploads run under a step's compute and download
   struct HostSlot {
     int64_t cap = 0, B = 0;
     int64_t* idx = nullptr;
@@ -133,7 +137,7 @@ struct tt_engine {
     DevStatus* h_st = nullptr;  // pinned: the device status right after the step
     cudaEvent_t ev_idx = nullptr, ev_up = nullptr, ev_fwd = nullptr, ev_done = nullptr, ev_out = nullptr;
     bool busy = false, has_out = false;
-  } hs[2];
+  } hs[TT_HOST_SLOTS];
   int hs_next = 0, hs_head = 0, hs_count = 0;
 
   // profiling (tt_set_profiling): event pairs per slot
@@ -456,6 +460,16 @@ void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int na
   unsigned long long* ticket = status + (int64_t)narr * nblk;
   cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ((size_t)narr * nblk + narr), s);
   LAUNCH(k_scan_onepass, dim3(nblk, narr), SC_THREADS, 0, s, a, stride, n_dev, status, ticket, nblk, sf);
+}
+
+// the device status into mapped host memory (UVA: the host pointer is valid
+// on the device)
+__global__ void k_status_to_host(const DevStatus* st, DevStatus* host) {
+  TT_PDL_ENTRY();
+  volatile DevStatus* h = host;
+  h->bad_pos = st->bad_pos;
+  h->bad_core = st->bad_core;
+  __threadfence_system();
 }
 
 __global__ void k_reset_status(DevStatus* st, int which) {
@@ -1938,12 +1952,13 @@ int tt_train_step_wait(tt_engine* h) {
   if (h->hs_count == 0) return TT_OK;
   CU(cudaSetDevice(h->device));
   auto& sl = h->hs[h->hs_head];
-  h->hs_head ^= 1;
+  h->hs_head = (h->hs_head + 1) % TT_HOST_SLOTS;
   --h->hs_count;
   sl.busy = false;
   CU(cudaEventSynchronize(sl.ev_done));
   if (sl.has_out) CU(cudaEventSynchronize(sl.ev_out));  // (ev_done follows the slot's uploads)
-  const DevStatus st = *sl.h_st;
+  DevStatus st;
+  memcpy(&st, (const void*)sl.h_st, sizeof(st));
   if (st.bad_pos != TT_NO_POS) {
     const int64_t val = sl.h_idx ? sl.h_idx[st.bad_pos] : 0;
     h->plan_valid = false;
@@ -1963,7 +1978,7 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const fl
   if (!h) return fail(TT_ERR_ARG, "tt_train_step_submit: null handle");
   if (B <= 0 || !h_idx || !h_up) return fail(TT_ERR_ARG, "tt_train_step_submit: empty batch or null buffer");
   CU(cudaSetDevice(h->device));
-  if (h->hs_count == 2) {  // both slots in flight: retire the oldest first
+  if (h->hs_count == TT_HOST_SLOTS) {  // every slot in flight: retire the oldest first
     int rc = tt_train_step_wait(h);
     if (rc) return rc;
   }
@@ -1987,7 +2002,7 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const fl
   if (!sl.ev_idx) {
     for (cudaEvent_t* e : {&sl.ev_idx, &sl.ev_up, &sl.ev_fwd, &sl.ev_done, &sl.ev_out})
       CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    CU(cudaMallocHost(&sl.h_st, sizeof(DevStatus)));
+    CU(cudaHostAlloc(&sl.h_st, sizeof(DevStatus), cudaHostAllocMapped));
   }
   cudaStream_t s = h->own;
   const size_t rows = sizeof(float) * (size_t)B * (size_t)N;
@@ -2011,12 +2026,17 @@ int tt_train_step_submit(tt_engine* h, const int64_t* h_idx, int64_t B, const fl
   rc = tt_backward(h, nullptr, B, sl.up, s);
   if (!rc) rc = tt_step(h, s);
   if (rc) { cudaStreamSynchronize(h->s_h2d); cudaStreamSynchronize(h->s_d2h); cudaStreamSynchronize(s); return rc; }
-  CU(cudaMemcpyAsync(sl.h_st, h->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  // the step's status goes to host memory by a one-thread kernel writing
+  // mapped (zero-copy) pinned memory: a 16-byte cudaMemcpy here would queue on
+  // the device-to-host copy engine behind the 134 MB row download and hold the
+  // compute stream (the next step's forward) until it finished -- measured
+  // 3.67 -> 2.8 ms per pipelined step at papers
+  LAUNCH(k_status_to_host, 1, 1, 0, s, (const DevStatus*)h->st, sl.h_st);
   CU(cudaEventRecord(sl.ev_done, s));
   sl.B = B;
   sl.h_idx = h_idx;
   sl.busy = true;
-  h->hs_next ^= 1;
+  h->hs_next = (h->hs_next + 1) % TT_HOST_SLOTS;
   ++h->hs_count;
   return TT_OK;
 }
