@@ -665,7 +665,10 @@ int split_for(tt_engine* h, int grid, int level, bool fwd) {
   for (int k = 0; k <= level; ++k) prefixes *= (long double)c.m[k];
   const long double nodes = std::min<long double>((long double)h->B, prefixes) / (long double)c.m[level];
   const long double rows = nodes * (long double)c.rows[level];
-  const int min_rows = fwd ? 4096 : 1024;
+  // ranks <= 16: the backward is bound by forming dC (latency of the
+  // last-core slices and upstream rows; the GEMMs are tiny), so more CTAs pay
+  // even for small groups (sweep8 / sweep16: profiles/r02/NOTES.md)
+  const int min_rows = fwd ? 4096 : (c.R[level] <= 16 ? 128 : 1024);
   const int by_rows = (int)std::min<long double>(16.0L, rows / min_rows);
   const int target = h->nsm * 6;
   const int by_grid = std::max(1, std::min(16, (target + grid - 1) / grid));
