@@ -1193,48 +1193,62 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
   float4 pv[PIPE ? PB : 1], gr[PIPE ? GV : 1];
-  auto issue = [&](int p, int dg) {  // a block and slice into registers
-    const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
+  auto issue = [&](int p, int dg, bool block) {  // (a block and) a slice into registers
+    if (block) {
+      const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
 #pragma unroll
-    for (int b = 0; b < PB; ++b)
-      if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+      for (int b = 0; b < PB; ++b)
+        if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+    }
     const float4* gs = reinterpret_cast<const float4*>(Gl + (int64_t)dg * sliceL);
 #pragma unroll
     for (int b = 0; b < GV; ++b)
       if (b * 32 + lane < K * NL / 4) gr[b] = __ldg(gs + b * 32 + lane);
   };
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // each warp owns a contiguous run of distinct IDs: consecutive IDs share
+  // their level-F prefix whenever the batch has locality (8 IDs per prefix in
+  // the rank sweep), and the staged prefix block is then reused, not reloaded
+  const int per = (U + nwarps - 1) / nwarps;
+  int u = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * per;
+  const int uend = min(U, u + per);
+  int staged = -1;  // parent whose block is in buf
   int pn = 0, dn = 0, sn0 = 0, sn1 = 0;
-  if (u < U) { pn = __ldg(parentL + u); dn = __ldg(a.digitL + u); sn0 = __ldg(a.seg + u); sn1 = __ldg(a.seg + u + 1); }
+  if (u < uend) { pn = __ldg(parentL + u); dn = __ldg(a.digitL + u); sn0 = __ldg(a.seg + u); sn1 = __ldg(a.seg + u + 1); }
   if constexpr (PIPE) {
-    if (u < U) issue(pn, dn);
+    if (u < uend) issue(pn, dn, true);
   }
-  for (; u < U; u += nwarps) {
+  for (; u < uend; ++u) {
     const int p = pn, dg = dn, s0 = sn0, s1 = sn1;
-    const int un = u + nwarps;
-    if (un < U) {  // the next ID's indices under this ID
+    const int un = u + 1;
+    if (un < uend) {  // the next ID's indices under this ID
       pn = __ldg(parentL + un); dn = __ldg(a.digitL + un);
       sn0 = __ldg(a.seg + un); sn1 = __ldg(a.seg + un + 1);
     }
     if constexpr (PIPE) {
+      if (p != staged) {
 #pragma unroll
-      for (int b = 0; b < PB; ++b) {
-        const int i = b * 32 + lane;
-        if (i < n4) {
-          const int row = i / (K / 4), c4 = i - row * (K / 4);
-          *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+        for (int b = 0; b < PB; ++b) {
+          const int i = b * 32 + lane;
+          if (i < n4) {
+            const int row = i / (K / 4), c4 = i - row * (K / 4);
+            *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+          }
         }
+        staged = p;
       }
 #pragma unroll
       for (int b = 0; b < GV; ++b)
         if (b * 32 + lane < K * NL / 4) reinterpret_cast<float4*>(Gs)[b * 32 + lane] = gr[b];
       __syncwarp();
-      if (un < U) issue(pn, dn);  // lands while this ID is computed
+      if (un < uend) issue(pn, dn, pn != p);  // lands while this ID is computed
     } else {
       const float* Gsrc = Gl + (int64_t)dg * sliceL;
       for (int i = lane; i < K * NL / 4; i += 32)
         reinterpret_cast<float4*>(Gs)[i] = __ldg(reinterpret_cast<const float4*>(Gsrc) + i);
-      stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+      if (p != staged) {
+        stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+        staged = p;
+      }
     }
     const float* Gp = Gs;
     // KS lanes per output row, each over K / KS ranks (KS = 2 when a block
@@ -1310,44 +1324,57 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
   const int64_t npad = a.c.npad;
   const int r0 = lane * RPL;
   float4 pv[PIPE ? PB : 1], yr[PIPE ? YB : 1];
-  auto issue = [&](int u, int p) {  // ID u's prefix block and dY row into registers
-    const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
+  auto issue = [&](int u, int p, bool block) {  // ID u's (prefix block and) dY row into registers
+    if (block) {
+      const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
 #pragma unroll
-    for (int b = 0; b < PB; ++b)
-      if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+      for (int b = 0; b < PB; ++b)
+        if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+    }
     const float4* ys = reinterpret_cast<const float4*>(a.dY + (int64_t)u * npad);
 #pragma unroll
     for (int b = 0; b < YB; ++b)
       if (b * 32 + lane < y4) yr[b] = __ldg(ys + b * 32 + lane);
   };
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int pn = u < U ? __ldg(parentL + u) : 0;
+  // contiguous runs of IDs per warp, the staged prefix block reused across
+  // IDs of one prefix (as in k_last_level)
+  const int per = (U + nwarps - 1) / nwarps;
+  int u = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * per;
+  const int uend = min(U, u + per);
+  int staged = -1;
+  int pn = u < uend ? __ldg(parentL + u) : 0;
   if constexpr (PIPE) {
-    if (u < U) issue(u, pn);
+    if (u < uend) issue(u, pn, true);
   }
-  for (; u < U; u += nwarps) {
+  for (; u < uend; ++u) {
     const int p = pn;
-    const int un = u + nwarps;
-    if (un < U) pn = __ldg(parentL + un);  // next ID's parent under this ID
+    const int un = u + 1;
+    if (un < uend) pn = __ldg(parentL + un);  // next ID's parent under this ID
     if constexpr (PIPE) {
+      if (p != staged) {
 #pragma unroll
-      for (int b = 0; b < PB; ++b) {
-        const int i = b * 32 + lane;
-        if (i < n4) {
-          const int row = i / (K / 4), c4 = i - row * (K / 4);
-          *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+        for (int b = 0; b < PB; ++b) {
+          const int i = b * 32 + lane;
+          if (i < n4) {
+            const int row = i / (K / 4), c4 = i - row * (K / 4);
+            *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+          }
         }
+        staged = p;
       }
 #pragma unroll
       for (int b = 0; b < YB; ++b)
         if (b * 32 + lane < y4) reinterpret_cast<float4*>(Ys)[b * 32 + lane] = yr[b];
       __syncwarp();
-      if (un < U) issue(un, pn);  // lands while this ID is computed
+      if (un < uend) issue(un, pn, pn != p);  // lands while this ID is computed
     } else {
       const float* Yp = a.dY + (int64_t)u * npad;
       for (int i = lane; i < y4; i += 32)
         reinterpret_cast<float4*>(Ys)[i] = __ldg(reinterpret_cast<const float4*>(Yp) + i);
-      stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+      if (p != staged) {
+        stage_prefix_block<K>(a.Psave + (int64_t)p * RP * a.NC, nrow, buf, lane);
+        staged = p;
+      }
     }
     if (r0 < K) {
       float wv[RPL][NL];
