@@ -25,6 +25,7 @@
 #include "kernels_init.cuh"
 #include "kernels_owner.cuh"
 #include "kernels_plan.cuh"
+#include "kernels_plan_small.cuh"
 #include "kernels_rows.cuh"
 #include "kernels_tcgen05.cuh"
 #include "kernels_update.cuh"
@@ -452,6 +453,15 @@ void sort_levels(tt_engine* h, cudaStream_t s) {
   LAUNCH(k_rs_scatter<unsigned>, dim3(ntiles, d - 1), RS_THREADS, smem, s, rb, 0, nbits);
 }
 
+// TT_PLAN_SMALL=0 keeps the multi-kernel plan for small batches too
+bool plan_small_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_PLAN_SMALL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 // one memset (status words + tickets) and one single-pass scan kernel
 void scan_inclusive(tt_engine* h, cudaStream_t s, int* a, int64_t stride, int narr, const int* n_dev, int64_t nmax,
                     const ScanFlags& sf) {
@@ -489,9 +499,42 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
   h->B = B;
   h->last_idx = d_idx;
   h->d_B = h->counts + TT_MAXD;
+  const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
+  if (B <= PS_MAXB && idbits + PS_IBITS <= 64 && plan_small_enabled()) {
+    // the whole plan in one CTA (kernels_plan_small.cuh)
+    PlanSmallArgs ps{};
+    ps.c = c;
+    ps.idx = d_idx;
+    ps.B = (int)B;
+    ps.perm = h->perm;
+    ps.idbits = idbits;
+    ps.cap = cap;
+    ps.skeys = h->keys_b;
+    ps.spos = h->pos_b;
+    ps.flag = h->flag;
+    ps.uniq = h->uniq;
+    ps.seg = h->seg;
+    ps.counts = h->counts;
+    ps.digit = h->digit;
+    ps.parent = h->parent;
+    ps.first = h->first;
+    ps.cstart = h->cstart;
+    for (int k = 0; k < d; ++k) {
+      ps.sdig[k] = k == 0 ? h->gk[0][0] : h->gk[k][1];
+      ps.order[k] = k == 0 ? h->gv[0][0] : h->gv[k][1];
+      ps.goff[k] = h->goff[k];
+      h->sdig[k] = ps.sdig[k];
+      h->order[k] = ps.order[k];
+    }
+    ps.st = h->st;
+    CU(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PS_SMEM));
+    LAUNCH(k_plan_small, 1, PS_THREADS, PS_SMEM, s, ps);
+    h->skeys = h->keys_b;
+    h->spos = h->pos_b;
+    return TT_OK;
+  }
   LAUNCH(k_decompose_validate, grid_for(B, 256, INT_MAX), 256, 0, s, d_idx, B, c.num_nodes, h->keys_a, h->pos_a, h->st,
          (const int*)h->perm, h->counts + TT_MAXD);
-  const int idbits = (int)std::max<int64_t>(1, bitlen((uint64_t)(c.num_nodes - 1)));
   h->skeys = radix_sort<unsigned long long>(h, s, h->keys_a, h->pos_a, h->keys_b, h->pos_b, nullptr, (int)B, B,
                                             idbits, &h->spos);
   ScanFlags uf{};
