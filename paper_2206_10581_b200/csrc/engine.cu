@@ -155,6 +155,7 @@ struct tt_engine {
   int last_path = 0;
   bool fused_ok = false;
   FusedShape fs{};
+  int level_shift_F = 0;  // level-F sort keys carry an ID-count class in their low bits
   bool tc_ok = false;  // tensor-core (tcgen05) kernels exist for this shape
   TcShape ts{};
 
@@ -424,6 +425,15 @@ K* radix_sort(tt_engine* h, cudaStream_t s, K* ka, int* va, K* kb, int* vb, cons
 // The plan's per-level digit sorts (levels 1..d-1) in one pass for all levels
 // at once (3 launches instead of 4 per level): stable by node index.
 // Requires every m_k <= 2^RS_MAXBITS.
+// TT_COUNT_ORDER=0: level-F nodes in plain digit order (no ID-count refinement)
+bool count_order_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_COUNT_ORDER");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 void sort_levels(tt_engine* h, cudaStream_t s) {
   const DevCfg& c = h->dc;
   const int d = c.d;
@@ -431,11 +441,21 @@ void sort_levels(tt_engine* h, cudaStream_t s) {
   const int ntiles = (int)((cap + RS_TILE - 1) / RS_TILE);
   int nbits = 1;
   for (int k = 1; k < d; ++k) nbits = std::max<int>(nbits, (int)bitlen((uint64_t)(c.m[k] - 1)));
+  // the fused level F sorts on (digit, ID-count class) when the key still
+  // fits one radix pass (k_levelF_keys)
+  const int F = d - 2;
+  h->level_shift_F = 0;
+  if (F >= 1 && count_order_enabled() && bitlen((uint64_t)(c.m[F] - 1)) + 2 <= RS_MAXBITS) {
+    h->level_shift_F = 2;
+    nbits = std::max<int>(nbits, (int)bitlen((uint64_t)(c.m[F] - 1)) + 2);
+    LAUNCH(k_levelF_keys, grid_for(cap, 256, INT_MAX), 256, 0, s, (const int*)h->counts, F,
+           (const int*)(h->digit + F * cap), (const int*)(h->cstart + F * (cap + 1)), h->gk[F][0]);
+  }
   rs_set_attrs<unsigned>(h->device);
   RSBatch<unsigned> rb{};
   for (int k = 1; k < d; ++k) {
     const int y = k - 1;
-    rb.kin[y] = reinterpret_cast<const unsigned*>(h->digit + k * cap);
+    rb.kin[y] = (k == F && h->level_shift_F) ? h->gk[F][0] : reinterpret_cast<const unsigned*>(h->digit + k * cap);
     rb.vin[y] = nullptr;
     rb.kout[y] = h->gk[k][1];
     rb.vout[y] = h->gv[k][1];
@@ -575,6 +595,7 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
     ga.sdig[k] = h->sdig[k];
     ga.goff[k] = h->goff[k];
     ga.m[k] = (int)c.m[k];
+    ga.shift[k] = (batched && k == d - 2) ? h->level_shift_F : 0;
     mmax = std::max<int64_t>(mmax, c.m[k]);
   }
   LAUNCH(k_group_offsets_all, dim3(grid_for(mmax + 1, 256, INT_MAX), d), 256, 0, s, ga, h->counts);

@@ -456,7 +456,23 @@ struct GroupOffArgs {
   const unsigned* sdig[TT_MAXD];
   int* goff[TT_MAXD];
   int m[TT_MAXD];
+  int shift[TT_MAXD];  // sorted keys are (digit << shift) | refinement
 };
+
+// Level-F sort keys with a secondary refinement: (digit << 2) | min(#IDs - 1, 3).
+// Inside a digit group the level-F nodes then come ordered by their number of
+// distinct IDs, so a GEMM tile holds nodes of similar dC cost: the tile's dC
+// phase lasts as long as its most expensive node, and mixing one 4-ID node
+// into a tile of 1-ID nodes stalls every other thread at the tile barrier.
+__global__ void k_levelF_keys(const int* __restrict__ counts, int F, const int* __restrict__ digitF,
+                              const int* __restrict__ cstartF, unsigned* __restrict__ keys) {
+  TT_PDL_ENTRY();
+  const int n = ld_count(&counts[F]);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int nid = cstartF[i + 1] - cstartF[i];
+  keys[i] = ((unsigned)digitF[i] << 2) | (unsigned)min(nid - 1, 3);
+}
 
 // all levels at once: blockIdx.y = level
 __global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ counts) {
@@ -466,10 +482,11 @@ __global__ void k_group_offsets_all(GroupOffArgs ga, const int* __restrict__ cou
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > ga.m[k]) return;
   const unsigned* sd = ga.sdig[k];
+  const int sh = ga.shift[k];
   int lo = 0, hi = n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if ((int)sd[mid] < v) lo = mid + 1; else hi = mid;
+    if ((int)(sd[mid] >> sh) < v) lo = mid + 1; else hi = mid;
   }
   ga.goff[k][v] = lo;
 }
