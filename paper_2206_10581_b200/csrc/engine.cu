@@ -987,7 +987,10 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   a.BNj = f.BNjf;
   {
     Phase ph(h, 1, s);
-    if (use_tc(h)) {
+    if (use_tc(h) && f.K == 128) {  // rank 128: the FFMA forward, the tcgen05 backward
+      rc = fused_dispatch(h, true, a, (int)(c.m[f.F] * f.ncbf), s);
+      h->last_path = 2;
+    } else if (use_tc(h)) {
       a.ncb = h->ts.ncbf;
       a.mode = diag().tc_fwd_variant;
       static long long* trace_fwd = nullptr;
@@ -1077,7 +1080,34 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   int rc;
   {
     Phase ph(h, 2, s);
-    if (h->last_path == 2) {
+    if (h->last_path == 2 && f.K == 128) {
+      a.ncb = h->ts.ncbb;
+      a.split = split_for(h, (int)(c.m[f.F] * h->ts.ncbb), f.F, false);
+      a.split_rows = split_rows_env(false, 128);
+      if (a.split > 1) {
+        const int64_t need = c.m[f.F] * a.split * c.slice[f.F];
+        if (h->F.cap_gsplit < need) {
+          cudaFree(h->F.gsplit);
+          h->F.gsplit = nullptr;
+          h->F.cap_gsplit = 0;
+          CU(dalloc(&h->F.gsplit, need));
+          h->F.cap_gsplit = need;
+        }
+        a.gsplit = h->F.gsplit;
+      }
+      const int grid = (int)(c.m[f.F] * h->ts.ncbb * a.split);
+      rc = TT_OK;
+      if (false) {
+      }
+#define TT_TC128_CASE(rp_, nl_) \
+  else if (f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd128<rp_, nl_>), h->ts.smem_bwd, grid, TCB_THREADS, s, a);
+      TT_TC128_SHAPES(TT_TC128_CASE)
+#undef TT_TC128_CASE
+      if (a.split > 1)
+        LAUNCH(k_fused_reduce_gsplit, grid_for(c.m[f.F] * c.slice[f.F] / 4, 256, 148 * 8), 256, 0, s, c, f.F, a.split,
+               a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
+      h->bwd_kernel = "k_tc_bwd128";
+    } else if (h->last_path == 2) {
       a.ncb = h->ts.ncbb;
       a.mode = diag().tc_bwd_variant;
       static long long* trace_buf = nullptr;

@@ -624,12 +624,205 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
   if (warp == 0) tc::tmem_free<TCOLS>(tslot);
 }
 
+// ---------------------------------------------------------------------------
+// Backward at rank 128 (the rank sweep's R = 128): 64-column blocks, so the
+// BF16x3 planes fit in 192 KB (S 48 KB, A 96 KB, dC 48 KB; 128-column blocks
+// would need 288 KB).  dG_F is accumulated untransposed, M = 128 (k) x N = 64
+// (columns) with A^T read MN-major, since an M = 64 dG_F^T accumulator has a
+// different TMEM lane layout; dA = dC . S^T is M = 128 (rows) x N = 128 (k).
+// dC unit: 2 rows of one node x 8 columns per thread (512 units); thread bits
+// [0] c8 low, [1] row pair, [2] node low, [3,5) c8 high, [5,9) node high, and
+// row i of the pair stored in rotated order i ^ (c8 & 1), so the 8 threads of
+// a store phase write 8 distinct rows of a core matrix: conflict-free.
+// The forward at rank 128 runs the FFMA kernel (the forward's TMEM budget,
+// 2 x 128 accumulator + 2 x 3 x 64 A columns, exceeds 512).
+template <int RP, int NL>
+__global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd128(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int K = 128, BN = 64, T = TCB_THREADS;
+  static_assert(RP == 4, "rank-128 tensor backward: 4 rows per node");
+  constexpr int NPT = TC_BM / RP;
+  extern __shared__ __align__(128) uint8_t tsm[];
+  uint8_t* S0 = tsm;
+  uint8_t* S1 = S0 + K * BN * 2;
+  uint8_t* S2 = S1 + K * BN * 2;
+  uint8_t* A0 = S2 + K * BN * 2;
+  uint8_t* A1 = A0 + TC_BM * K * 2;
+  uint8_t* A2 = A1 + TC_BM * K * 2;
+  uint8_t* D0 = A2 + TC_BM * K * 2;
+  uint8_t* D1 = D0 + TC_BM * BN * 2;
+  uint8_t* D2 = D1 + TC_BM * BN * 2;
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(D2 + TC_BM * BN * 2);
+  int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
+  int* s_cs0 = s_node + FB_NB;
+  int* s_pref = s_cs0 + FB_NB;
+  int* s_wsum = s_pref + FB_NB + 4;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+
+  if (tt_failed(a.st)) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  if (warp == 0) tc::tmem_alloc<256>(&tslot);
+  if (threadIdx.x == 32) {
+    tc::mbar_init(&bar, 2);
+    tc::fence_mbar_init();
+  }
+  tc_stage_slice<K, BN, T>(a, g, cb, S0, S1, S2);
+  const int nF = a.nF;
+  const int64_t npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const uint32_t id_g = tc::idesc_bf16(K, BN, 1, 1);     // dG = A^T . dC   (M = 128 k, N = 64 cols)
+  const uint32_t id_a = tc::idesc_bf16(TC_BM, K, 0, 0);  // dA = dC . S^T   (M = 128 rows, N = 128 k)
+  uint32_t phase = 0;
+  int tiles = 0;
+  ATileRegs<K, T> ar;
+  const int t = threadIdx.x;
+  const int c8 = (t & 1) | (((t >> 3) & 3) << 1);
+  const int hh = (t >> 1) & 1;
+  const int uj = ((t >> 2) & 1) | ((t >> 5) << 1);
+  const int rot = c8 & 1;
+  const int a0 = 2 * hh;  // the unit's first row within its node
+  const int colg = cb * BN + c8 * 8, jf = colg / K, r0 = colg - jf * K;
+  auto compute_dC = [&](int tb, int nn, float (&acc)[2][8]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[i][q] = 0.f;
+    if (uj >= nn) return;
+    const int fA = s_pref[tb + uj], fB = s_pref[tb + uj + 1], cs0 = s_cs0[tb + uj];
+    for (int f = fA; f < fB; ++f) {
+      const int u = cs0 + (f - fA);
+      const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL;
+      const float* Yp = a.dY + (int64_t)u * npad + ((int64_t)a0 * nF + jf) * NL;
+      float yv[2][NL];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int ii = i ^ rot;
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)ii * nF * NL + l4));
+          yv[i][l4] = x.x; yv[i][l4 + 1] = x.y; yv[i][l4 + 2] = x.z; yv[i][l4 + 3] = x.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float gv[NL];
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + q * NL + l4));
+          gv[l4] = x.x; gv[l4 + 1] = x.y; gv[l4 + 2] = x.z; gv[l4 + 3] = x.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          float sacc = acc[i][q];
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) sacc = fmaf(yv[i][jl], gv[jl], sacc);
+          acc[i][q] = sacc;
+        }
+      }
+    }
+  };
+  float acc[2][8];
+  const int em = 32 * (warp & 3) + lane;  // epilogue row (TMEM lane)
+  const int emj = em / RP, ema = em - emj * RP;
+  const int esl = (warp >> 2) * 32;       // dA epilogue: 32 of the 128 k columns
+  for (int nb0 = g0; nb0 < g1; nb0 += FB_NB) {
+    const int nbn = min(FB_NB, g1 - nb0);
+    tc_prep_nodes<T>(a, nb0, nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+    tc_load_A<K, RP, T>(a, 0, min(NPT, nbn), s_aoff, ar);
+    compute_dC(0, min(NPT, nbn), acc);
+    for (int tb = 0; tb < nbn; tb += NPT, ++tiles) {
+      const int nn = min(NPT, nbn - tb);
+      tc_store_A<K, T>(ar, A0, A1, A2);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) tc::store_split8(D0, D1, D2, 4 * uj + a0 + (i ^ rot), c8 * 8, BN, acc[i]);
+      tc::fence_async_smem();
+      tc::before_sync();
+      __syncthreads();
+      tc::after_sync();
+      const uint32_t tm = tslot;
+      const bool more = tb + NPT < nbn;
+      if (more) tc_load_A<K, RP, T>(a, tb + NPT, min(NPT, nbn - tb - NPT), s_aoff, ar);
+      if (threadIdx.x == 0) {  // dG += A^T . dC   (accumulated over the group)
+        const tc::Operand aT = tc::mnmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
+        const tc::Operand dcB = tc::mnmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
+        tc::mma_x3<TC_BM / 16>(tm, aT, dcB, id_g, tiles > 0);
+        tc::commit(&bar);
+      } else if (threadIdx.x == 32) {  // dA = dC . S^T
+        const tc::Operand dcK = tc::kmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
+        const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
+        tc::mma_x3<BN / 16>(tm + BN, dcK, sT, id_a, false);
+        tc::commit(&bar);
+      }
+      __syncwarp();
+      float* dst = emj < nn ? a.dPc + ((int64_t)s_node[tb + emj] * a.ncb + cb) * RP * K + ema * K + esl : nullptr;
+      if (more) compute_dC(tb + NPT, min(NPT, nbn - tb - NPT), acc);
+      tc::mbar_wait(&bar, phase);  // planes free for the next tile
+      phase ^= 1;
+      tc::after_sync();
+      {
+        float v[16];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          tc::tmem_ld16(tm + lane_base + BN + esl + 16 * h2, v);
+          if (dst) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<float4*>(dst + 16 * h2 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+      }
+      tc::before_sync();
+    }
+    tc::before_sync();
+    __syncthreads();
+  }
+  // dG_F block: TMEM lane = k, column = n of the block
+  tc::after_sync();
+  {
+    const uint32_t tm = tslot;
+    const int k = 32 * (warp & 3) + lane, n0 = (warp >> 2) * 16;
+    float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) +
+                  (int64_t)k * a.NC + cb * BN + n0;
+    float v[16];
+    tc::tmem_ld16(tm + lane_base + n0, v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(gdst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  tc::before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<256>(tslot);
+}
+
+// (RP, NL) instantiations of the rank-128 tensor backward (sweep128)
+#define TT_TC128_SHAPES(X) X(4, 8)
+
 // (K, BNf, RP, NL) instantiations of the tensor-core path
 #define TT_TC_SHAPES(X) X(64, 128, 4, 4) X(32, 128, 4, 8) X(32, 128, 16, 4) X(64, 128, 4, 8)
 
 inline bool tc_plan_shape(const FusedShape& f, TcShape* t) {
   *t = TcShape{};
   bool ok = false;
+  if (f.K == 128) {  // FFMA forward + k_tc_bwd128 (64-column blocks)
+#define TT_TC128_EQ(rp_, nl_) if (f.RP == rp_ && f.NL == nl_ && f.NC % 64 == 0) ok = true;
+    TT_TC128_SHAPES(TT_TC128_EQ)
+#undef TT_TC128_EQ
+    if (!ok) return false;
+    t->BNf = 0;
+    t->ncbf = 0;
+    t->BNb = 64;
+    t->ncbb = f.NC / 64;
+    t->smem_fwd = 0;
+    t->smem_bwd = 3 * (size_t)128 * 64 * 2 + 3 * (size_t)TC_BM * 128 * 2 + 3 * (size_t)TC_BM * 64 * 2 + TC_META;
+    t->ok = t->smem_bwd <= (size_t)FB_SMEM_MAX;
+    return t->ok;
+  }
 #define TT_TC_EQ(k_, bn_, rp_, nl_) \
   if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC % bn_ == 0 && f.NC % 128 == 0) ok = true;
   TT_TC_SHAPES(TT_TC_EQ)

@@ -98,7 +98,7 @@ def test_full_batch_backward_linearity(path):
 # cores the oracle's update with that gradient (autodiff.cpp:147-173).
 FULL_CASES = [("papers", "auto", 3000), ("papers", "tc", 3000), ("billion", "auto", 2000),
               ("billion", "tc", 2000), ("sweep64", "auto", 3000), ("sweep64", "tc", 3000),
-              ("sweep16", "auto", 3000), ("sweep128", "auto", 1500)]
+              ("sweep16", "auto", 3000), ("sweep128", "auto", 1500), ("sweep128", "tc", 1500)]
 
 
 def _full_inputs(name):

@@ -82,7 +82,7 @@ SHAPES = {
 FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep16", "sweep32", "sweep64", "sweep128", "billion"}
 
 # shapes with tcgen05 kernels (rank >= 32)
-TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64")
+TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64", "sweep128")
 
 
 @pytest.mark.parametrize("name", list(SHAPES))

@@ -59,6 +59,8 @@ def reached(cfg):
     ffma |= {(K, BN, RP, NL), (K, BNf, RP, NL)}
     if K in (32, 64) and NC % 128 == 0:
         tc.add((K, 128, RP, NL))
+    if K == 128 and NC % 64 == 0:
+        tc.add((RP, NL))  # k_tc_bwd128 (TT_TC128_SHAPES)
     for k in range(1, F):  # wide levels on the fused kernels
         Kw, NCw, RPw = R[k], cols[k], rows[k]
         BNw = _block(Kw, NCw, wide=True)
@@ -103,13 +105,25 @@ def test_every_bwdk32_instantiation_has_a_parity_case():
     assert not missing, f"compiled rank-32 backward instantiations with no parity case: {missing}"
 
 
+def test_every_rank128_tcgen05_instantiation_has_a_parity_case():
+    src = open(os.path.join(CSRC, "kernels_tcgen05.cuh")).read()
+    m = re.search(r"#define\s+TT_TC128_SHAPES\(X\)([^\n]*)", src)
+    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+)\)", m.group(1))}
+    covered = set()
+    for name in TC_SHAPES:
+        _, tc = reached(SHAPES[name][0]())
+        covered |= {t for t in tc if len(t) == 2}
+    missing = sorted(t for t in compiled if t not in covered)
+    assert not missing, f"compiled rank-128 tcgen05 instantiations with no parity case: {missing}"
+
+
 def test_every_tcgen05_instantiation_has_a_parity_case():
     compiled = _macro_tuples("kernels_tcgen05.cuh", "TT_TC_SHAPES")
     covered = set()
     for name in TC_SHAPES:
         _, tc = reached(SHAPES[name][0]())
         assert tc, f"{name} is listed as a tensor-core parity shape but admits no tcgen05 kernel"
-        covered |= tc
+        covered |= {t for t in tc if len(t) == 4}
     missing = sorted(t for t in compiled if t not in covered)
     assert not missing, f"compiled tcgen05 instantiations with no parity case: {missing}"
 
