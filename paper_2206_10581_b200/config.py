@@ -225,6 +225,23 @@ for _r in (8, 16, 32, 64, 128):
         batch=131_072, dist="locality", block=140 * 140, opt="adagrad")
 
 
+# The paper's own Table-4 factorisations, at the BASELINE
+# batch and distribution of the same dataset -- not BASELINE configs, measured
+# to show the fused path covers them.
+WORKLOADS["arxivT4_r32"] = dict(
+    cfg=lambda: plan_factorization(169_343, 128, [55, 55, 56], [8, 4, 4], [1, 32, 32, 1]),
+    batch=4096, dist="uniform", opt="sgd")
+WORKLOADS["productsT4_r32"] = dict(
+    cfg=lambda: plan_factorization(2_449_029, 100, [125, 140, 140], [4, 5, 5], [1, 32, 32, 1]),
+    batch=65_536, dist="zipf", alpha=1.1, opt="adagrad")
+WORKLOADS["productsT4_r64"] = dict(
+    cfg=lambda: plan_factorization(2_449_029, 100, [125, 140, 140], [4, 5, 5], [1, 64, 64, 1]),
+    batch=65_536, dist="zipf", alpha=1.1, opt="adagrad")
+WORKLOADS["papersT4_r64"] = dict(
+    cfg=lambda: plan_factorization(111_059_956, 128, [480, 500, 500], [8, 4, 4], [1, 64, 64, 1]),
+    batch=262_144, dist="zipf", alpha=1.05, opt="adagrad")
+
+
 def workload_inputs(name: str, seed: int = 2026, batch: int | None = None):
     """(cfg, indices int64[B], upstream f32[B, emb_dim], cores f32 list) for a
     BASELINE workload, from the portable generator in synth.py."""

@@ -253,6 +253,33 @@ __device__ __forceinline__ void store_row_frag(float* row, int lane, const float
   }
 }
 
+// NL consecutive floats (the last core's column factor n_d) into registers:
+// 16-byte loads when NL is a multiple of 4, scalar loads otherwise (the
+// paper's Table-4 products shape has n = (4,5,5))
+template <int NL>
+__device__ __forceinline__ void ldg_vec(const float* p, float* v) {
+  if constexpr (NL % 4 == 0) {
+#pragma unroll
+    for (int l4 = 0; l4 < NL; l4 += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p + l4));
+      v[l4] = x.x; v[l4 + 1] = x.y; v[l4 + 2] = x.z; v[l4 + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int jl = 0; jl < NL; ++jl) v[jl] = __ldg(p + jl);
+  }
+}
+template <int NL>
+__device__ __forceinline__ void st_vec(float* p, const float* v) {
+  if constexpr (NL % 4 == 0) {
+#pragma unroll
+    for (int l4 = 0; l4 < NL; l4 += 4) *reinterpret_cast<float4*>(p + l4) = make_float4(v[l4], v[l4 + 1], v[l4 + 2], v[l4 + 3]);
+  } else {
+#pragma unroll
+    for (int jl = 0; jl < NL; ++jl) p[jl] = v[jl];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Column map of a warp's micro-tile (the backward's dC pass): rows m0..m0+7
 // and, per lane, NQ column groups of W4 consecutive columns; group q of lane l
@@ -378,21 +405,11 @@ __device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int 
         const int r0 = colg % K, jf = colg / K;
         float gv[W4][NL];
 #pragma unroll
-        for (int t = 0; t < W4; ++t)
-#pragma unroll
-          for (int l4 = 0; l4 < NL; l4 += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(Gp + (r0 + t) * NL + l4));
-            gv[t][l4] = x.x; gv[t][l4 + 1] = x.y; gv[t][l4 + 2] = x.z; gv[t][l4 + 3] = x.w;
-          }
+        for (int t = 0; t < W4; ++t) ldg_vec<NL>(Gp + (r0 + t) * NL, gv[t]);
 #pragma unroll
         for (int ii = 0; ii < NR; ++ii) {
           float yv[NL];
-          const float* yrow = Yp + ((int64_t)(ar0 + ii) * nF + jf) * NL;
-#pragma unroll
-          for (int l4 = 0; l4 < NL; l4 += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(yrow + l4));
-            yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
-          }
+          ldg_vec<NL>(Yp + ((int64_t)(ar0 + ii) * nF + jf) * NL, yv);
 #pragma unroll
           for (int t = 0; t < W4; ++t) {
             float s = dacc[jw * NR + ii][q * W4 + t];
@@ -1269,15 +1286,21 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
         const float4 c = *reinterpret_cast<const float4*>(crow + r);
         const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 4; ++t) {
+          if constexpr (NL % 4 == 0) {
 #pragma unroll
-          for (int l4 = 0; l4 < NL; l4 += 4) {
-            const float4 gv = *reinterpret_cast<const float4*>(Gk + (r + t) * NL + l4);
-            o[l4] = fmaf(cv[t], gv.x, o[l4]);
-            o[l4 + 1] = fmaf(cv[t], gv.y, o[l4 + 1]);
-            o[l4 + 2] = fmaf(cv[t], gv.z, o[l4 + 2]);
-            o[l4 + 3] = fmaf(cv[t], gv.w, o[l4 + 3]);
+            for (int l4 = 0; l4 < NL; l4 += 4) {
+              const float4 gv = *reinterpret_cast<const float4*>(Gk + (r + t) * NL + l4);
+              o[l4] = fmaf(cv[t], gv.x, o[l4]);
+              o[l4 + 1] = fmaf(cv[t], gv.y, o[l4 + 1]);
+              o[l4 + 2] = fmaf(cv[t], gv.z, o[l4 + 2]);
+              o[l4 + 3] = fmaf(cv[t], gv.w, o[l4 + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int jl = 0; jl < NL; ++jl) o[jl] = fmaf(cv[t], Gk[(r + t) * NL + jl], o[jl]);
           }
+        }
       }
       if constexpr (KS == 2) {
 #pragma unroll
@@ -1286,15 +1309,17 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, co
       if (q >= nrow || kpart != 0) continue;
       const int64_t col = (int64_t)q * NL;
       if (s1 - s0 > HEAVY_POS) {
-#pragma unroll
-        for (int l4 = 0; l4 < NL; l4 += 4)
-          *reinterpret_cast<float4*>(a.Yu + (int64_t)u * npad + col + l4) = make_float4(o[l4], o[l4 + 1], o[l4 + 2], o[l4 + 3]);
+        st_vec<NL>(a.Yu + (int64_t)u * npad + col, o);
       } else if (col < emb) {
         for (int s = s0; s < s1; ++s) {
           float* orow = a.out + (int64_t)__ldg(a.spos + s) * emb + col;
+          if constexpr (NL % 4 == 0) {
+            st_vec<NL>(orow, o);
+          } else {  // (rows are truncated to emb_dim: the last block may be partial)
 #pragma unroll
-          for (int l4 = 0; l4 < NL; l4 += 4)
-            *reinterpret_cast<float4*>(orow + l4) = make_float4(o[l4], o[l4 + 1], o[l4 + 2], o[l4 + 3]);
+            for (int jl = 0; jl < NL; ++jl)
+              if (col + jl < emb) orow[jl] = o[jl];
+          }
         }
       }
     }
@@ -1385,10 +1410,15 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
 #pragma unroll 8
       for (int q = 0; q < nrow; ++q) {
         float yv[NL], cv[RPL];
+        if constexpr (NL % 4 == 0) {
 #pragma unroll
-        for (int l4 = 0; l4 < NL; l4 += 4) {
-          const float4 x = *reinterpret_cast<const float4*>(Ys + q * NL + l4);
-          yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+          for (int l4 = 0; l4 < NL; l4 += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(Ys + q * NL + l4);
+            yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) yv[jl] = Ys[q * NL + jl];
         }
 #pragma unroll
         for (int i = 0; i < RPL; ++i) cv[i] = buf[q * (K + 4) + r0 + i];
@@ -1399,10 +1429,7 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
       }
       float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
 #pragma unroll
-      for (int i = 0; i < RPL; ++i)
-#pragma unroll
-        for (int l4 = 0; l4 < NL; l4 += 4)
-          *reinterpret_cast<float4*>(wdst + i * NL + l4) = make_float4(wv[i][l4], wv[i][l4 + 1], wv[i][l4 + 2], wv[i][l4 + 3]);
+      for (int i = 0; i < RPL; ++i) st_vec<NL>(wdst + i * NL, wv[i]);
     }
     __syncwarp();
   }
@@ -1527,11 +1554,13 @@ __global__ void k_fused_reduce_gsplit(DevCfg c, int F, int split, int split_rows
 }
 
 // The (K, BN, RP, NL) instantiations compiled into the library (engine.cu
-// FUSED_SWITCH): papers, products / sweep32, small, billion, sweep16,
-// sweep64, sweep128, sweep8.
+// FUSED_SWITCH): papers, products / sweep32, small (and the paper's Table-4
+// arxiv / papers100M shapes at R = 16), billion, sweep16, sweep64, sweep128,
+// sweep8, the Table-4 arxiv / papers100M shapes (n = (8,4,4)) at R = 32 and
+// 64, and the Table-4 products shape (n = (4,5,5), NC = 5R) at R = 32 and 64.
 #define TT_FUSED_SHAPES(X) \
   X(64, 128, 4, 4) X(32, 128, 4, 8) X(16, 64, 8, 4) X(32, 128, 16, 4) X(16, 64, 4, 8) X(64, 128, 4, 8) X(128, 64, 4, 8) \
-  X(128, 128, 4, 8) X(8, 32, 4, 8)
+  X(128, 128, 4, 8) X(8, 32, 4, 8) X(32, 128, 8, 4) X(64, 128, 8, 4) X(32, 32, 4, 5) X(64, 64, 4, 5)
 #define TT_FUSED_FWD_SHAPES(X) TT_FUSED_SHAPES(X)
 
 inline bool fused_shape_compiled(int K, int BN, int RP, int NL) {
@@ -1554,6 +1583,9 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   if (K == 32 && NC % 128 == 0) BN = 128;
   if (K == 64 && NC % 128 == 0) BN = 128;
   if (K == 128 && NC % 64 == 0) BN = 64;  // 64-column blocks: two CTAs per SM at rank 128
+  // column counts that are no multiple of 128 (NC = n_F R with n_F = 5 in the
+  // paper's Table-4 products shape): one core-F column block of K columns each
+  if (!BN && (K == 32 || K == 64) && NC % K == 0) BN = (int)K;
   if (!BN || !fused_shape_compiled((int)K, BN, (int)RP, (int)NL)) return false;
   if (c.emb_dim % 4 || c.npad % 4 || c.npad > 512) return false;
   for (int k = 0; k < c.d; ++k)

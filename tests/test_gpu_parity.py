@@ -72,6 +72,16 @@ SHAPES = {
     "sweep128": (lambda: C.WORKLOADS["sweep128"]["cfg"](), 512, "locality"),
     "billion": (lambda: C.WORKLOADS["billion"]["cfg"](), 512, "zipf"),
     "ragged": (lambda: C.plan_factorization(1000, 30, [7, 11, 13], [2, 3, 5], [1, 5, 3, 1]), 700, "zipf"),
+    # the paper's Table 4: ogbn-arxiv (55,55,56)/(8,4,4) and
+    # ogbn-papers100M (480,500,500)/(8,4,4) at R = 32 and 64
+    "arxivT4_r32": (lambda: C.plan_factorization(169_363, 128, [55, 55, 56], [8, 4, 4], [1, 32, 32, 1]), 1024, "uniform"),
+    "papersT4_r64": (lambda: C.plan_factorization(111_059_956, 128, [480, 500, 500], [8, 4, 4], [1, 64, 64, 1]), 1024,
+                     "zipf"),
+    # ogbn-products (125,140,140)/(4,5,5), dim 100: n_d = 5, NC = 5R
+    "productsT4_r32": (lambda: C.plan_factorization(2_449_029, 100, [125, 140, 140], [4, 5, 5], [1, 32, 32, 1]), 2048,
+                       "zipf"),
+    "productsT4_r64": (lambda: C.plan_factorization(2_449_029, 100, [125, 140, 140], [4, 5, 5], [1, 64, 64, 1]), 1024,
+                       "zipf"),
 }
 
 
@@ -79,7 +89,8 @@ SHAPES = {
 # ragged test shapes run the generic path).  tests/test_instantiations.py
 # checks that every compiled (K, BN, RP, NL) instantiation is reached by one
 # of these.
-FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep16", "sweep32", "sweep64", "sweep128", "billion"}
+FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep16", "sweep32", "sweep64", "sweep128", "billion",
+                "arxivT4_r32", "papersT4_r64", "productsT4_r32", "productsT4_r64"}
 
 # shapes with tcgen05 kernels (rank >= 32)
 TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64", "sweep128")

@@ -36,6 +36,8 @@ def _block(K, NC, wide=False):
             return 128
         if not wide and NC % 64 == 0:
             return 64
+    if not wide and K in (32, 64) and NC % K == 0:
+        return K
     return 0
 
 
