@@ -444,15 +444,19 @@ def main():
                       "tolerance": "|x - x_ref| <= 1e-5 a_ref (same bound as the FP32 path; tests/test_gpu_parity.py)",
                       "step_tflops": tf_ / (tc_ms * 1e-3) / 1e12,
                       "roofline": {
-                          "bound": "tensor", "kernel": "k_tc_bwd", "unit": "TFLOP/s",
+                          "bound": "tensor", "kernel": tc_run["kernels"]["bwd"] or "k_tc_bwd", "unit": "TFLOP/s",
                           "achieved": bwd_flops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None,
                           "bf16_mma_tflops": mma_flops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None,
                           "peak": bf16_peak, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst)",
-                          "frac": (mma_flops / (bwd_ms * 1e-3) / 1e12 / bf16_peak) if (bwd_ms > 0 and bf16_peak) else None,
-                          "traffic": _traffic(name, "k_tc_bwd"), "flops_per_launch": bwd_flops, "ms_per_launch": bwd_ms,
-                          "note": "frac = issued BF16 MMA FLOPs (6 per algorithmic MAC of dG_F and dA) over the "
-                                  "dense BF16 peak; the kernel is bound by forming dC on the CUDA cores (latency of "
-                                  "the per-ID loads), not by the tensor pipe (DESIGN.md c2)"},
+                          "frac": (bwd_flops / (bwd_ms * 1e-3) / 1e12 / bf16_peak) if (bwd_ms > 0 and bf16_peak) else None,
+                          "issued_mma_frac": (mma_flops / (bwd_ms * 1e-3) / 1e12 / bf16_peak) if (bwd_ms > 0 and bf16_peak) else None,
+                          "traffic": _traffic(name, tc_run["kernels"]["bwd"] or "k_tc_bwd"), "flops_per_launch": bwd_flops,
+                          "ms_per_launch": bwd_ms,
+                          "note": "frac = algorithmic FLOPs (4 U_F c_F + 2 U_d c_d) over the dense BF16 peak; "
+                                  "issued_mma_frac = the BF16 MMA FLOPs actually issued (6 per algorithmic MAC of "
+                                  "dG_F and dA, the BF16x3 split) over the same peak; the kernel is bound by forming "
+                                  "dC on the CUDA cores (latency of the per-ID loads), not by the tensor pipe "
+                                  "(DESIGN.md c2)"},
                       "gpu_launches": tc_run["launches"]}
         emb.set_path(a.path)
 
