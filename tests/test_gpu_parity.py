@@ -77,6 +77,10 @@ SHAPES = {
     "arxivT4_r32": (lambda: C.plan_factorization(169_363, 128, [55, 55, 56], [8, 4, 4], [1, 32, 32, 1]), 1024, "uniform"),
     "papersT4_r64": (lambda: C.plan_factorization(111_059_956, 128, [480, 500, 500], [8, 4, 4], [1, 64, 64, 1]), 1024,
                      "zipf"),
+    # emb_dim < prod(n): rows truncated (tt_embedding.cpp:122), upstream zero-padded
+    # (autodiff.cpp:96-97) on the fused path
+    "papers_trunc": (lambda: C.plan_factorization(111_059_956, 120, [480, 481, 482], [4, 8, 4], [1, 64, 64, 1]), 1024,
+                     "zipf"),
     # ogbn-products (125,140,140)/(4,5,5), dim 100: n_d = 5, NC = 5R
     "productsT4_r32": (lambda: C.plan_factorization(2_449_029, 100, [125, 140, 140], [4, 5, 5], [1, 32, 32, 1]), 2048,
                        "zipf"),
@@ -90,10 +94,10 @@ SHAPES = {
 # checks that every compiled (K, BN, RP, NL) instantiation is reached by one
 # of these.
 FUSED_SHAPES = {"small", "products", "papers", "sweep8", "sweep16", "sweep32", "sweep64", "sweep128", "billion",
-                "arxivT4_r32", "papersT4_r64", "productsT4_r32", "productsT4_r64"}
+                "arxivT4_r32", "papersT4_r64", "productsT4_r32", "productsT4_r64", "papers_trunc"}
 
 # shapes with tcgen05 kernels (rank >= 32)
-TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64", "sweep128")
+TC_SHAPES = ("products", "papers", "billion", "sweep32", "sweep64", "sweep128", "papers_trunc")
 
 
 @pytest.mark.parametrize("name", list(SHAPES))
