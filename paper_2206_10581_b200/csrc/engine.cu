@@ -148,6 +148,7 @@ struct tt_engine {
 
   // bookkeeping
   bool plan_valid = false;
+  bool psave_valid = false;  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
   int64_t cores_version = 0, plan_version = -1;
   int64_t batch_count = 0;
   int64_t launches = 0;
@@ -750,6 +751,26 @@ bool bwdk32_enabled(int rp) {
   return (rp == 4 && (mask & 1)) || (rp == 16 && (mask & 2));
 }
 
+// TT_TCBWD: the tensor backward at K <= 64.  1 (default): k_tc_bwd (one CTA
+// per item, dC formed in the kernel); 2: the persistent k_tc_bwd2 forming dC
+// itself (same time: 0.764 vs 0.765 ms at papers); 3: k_fused_wdc forms
+// dC = dP_F (with the last core's W_u) over the saved P_F blocks and
+// k_tc_bwd2<..., true> streams it (0.27 + 0.71 ms: slower).  Measured phase
+// split of k_tc_bwd2 (scripts/tc_bwd2_phases.py): per 128-row tile ~17.5k
+// cycles against 4.6k of MMAs -- the roles run one after another.
+int tcbwd_mode() {
+  static const int m = [] {
+    const char* e = getenv("TT_TCBWD");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return m;
+}
+// k_fused_wdc's shape condition (PIPE blocks, K in {32, 64})
+static bool wdc_ok(const FusedShape& f) {
+  return (f.K == 32 || f.K == 64) && (int64_t)f.RP * f.nF * f.K <= 2048 && (int64_t)f.RP * f.nF * f.NL <= 256 &&
+         f.NL % 4 == 0;
+}
+
 // TT_BWDWS = bit mask of the level-F shapes using the warp-specialised
 // backward (1: K = 32 with RP = 16, 2: K = 32 with RP = 4; default 1); 0
 // selects k_fused_bwd_k32 / k_fused_bwd
@@ -1052,6 +1073,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   if (d_out)
     LAUNCH(k_scatter_heavy, grid_for((h->B + 31) / 32 * 32, 256, 148 * 8), 256, 0, s, (int)h->B, c.emb_dim, c.npad, h->flag,
            h->spos, h->seg, h->F.Yu, d_out, h->st);
+  h->psave_valid = true;
   return TT_OK;
 }
 
@@ -1078,6 +1100,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   a.CH = f.CHB;
   a.mode = 0;
   int rc;
+  bool wdc_done = false;  // W_u already formed (k_fused_wdc)
   {
     Phase ph(h, 2, s);
     if (h->last_path == 2 && f.K == 128) {
@@ -1132,13 +1155,49 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
       }
       const int grid = (int)(c.m[f.F] * h->ts.ncbb * a.split);
       rc = TT_OK;
-      if (false) {
-      }
+      const int mode = tcbwd_mode();
+      if (mode == 3 && wdc_ok(f)) {
+        const int64_t cap = h->cap;
+        const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (f.K + 4) + f.RP * f.nF * f.NL);
+        if (false) {
+        }
+#define TT_WDC_CASE(k_, nl_)                                                                                        \
+  else if (f.K == k_ && f.NL == nl_) {                                                                              \
+    CU(cudaFuncSetAttribute((k_fused_wdc<k_, nl_>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_));       \
+    LAUNCH((k_fused_wdc<k_, nl_>), h->nsm, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap);    \
+  }
+        TT_WDC_CASE(64, 4) TT_WDC_CASE(64, 8) TT_WDC_CASE(32, 4) TT_WDC_CASE(32, 8)
+#undef TT_WDC_CASE
+        wdc_done = true;
+        h->psave_valid = false;
+        const int pgrid = std::min(grid, h->nsm);
+        const size_t smem2 = tc_bwd2_smem(f.K, 128);
+        if (false) {
+        }
+#define TT_TC_BWD3_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd2<k_, 128, rp_, nl_, true>), smem2, pgrid, TCB2_THREADS, s, a);
+        TT_TC_SHAPES(TT_TC_BWD3_CASE)
+#undef TT_TC_BWD3_CASE
+        h->bwd_kernel = "k_tc_bwd2";
+      } else if (mode == 2) {
+        const int pgrid = std::min(grid, h->nsm);
+        const size_t smem2 = tc_bwd2_smem(f.K, 128);
+        if (false) {
+        }
+#define TT_TC_BWD2_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd2<k_, 128, rp_, nl_, false>), smem2, pgrid, TCB2_THREADS, s, a);
+        TT_TC_SHAPES(TT_TC_BWD2_CASE)
+#undef TT_TC_BWD2_CASE
+        h->bwd_kernel = "k_tc_bwd2";
+      } else {
+        if (false) {
+        }
 #define TT_TC_BWD_CASE(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd<k_, 128, rp_, nl_>), h->ts.smem_bwd, grid, TCB_THREADS, s, a);
-      TT_TC_SHAPES(TT_TC_BWD_CASE)
+        TT_TC_SHAPES(TT_TC_BWD_CASE)
 #undef TT_TC_BWD_CASE
-      h->bwd_kernel = "k_tc_bwd";
+        h->bwd_kernel = "k_tc_bwd";
+      }
       if (a.split > 1)
         LAUNCH(k_fused_reduce_gsplit, grid_for(c.m[f.F] * c.slice[f.F] / 4, 256, 148 * 8), 256, 0, s, c, f.F, a.split,
                a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);
@@ -1171,7 +1230,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
       LAUNCH((k_fused_w<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
     } \
   }
-  if (false) {
+  if (wdc_done) {
   }
   TT_FUSED_SHAPES(TT_W_CASE)
 #undef TT_W_CASE
@@ -1256,6 +1315,10 @@ int do_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   h->gF_ready = false;
   if (h->dense) CU(cudaMemsetAsync(h->grads, 0, sizeof(float) * (size_t)(h->dc.nparams + h->ntc), s));
   int rc;
+  if (h->last_path >= 1 && !h->psave_valid) {  // a second backward of one forward: P_F again
+    rc = fused_forward(h, nullptr, s);
+    if (rc) return rc;
+  }
   if (h->last_path >= 1)
     rc = fused_backward(h, d_up, s);
   else

@@ -124,18 +124,19 @@ __host__ __device__ __forceinline__ int group_chunks(int n, int RP, int split, i
   return (int)(by_rows < 1 ? 1 : (by_rows < split ? by_rows : split));
 }
 
-__device__ __forceinline__ bool work_item(const FusedArgs& a, int& g, int& cb, int& chunk, int& g0, int& g1) {
+__device__ __forceinline__ bool work_item_at(const FusedArgs& a, int it, int& g, int& cb, int& chunk, int& g0,
+                                             int& g1) {
   if (a.split <= 1) {
-    g = blockIdx.x / a.ncb;
-    cb = blockIdx.x - g * a.ncb;
+    g = it / a.ncb;
+    cb = it - g * a.ncb;
     chunk = 0;
     g0 = a.goffF[g];
     g1 = a.goffF[g + 1];
     return g0 < g1;
   }
   const int split = a.split;
-  const int gc = blockIdx.x / a.ncb;
-  cb = blockIdx.x - gc * a.ncb;
+  const int gc = it / a.ncb;
+  cb = it - gc * a.ncb;
   g = gc / split;
   chunk = gc - g * split;
   const int n0 = a.goffF[g], n = a.goffF[g + 1] - n0;
@@ -144,6 +145,9 @@ __device__ __forceinline__ bool work_item(const FusedArgs& a, int& g, int& cb, i
   g0 = n0 + (int)(((int64_t)n * chunk) / nch);
   g1 = n0 + (int)(((int64_t)n * (chunk + 1)) / nch);
   return g0 < g1;
+}
+__device__ __forceinline__ bool work_item(const FusedArgs& a, int& g, int& cb, int& chunk, int& g0, int& g1) {
+  return work_item_at(a, blockIdx.x, g, cb, chunk, g0, g1);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1430,6 +1434,144 @@ __global__ void __launch_bounds__(SK_WARPS * 32, 2) k_fused_w(FusedArgs a, const
       float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
 #pragma unroll
       for (int i = 0; i < RPL; ++i) st_vec<NL>(wdst + i * NL, wv[i]);
+    }
+    __syncwarp();
+  }
+}
+
+// k_fused_w plus dC = dP_F for the tensor backward (path tc, round 2): per
+// level-F node p, dC[q][r] = sum over p's distinct IDs u of
+// sum_jl dY_u[q][jl] G_{d-1}[r, i_d(u), jl], written over p's saved P_F block
+// (same layout: row q = a n_F + jf, column r) once every W_u of p has read it.
+// k_tc_bwd2<..., true> then streams dC tiles instead of forming them from
+// dependent L2 loads.  Warps own node-aligned runs of IDs (a run starts at the
+// first ID of a node: cstartF), so each block is written by one warp.  Lane
+// owns rank columns r0 .. r0 + RPL of both W_u and dC.
+template <int K, int NL>
+__global__ void __launch_bounds__(SK_WARPS * 32, 1) k_fused_wdc(FusedArgs a, const int* __restrict__ counts,
+                                                             const int* __restrict__ parentL) {
+  TT_PDL_ENTRY();
+  extern __shared__ __align__(16) float sk_smem[];
+  if (tt_failed(a.st)) return;
+  static_assert(K == 32 || K == 64, "rank");
+  constexpr int RPL = K / 32;
+  constexpr int QMAX = 2048 / K;  // block rows (PIPE blocks: <= 2048 floats)
+  constexpr int PB = 16;
+  constexpr int YB = 2;
+  const int U = ld_count(&counts[a.c.d - 1]);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int RP = a.RP, nF = a.nF, nrow = RP * nF;
+  const int n4 = nrow * (K / 4), y4 = nrow * NL / 4;
+  float* buf = sk_smem + wib * (nrow * (K + 4) + nrow * NL);
+  float* Ys = buf + nrow * (K + 4);
+  const int64_t npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const int r0 = lane * RPL;
+  float4 pv[PB], yr[YB];
+  float gr[RPL * NL];
+  auto issue = [&](int u, int p, bool block) {  // ID u's (prefix block,) dY row and slice rows
+    if (block) {
+      const float4* src = reinterpret_cast<const float4*>(a.Psave + (int64_t)p * RP * a.NC);
+#pragma unroll
+      for (int b = 0; b < PB; ++b)
+        if (b * 32 + lane < n4) pv[b] = __ldg(src + b * 32 + lane);
+    }
+    const float4* ys = reinterpret_cast<const float4*>(a.dY + (int64_t)u * npad);
+#pragma unroll
+    for (int b = 0; b < YB; ++b)
+      if (b * 32 + lane < y4) yr[b] = __ldg(ys + b * 32 + lane);
+    const float4* gs = reinterpret_cast<const float4*>(Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL);
+#pragma unroll
+    for (int b = 0; b < RPL * NL / 4; ++b) {
+      const float4 x = __ldg(gs + b);
+      gr[4 * b] = x.x; gr[4 * b + 1] = x.y; gr[4 * b + 2] = x.z; gr[4 * b + 3] = x.w;
+    }
+  };
+  // node-aligned run: the first ID at or after v that starts a node
+  auto node_start = [&](int v) {
+    if (v <= 0) return 0;
+    if (v >= U) return U;
+    const int p = __ldg(parentL + v);
+    const int c0 = __ldg(a.cstartF + p);
+    return c0 == v ? v : __ldg(a.cstartF + p + 1);
+  };
+  const int per = (U + nwarps - 1) / nwarps;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int u = node_start(min(U, w * per));
+  const int uend = node_start(min(U, (w + 1) * per));
+  float dc[QMAX][RPL];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q)
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) dc[q][i] = 0.f;
+  int staged = -1;
+  int pn = u < uend ? __ldg(parentL + u) : 0;
+  if (u < uend) issue(u, pn, true);
+  for (; u < uend; ++u) {
+    const int p = pn;
+    const int un = u + 1;
+    if (un < uend) pn = __ldg(parentL + un);
+    if (p != staged) {
+#pragma unroll
+      for (int b = 0; b < PB; ++b) {
+        const int i = b * 32 + lane;
+        if (i < n4) {
+          const int row = i / (K / 4), c4 = i - row * (K / 4);
+          *reinterpret_cast<float4*>(buf + row * (K + 4) + c4 * 4) = pv[b];
+        }
+      }
+      staged = p;
+    }
+#pragma unroll
+    for (int b = 0; b < YB; ++b)
+      if (b * 32 + lane < y4) reinterpret_cast<float4*>(Ys)[b * 32 + lane] = yr[b];
+    float g[RPL * NL];
+#pragma unroll
+    for (int i = 0; i < RPL * NL; ++i) g[i] = gr[i];
+    __syncwarp();
+    const bool last = un >= uend || pn != p;
+    if (un < uend) issue(un, pn, pn != p);  // lands while this ID is computed
+    float wv[RPL][NL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i)
+#pragma unroll
+      for (int jl = 0; jl < NL; ++jl) wv[i][jl] = 0.f;
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      if (q < nrow) {
+        float yv[NL], cv[RPL];
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(Ys + q * NL + l4);
+          yv[l4] = x.x; yv[l4 + 1] = x.y; yv[l4 + 2] = x.z; yv[l4 + 3] = x.w;
+        }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) cv[i] = buf[q * (K + 4) + r0 + i];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) {
+            wv[i][jl] = fmaf(cv[i], yv[jl], wv[i][jl]);
+            dc[q][i] = fmaf(yv[jl], g[i * NL + jl], dc[q][i]);
+          }
+      }
+    }
+    float* wdst = a.W + (int64_t)u * K * NL + r0 * NL;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) st_vec<NL>(wdst + i * NL, wv[i]);
+    if (last) {  // p's block is in smem (and every W_u of p done): dC over it
+      float* dst = a.Psave + (int64_t)p * RP * a.NC + r0;
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        if (q < nrow) {
+          if constexpr (RPL == 2) *reinterpret_cast<float2*>(dst + q * K) = make_float2(dc[q][0], dc[q][1]);
+          else dst[q * K] = dc[q][0];
+        }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) dc[q][i] = 0.f;
+      }
     }
     __syncwarp();
   }

@@ -625,6 +625,358 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) k_tc_bwd(FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Backward, persistent (round 2, the default at K <= 64): the same tiles and
+// products as k_tc_bwd, with
+//   * a warp of its own (warp 8) that only issues the MMAs: in k_tc_bwd the
+//     two issuing threads sat in dC-forming warps, and an issue that blocks on
+//     a full tensor-pipe queue delayed their warps' next dC unit, so the MMAs
+//     added to the tile time instead of running under the dC formation.  Nine
+//     warps keep 168 registers per thread (17 warps would cap it at 96: five
+//     warps on one SM sub-partition), so each of the 256 worker threads forms
+//     two dC units of one node, column chunks c8 and c8 + 8 -- the same IDs and
+//     last-core rows, two upstream column blocks: one latency chain, twice the
+//     FMAs;
+//   * dA double-buffered in TMEM: tile t's dA epilogue runs under tile t+1's
+//     MMAs (TMEM: dG_F^T [0, K), dA [K, 2K) and [2K, 3K));
+//   * one CTA per SM walking the items it = blockIdx.x + k * gridDim.x, with
+//     the node metadata of the next node batch staged into the other of two
+//     buffers and the next tile's A rows and dC units formed under the current
+//     tile's MMAs across item boundaries: the per-item prologue (node
+//     metadata chain, first tile) no longer stands alone on the SM.
+// Per tile: wait MMA(t-1) -> [new item: drain dG_F^T of the last item,
+// stage the slice block] -> store A(t), dC(t) planes -> barrier -> issue
+// MMA(t) | dA epilogue of t-1, next batch's metadata, A(t+1) loads, dC(t+1).
+constexpr int TCB2_WORKERS = 256;
+constexpr int TCB2_THREADS = TCB2_WORKERS + 32;
+constexpr size_t TC_META2 = 2 * (sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 8)) + sizeof(int) * 40 + 64;
+inline size_t tc_bwd2_smem(int K, int BN) {
+  return 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + 3 * (size_t)TC_BM * BN * 2 + TC_META2;
+}
+
+struct BwdCursor {
+  int it, g, cb, chunk, g0, g1, nb0, nbn, tb;
+  // first non-empty item at or after `it` (stride gridDim.x); false: none left
+  __device__ __forceinline__ bool seek_item(const FusedArgs& a, int nitems) {
+    for (; it < nitems; it += gridDim.x)
+      if (work_item_at(a, it, g, cb, chunk, g0, g1)) {
+        nb0 = g0;
+        nbn = min(FB_NB, g1 - g0);
+        tb = 0;
+        return true;
+      }
+    return false;
+  }
+  // next tile; sets new_batch / new_item
+  __device__ __forceinline__ bool advance(const FusedArgs& a, int nitems, int npt, bool& new_batch, bool& new_item) {
+    tb += npt;
+    new_batch = new_item = false;
+    if (tb < nbn) return true;
+    new_batch = true;
+    nb0 += FB_NB;
+    tb = 0;
+    if (nb0 < g1) {
+      nbn = min(FB_NB, g1 - nb0);
+      return true;
+    }
+    new_item = true;
+    it += gridDim.x;
+    return seek_item(a, nitems);
+  }
+};
+
+// dC tile of the LDC variant: 128 rows x BN columns of the dC blocks that
+// k_fused_wdc wrote over P_F, 8 units of 8 floats per worker thread, unit u:
+// column chunk (u / 8) % (BN / 8), row 8 (u / 8 / (BN / 8)) + u % 8
+template <int BN>
+struct DTileRegs {
+  static constexpr int N = TC_BM * BN / 8 / TCB2_WORKERS;
+  float4 v[N][2];
+};
+
+template <int K, int BN, int RP, int NL, bool LDC>
+__global__ void __launch_bounds__(TCB2_THREADS, 1) k_tc_bwd2(FusedArgs a) {
+  TT_PDL_ENTRY();
+  static_assert(BN == 128 && K % 16 == 0 && K <= 64 && 64 % K == 0 && TC_BM % RP == 0 && RP % 4 == 0,
+                "tcgen05 backward shape");
+  constexpr int W = TCB2_WORKERS;  // warps 0-7: dC, planes, epilogues; warp 8: MMA issue
+  constexpr int NPT = TC_BM / RP;
+  constexpr uint32_t TCOLS = 3 * K <= 128 ? 128 : 256;
+  constexpr int EC = K / 2;  // epilogue columns per warp (8 warps = 4 lane quadrants x 2 column halves)
+  static_assert(EC == 16 || EC == 32, "epilogue column slice");
+  extern __shared__ __align__(128) uint8_t tsm[];
+  uint8_t* S0 = tsm;
+  uint8_t* S1 = S0 + K * BN * 2;
+  uint8_t* S2 = S1 + K * BN * 2;
+  uint8_t* A0 = S2 + K * BN * 2;
+  uint8_t* A1 = A0 + TC_BM * K * 2;
+  uint8_t* A2 = A1 + TC_BM * K * 2;
+  uint8_t* D0 = A2 + TC_BM * K * 2;
+  uint8_t* D1 = D0 + TC_BM * BN * 2;
+  uint8_t* D2 = D1 + TC_BM * BN * 2;
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(D2 + TC_BM * BN * 2);  // [2][FB_NB]
+  int* s_node = reinterpret_cast<int*>(s_aoff + 2 * FB_NB);           // [2][FB_NB]
+  int* s_cs0 = s_node + 2 * FB_NB;                                    // [2][FB_NB]
+  int* s_pref = s_cs0 + 2 * FB_NB;                                    // [2][FB_NB + 8]
+  int* s_wsum = s_pref + 2 * (FB_NB + 8);                             // [40]
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+
+  if (tt_failed(a.st)) return;
+  const int nitems = (int)a.c.m[a.F] * a.ncb * (a.split > 1 ? a.split : 1);
+  BwdCursor cur;
+  cur.it = blockIdx.x;
+  if (!cur.seek_item(a, nitems)) return;
+  // TT_TC_TRACE=1: thread 0's clock cycles per phase, summed per CTA into
+  // a.dbg[blockIdx.x * 16 + phase] (scripts/tc_trace.py with BWD2=1)
+  const bool trace = a.dbg != nullptr && threadIdx.x == 0;
+  long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  auto mark = [&](int k) {
+    if (trace) {
+      const long long now = clock64();
+      ph[k] += now - tlast;
+      tlast = now;
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool worker = threadIdx.x < W;
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  const int eslice = ((warp >> 2) & 1) * EC;
+  if (warp == 0) tc::tmem_alloc<TCOLS>(&tslot);
+  if (threadIdx.x == 32) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  const int nF = a.nF;
+  const int64_t npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const uint32_t id_g = tc::idesc_bf16(BN, K, 1, 1);
+  const uint32_t id_a = tc::idesc_bf16(TC_BM, K, 0, 0);
+  ATileRegs<K, W> ar;
+  // this thread's dC units: unit0 = thread index with a 0 inserted at bit 4,
+  // unit1 = unit0 | 16 (column chunk c8 + 8, same rows); k_tc_bwd's unit bit
+  // layout, so each 8-thread store phase stays conflict-free
+  const int x = threadIdx.x & (W - 1);
+  const int unit = (x & 15) | ((x >> 4) << 5);
+  const int c8 = (unit & 3) + 4 * ((unit >> 3) & 3);  // < 8
+  const int rg = ((unit >> 2) & 1) + 2 * (unit >> 5);
+  const int rot = unit & 3;
+  const int m0 = rg * 4, uj = m0 / RP, a0 = m0 - uj * RP;
+  constexpr int JF1 = 64 / K;  // unit1's core-F column block offset
+  auto compute_dC = [&](const int* pref, const int* cs0s, int cb, int tb, int nn, float (&acc)[2][4][8]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[v][i][t] = 0.f;
+    if (uj >= nn || (a.mode & 16)) return;
+    const int col0 = cb * BN + c8 * 8, jf = col0 / K, r0 = col0 - jf * K;
+    const int fA = pref[tb + uj], fB = pref[tb + uj + 1], cs0 = cs0s[tb + uj];
+    for (int f = fA; f < fB; ++f) {
+      const int u = cs0 + (f - fA);
+      const float* Gp = Gl + (int64_t)__ldg(a.digitL + u) * sliceL + r0 * NL;
+      const float* Yp = a.dY + (int64_t)u * npad + ((int64_t)a0 * nF + jf) * NL;
+      float yv[2][4][NL];
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ii = (i + rot) & 3;
+#pragma unroll
+          for (int l4 = 0; l4 < NL; l4 += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(Yp + (int64_t)ii * nF * NL + v * JF1 * NL + l4));
+            yv[v][i][l4] = q.x; yv[v][i][l4 + 1] = q.y; yv[v][i][l4 + 2] = q.z; yv[v][i][l4 + 3] = q.w;
+          }
+        }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        float gv[NL];
+#pragma unroll
+        for (int l4 = 0; l4 < NL; l4 += 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(Gp + t * NL + l4));
+          gv[l4] = q.x; gv[l4 + 1] = q.y; gv[l4 + 2] = q.z; gv[l4 + 3] = q.w;
+        }
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float s = acc[v][i][t];
+#pragma unroll
+            for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[v][i][jl], gv[jl], s);
+            acc[v][i][t] = s;
+          }
+      }
+    }
+  };
+  const int em = 32 * (warp & 3) + lane;  // epilogue row (TMEM lane)
+  const int emj = em / RP, ema = em - emj * RP;
+  auto tmem_row = [&](uint32_t taddr, float (&v)[EC]) {
+    if constexpr (EC == 32) {
+      uint32_t r[32];
+      tc::tmem_ld16_async(taddr, r);
+      tc::tmem_ld16_async(taddr + 16, r + 16);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    } else {
+      tc::tmem_ld16(taddr, v);
+    }
+  };
+  // dG_F^T of a finished item -> its slice block (or its chunk's partial)
+  auto drain_dG = [&](uint32_t tm, int g, int cb, int chunk) {
+    const int col = 32 * (warp & 3) + lane;
+    float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN + col;
+    float v[EC];
+    tmem_row(tm + lane_base + eslice, v);
+#pragma unroll
+    for (int i = 0; i < EC; ++i) gdst[(int64_t)(eslice + i) * a.NC] = v[i];
+  };
+  auto drain_dA = [&](uint32_t tm, int buf, float* dst) {
+    float v[EC];
+    tmem_row(tm + lane_base + K + buf * K + eslice, v);
+    if (dst && !(a.mode & 4)) {
+#pragma unroll
+      for (int q = 0; q < EC / 4; ++q)
+        *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  };
+  auto store_dC = [&](const float (&acc)[2][4][8]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc::store_split8(D0, D1, D2, m0 + ((i + rot) & 3), (c8 + 8 * v) * 8, BN, acc[v][i]);
+  };
+
+  // prologue: first item's slice block, first batch's metadata, first tile
+  if (worker) tc_stage_slice<K, BN, W>(a, cur.g, cur.cb, S0, S1, S2);
+  int mb = 0;
+  tc_prep_nodes<TCB2_THREADS>(a, cur.nb0, cur.nbn, s_node, s_cs0, s_pref, s_aoff, s_wsum);
+  float acc[2][4][8];
+  DTileRegs<BN> dr;
+  auto load_dC = [&](const int* nodes, int cb, int tb, int nn) {
+#pragma unroll
+    for (int i = 0; i < DTileRegs<BN>::N; ++i) {
+      const int u = x + i * W;
+      const int kc = (u >> 3) % (BN / 8), m = ((u >> 3) / (BN / 8)) * 8 + (u & 7);
+      const int j = m / RP;
+      if (j < nn) {
+        const float* src = a.Psave + ((int64_t)nodes[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + kc * 8;
+        dr.v[i][0] = __ldg(reinterpret_cast<const float4*>(src));
+        dr.v[i][1] = __ldg(reinterpret_cast<const float4*>(src + 4));
+      } else {
+        dr.v[i][0] = dr.v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  if (worker) {
+    tc_load_A<K, RP, W>(a, 0, min(NPT, cur.nbn), s_aoff, ar);
+    if constexpr (LDC) load_dC(s_node, cur.cb, 0, min(NPT, cur.nbn));
+    else compute_dC(s_pref, s_cs0, cur.cb, 0, min(NPT, cur.nbn), acc);
+  }
+  mark(8);
+  bool first_of_item = true;
+  int pg = cur.g, pcb = cur.cb, pchunk = cur.chunk;  // item of the last issued tile
+  float* dst_prev = nullptr;
+  uint32_t t = 0;
+  for (;;) {
+    const int nn = min(NPT, cur.nbn - cur.tb);
+    if (t > 0) {
+      tc::mbar_wait(&bar, (t - 1) & 1);  // MMA(t-1) done: planes free, dA(t-1) ready
+      tc::after_sync();
+      mark(0);
+      if (first_of_item && worker) {
+        drain_dG(tslot, pg, pcb, pchunk);
+        tc_stage_slice<K, BN, W>(a, cur.g, cur.cb, S0, S1, S2);
+      }
+      mark(1);
+    }
+    if (worker) {
+      if (!(a.mode & 8)) tc_store_A<K, W>(ar, A0, A1, A2);
+      if constexpr (LDC) {
+#pragma unroll
+        for (int i = 0; i < DTileRegs<BN>::N; ++i) {
+          const int u = x + i * W;
+          const int kc = (u >> 3) % (BN / 8), m = ((u >> 3) / (BN / 8)) * 8 + (u & 7);
+          const float v8[8] = {dr.v[i][0].x, dr.v[i][0].y, dr.v[i][0].z, dr.v[i][0].w,
+                               dr.v[i][1].x, dr.v[i][1].y, dr.v[i][1].z, dr.v[i][1].w};
+          tc::store_split8(D0, D1, D2, m, kc * 8, BN, v8);
+        }
+      } else {
+        store_dC(acc);
+      }
+    }
+    mark(2);
+    tc::fence_async_smem();
+    tc::before_sync();
+    __syncthreads();
+    tc::after_sync();
+    mark(3);
+    const uint32_t tm = tslot;
+    if (!worker) {
+      if (lane == 0) {
+        if (!(a.mode & 2)) {
+          const tc::Operand dcT = tc::mnmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
+          const tc::Operand aB = tc::mnmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
+          tc::mma_x3<TC_BM / 16>(tm, dcT, aB, id_g, !first_of_item);
+          const tc::Operand dcK = tc::kmajor(tc::smem_u32(D0), tc::smem_u32(D1), tc::smem_u32(D2), BN);
+          const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
+          tc::mma_x3<BN / 16>(tm + K + (t & 1) * K, dcK, sT, id_a, false);
+        }
+        tc::commit(&bar);
+      }
+      __syncwarp();
+    } else if (t > 0) {
+      drain_dA(tm, (t - 1) & 1, dst_prev);
+    }
+    mark(4);
+    const int* nodes = s_node + mb * FB_NB;
+    dst_prev = (worker && emj < nn) ? a.dPc + ((int64_t)nodes[cur.tb + emj] * a.ncb + cur.cb) * RP * K + ema * K + eslice
+                                    : nullptr;
+    pg = cur.g;
+    pcb = cur.cb;
+    pchunk = cur.chunk;
+    bool new_batch, new_item;
+    if (!cur.advance(a, nitems, NPT, new_batch, new_item)) break;
+    first_of_item = new_item;
+    if (new_batch) {
+      mb ^= 1;
+      tc_prep_nodes<TCB2_THREADS>(a, cur.nb0, cur.nbn, s_node + mb * FB_NB, s_cs0 + mb * FB_NB,
+                                  s_pref + mb * (FB_NB + 8), s_aoff + mb * FB_NB, s_wsum);
+    }
+    mark(5);
+    if (worker) {
+      const int nn2 = min(NPT, cur.nbn - cur.tb);
+      if (!(a.mode & 8)) tc_load_A<K, RP, W>(a, cur.tb, nn2, s_aoff + mb * FB_NB, ar);
+      if constexpr (LDC) {
+        if (!(a.mode & 16)) load_dC(s_node + mb * FB_NB, cur.cb, cur.tb, nn2);
+      } else {
+        compute_dC(s_pref + mb * (FB_NB + 8), s_cs0 + mb * FB_NB, cur.cb, cur.tb, nn2, acc);
+      }
+    }
+    mark(6);
+    ++t;
+  }
+  // last tile: its dA, then the last item's dG_F
+  tc::mbar_wait(&bar, t & 1);
+  tc::after_sync();
+  if (worker) {
+    drain_dA(tslot, t & 1, dst_prev);
+    drain_dG(tslot, pg, pcb, pchunk);
+  }
+  mark(9);
+  if (trace) {
+    ph[7] = t + 1;
+    for (int k = 0; k < 12; ++k) a.dbg[blockIdx.x * 16 + k] = ph[k];
+  }
+  tc::before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<TCOLS>(tslot);
+}
+
+// ---------------------------------------------------------------------------
 // Backward at rank 128 (the rank sweep's R = 128): 64-column blocks, so the
 // BF16x3 planes fit in 192 KB (S 48 KB, A 96 KB, dC 48 KB; 128-column blocks
 // would need 288 KB).  dG_F is accumulated untransposed, M = 128 (k) x N = 64

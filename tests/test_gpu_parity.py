@@ -379,3 +379,28 @@ def test_forward_rejects_bad_out_buffer():
             emb.forward(idx, bad)
     with pytest.raises(C.InvalidArgument):
         emb.forward(idx.cpu())
+
+
+@pytest.mark.parametrize("path", ["auto", "tc"])
+def test_second_backward_of_one_forward(path):
+    # the tensor backward writes dC over the saved P_F blocks (k_fused_wdc): a
+    # second backward of the same forward recomputes P_F first, and matches
+    # the first bitwise (a different upstream in between)
+    import torch
+    mk, B, dist = SHAPES["papers"]
+    cfg = mk()
+    emb, cores = make(cfg, 41, path)
+    idx = ids_for(cfg, 42, B, dist)
+    up = synth.normal(43, 1, B * cfg.emb_dim).reshape(B, cfg.emb_dim)
+    up2 = synth.normal(43, 2, B * cfg.emb_dim).reshape(B, cfg.emb_dim)
+    ti, tu, tu2 = (torch.tensor(x, device="cuda") for x in (idx, up, up2))
+    emb.forward(ti)
+    emb.backward(tu)
+    emb.sync()
+    g1 = [x.copy() for x in emb._fetch_grads()]
+    emb.backward(tu2)
+    emb.backward(tu)
+    emb.sync()
+    g2 = emb._fetch_grads()
+    for k in range(cfg.d):
+        np.testing.assert_array_equal(g1[k], g2[k])
