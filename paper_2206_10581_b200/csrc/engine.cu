@@ -194,6 +194,9 @@ struct tt_engine {
   // [n_k R_{k+1}] fp32 view of core k, box {128, R_k})
   CUtensorMap tmap[TT_MAXD] = {};
   bool tmap_ok[TT_MAXD] = {};
+  CUtensorMap ps_tmap = {};  // saved P_F / dC blocks as [rows][NC] fp32, box {32, RP}, 128-byte swizzle
+  const void* ps_tmap_ptr = nullptr;
+  int64_t ps_tmap_rows = 0;
 
   // the level-F GEMM kernels of the last forward / backward (tt_main_kernels)
   const char* fwd_kernel = "";
@@ -751,19 +754,35 @@ bool bwdk32_enabled(int rp) {
   return (rp == 4 && (mask & 1)) || (rp == 16 && (mask & 2));
 }
 
-// TT_TCBWD: the tensor backward at K <= 64.  1 (default): k_tc_bwd (one CTA
-// per item, dC formed in the kernel); 2: the persistent k_tc_bwd2 forming dC
-// itself (same time: 0.764 vs 0.765 ms at papers); 3: k_fused_wdc forms
-// dC = dP_F (with the last core's W_u) over the saved P_F blocks and
-// k_tc_bwd2<..., true> streams it (0.27 + 0.71 ms: slower).  Measured phase
-// split of k_tc_bwd2 (scripts/tc_bwd2_phases.py): per 128-row tile ~17.5k
-// cycles against 4.6k of MMAs -- the roles run one after another.
-int tcbwd_mode() {
+// TT_TCBWD: the tensor backward at K <= 64.
+//   4 (default at K = 64): k_fused_wdc forms dC = dP_F (with the last core's
+//     W_u) over the saved P_F blocks; k_tc_bwd3 stages it by TMA and keeps both
+//     dC operands in TMEM (papers 1.62 -> 1.45 ms/step, sweep64 1.05 -> 0.75);
+//   1 (default at K = 32): k_tc_bwd, one CTA per item, dC formed in the kernel
+//     (billion 3.70 vs 4.12 and products 0.258 vs 0.267 with mode 4: there
+//     the extra pass over P_F costs more than the kernel saves);
+//   2: the persistent k_tc_bwd2 forming dC itself (0.764 vs 0.765 ms at papers);
+//   3: k_fused_wdc + k_tc_bwd2 streaming dC through registers (slower).
+// Phase split of k_tc_bwd2 (scripts/tc_bwd2_phases.py): ~17.5k cycles per
+// 128-row tile against 4.6k of MMAs -- its roles run one after another.
+int tcbwd_mode(const FusedShape& f) {
   static const int m = [] {
     const char* e = getenv("TT_TCBWD");
-    return e && *e ? atoi(e) : 1;
+    return e && *e ? atoi(e) : 0;
   }();
-  return m;
+  return m ? m : (f.K == 64 ? 4 : 1);
+}
+// The FFMA backward loads dC formed by k_fused_wdc (mode 1) instead of
+// forming it per tile: TT_FFMA_WDC=1 always, 0 never; default at K = 64 with
+// NL = 8 (the rank sweep's R = 64: 8 IDs per level-F node, 8-wide last-core
+// rows, 0.987 -> 0.856 ms/step).  Measured slower where dC per node is cheap:
+// papers 2.359 -> 2.391, products 0.276 -> 0.284, billion (K = 32) 4.90 -> 5.45.
+bool ffma_wdc_enabled(const FusedShape& f) {
+  static const int m = [] {
+    const char* e = getenv("TT_FFMA_WDC");
+    return e && *e ? atoi(e) : -1;
+  }();
+  return m >= 0 ? m == 1 : (f.K == 64 && f.NL == 8);
 }
 // k_fused_wdc's shape condition (PIPE blocks, K in {32, 64})
 static bool wdc_ok(const FusedShape& f) {
@@ -798,10 +817,7 @@ bool tma_enabled() {
   return on;
 }
 
-// The tensor map of core k for TMA loads of (K x 128) slice blocks; false
-// when the driver entry point is unavailable (the cp.async kernel runs).
-bool core_tmap(tt_engine* h, int k) {
-  if (h->tmap_ok[k]) return true;
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -810,6 +826,37 @@ bool core_tmap(tt_engine* h, int k) {
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
+  return encode;
+}
+
+// The tensor map of the saved level-F blocks (k_tc_bwd3's dC boxes): rows
+// node * RP + a of NC fp32 columns, viewed as [NC / 32][rows][32] so that one
+// box {32, RP, 4} is a node's 128-column block; 128-byte swizzle
+bool psave_tmap(tt_engine* h) {
+  const FusedShape& f = h->fs;
+  const int64_t rows = h->F.cap_nodes * f.RP;
+  if (h->ps_tmap_ptr == h->F.Psave && h->ps_tmap_rows == rows) return true;
+  auto encode = tmap_encoder();
+  if (!encode) return false;
+  // 3-D view [NC / 32 chunks][rows][32]: one box = a node's RP rows x 128 columns
+  const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(f.NC / 32)};
+  const cuuint64_t strides[2] = {(cuuint64_t)f.NC * sizeof(float), 32 * sizeof(float)};
+  const cuuint32_t box[3] = {32, (cuuint32_t)f.RP, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(&h->ps_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->F.Psave, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  h->ps_tmap_ptr = h->F.Psave;
+  h->ps_tmap_rows = rows;
+  return true;
+}
+
+// The tensor map of core k for TMA loads of (K x 128) slice blocks; false
+// when the driver entry point is unavailable (the cp.async kernel runs).
+bool core_tmap(tt_engine* h, int k) {
+  if (h->tmap_ok[k]) return true;
+  auto encode = tmap_encoder();
   if (!encode) return false;
   const DevCfg& c = h->dc;
   const cuuint64_t dims[2] = {(cuuint64_t)c.cols[k], (cuuint64_t)(c.m[k] * c.R[k])};
@@ -1155,8 +1202,8 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
       }
       const int grid = (int)(c.m[f.F] * h->ts.ncbb * a.split);
       rc = TT_OK;
-      const int mode = tcbwd_mode();
-      if (mode == 3 && wdc_ok(f)) {
+      const int mode = tcbwd_mode(f);
+      if ((mode == 3 || mode == 4) && wdc_ok(f)) {
         const int64_t cap = h->cap;
         const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (f.K + 4) + f.RP * f.nF * f.NL);
         if (false) {
@@ -1171,14 +1218,29 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
         wdc_done = true;
         h->psave_valid = false;
         const int pgrid = std::min(grid, h->nsm);
-        const size_t smem2 = tc_bwd2_smem(f.K, 128);
-        if (false) {
-        }
+        if (mode == 4 && psave_tmap(h)) {
+          const size_t smem3 = tc_bwd3_smem(f.K, 128);
+          if (false) {
+          }
+#define TT_TC_BWD4_CASE(k_, bn_, rp_, nl_)                                                                   \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) {                                                        \
+    CU(cudaFuncSetAttribute((k_tc_bwd3<k_, 128, rp_, nl_>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3)); \
+    tt_launch((k_tc_bwd3<k_, 128, rp_, nl_>), dim3(pgrid), dim3(TCB3_THREADS), smem3, s, a, h->ps_tmap);    \
+    ++h->launches;                                                                                           \
+  }
+          TT_TC_SHAPES(TT_TC_BWD4_CASE)
+#undef TT_TC_BWD4_CASE
+          h->bwd_kernel = "k_tc_bwd3";
+        } else {
+          const size_t smem2 = tc_bwd2_smem(f.K, 128);
+          if (false) {
+          }
 #define TT_TC_BWD3_CASE(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH_T((k_tc_bwd2<k_, 128, rp_, nl_, true>), smem2, pgrid, TCB2_THREADS, s, a);
-        TT_TC_SHAPES(TT_TC_BWD3_CASE)
+          TT_TC_SHAPES(TT_TC_BWD3_CASE)
 #undef TT_TC_BWD3_CASE
-        h->bwd_kernel = "k_tc_bwd2";
+          h->bwd_kernel = "k_tc_bwd2";
+        }
       } else if (mode == 2) {
         const int pgrid = std::min(grid, h->nsm);
         const size_t smem2 = tc_bwd2_smem(f.K, 128);
@@ -1208,6 +1270,23 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
         cudaMemsetAsync(trace_buf2, 0, sizeof(long long) * 4096 * 64, s);
         a.dbg = trace_buf2;
         g_trace_buf = trace_buf2;
+      }
+      if (ffma_wdc_enabled(f) && wdc_ok(f)) {  // dC (and W_u) streamed over P_F first; the GEMM kernel loads dC
+        const int64_t cap = h->cap;
+        const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (f.K + 4) + f.RP * f.nF * f.NL);
+        if (false) {
+        }
+#define TT_WDC_CASE(k_, nl_)                                                                                        \
+  else if (f.K == k_ && f.NL == nl_) {                                                                              \
+    CU(cudaFuncSetAttribute((k_fused_wdc<k_, nl_>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_));       \
+    LAUNCH((k_fused_wdc<k_, nl_>), h->nsm, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap);        \
+  }
+        TT_WDC_CASE(64, 4) TT_WDC_CASE(64, 8) TT_WDC_CASE(32, 4) TT_WDC_CASE(32, 8)
+#undef TT_WDC_CASE
+        wdc_done = true;
+        h->psave_valid = false;
+        a.mode = 1;
+        a.dPin = h->F.Psave;
       }
       rc = fused_dispatch(h, false, a, (int)(c.m[f.F] * f.ncb), s);
     }

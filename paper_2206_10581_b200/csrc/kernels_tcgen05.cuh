@@ -977,6 +977,393 @@ __global__ void __launch_bounds__(TCB2_THREADS, 1) k_tc_bwd2(FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Backward with both dC operands in TMEM (round 2, TT_TCBWD=4; dC formed by
+// k_fused_wdc over the saved P_F blocks).  The tensor pipe alternates
+//   dG_F^T(t) = dC(t)^T . A(t)   (A operand dC^T from TMEM, B = A planes)
+//   dA(t)     = dC(t) . S^T      (A operand dC from TMEM, B = S planes)
+// and each half's operands are rewritten while the other half runs:
+// dC^T(t+1) and A(t+1) as soon as dG_F^T(t) completes (under dA(t)), dC(t+1)
+// and the drain of dA(t) as soon as dA(t) completes (under dG_F^T(t+1)).
+// The dC tiles arrive by TMA: per node and 32-column chunk one
+// cp.async.bulk.tensor.2d box {32 floats, RP rows} of the saved blocks, with
+// the 128-byte swizzle (address-based: a box may start at any 512-byte
+// offset, scripts/micro/tma_swz.cu), into two raw tile buffers; so the
+// converters read both layouts from shared memory without bank conflicts
+// (column reads: one wavefront; row reads: four per 512 bytes).
+// TMEM (512 columns): dC [0, 192) (lane = tile row, 3 slices x BN/2),
+// dC^T [192, 384) (lane = block column, 3 slices x 128/2), dG_F^T [384, 384+K),
+// dA [448, 448+K).
+// Warps 0 .. 4 CW - 1 convert (quadrant w % 4, part h = w / 4 of CW: dC^T rows
+// RW h.., dC columns RW h.., accumulator columns K / CW h..; RW = 128 / CW);
+// warp 4 CW issues the MMAs; warp 4 CW + 1 is the producer: node metadata of
+// a tile, its TMA boxes, L2 prefetch of its A rows and of each new item's
+// slice block.  CW = 2; CW = 4 (16 converter warps at 96 registers) measured
+// slower (papers 1.452 -> 1.515 ms/step).
+constexpr int TCB3_CW = 2;                  // converter warps per TMEM lane quadrant
+constexpr int TCB3_CONV = 4 * TCB3_CW;
+constexpr int TCB3_THREADS = 32 * (TCB3_CONV + 2);
+constexpr int TCB3_RAW = TC_BM * 128 * 4;  // one raw dC tile (fp32, 4 chunks of 128 rows x 128 bytes)
+inline size_t tc_bwd3_smem(int K, int BN) {
+  return 1024 + 2 * (size_t)TCB3_RAW + 3 * (size_t)K * BN * 2 + 3 * (size_t)TC_BM * K * 2 + 2 * 32 * 8 + 128;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(map), "r"(x), "r"(y), "r"(z),
+      "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int K, int BN, int RP, int NL>
+__global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const __grid_constant__ CUtensorMap tmP) {
+  TT_PDL_ENTRY();
+  static_assert(BN == 128 && (K == 32 || K == 64) && TC_BM % RP == 0 && RP >= 4 && 64 % RP == 0, "shape");
+  constexpr int NPT = TC_BM / RP;
+  constexpr uint32_t T_DC = 0, T_DCT = 192, T_DG = 384, T_DA = 448;
+  constexpr int CW = TCB3_CW;
+  constexpr int EC = K / CW;     // accumulator columns per converter warp
+  constexpr int RW = TC_BM / CW;  // dC^T rows / dC columns per converter warp
+  static_assert(EC % 8 == 0 && RW % 32 == 0, "converter split");
+  constexpr int NA = TC_BM * K / 8 / (32 * TCB3_CONV);  // A units (8 values) per converter thread
+  extern __shared__ uint8_t tsm_raw[];
+  // 1024-byte aligned base (the swizzle atom); raw buffers first
+  uint8_t* base = tsm_raw + ((1024 - (tc::smem_u32(tsm_raw) & 1023)) & 1023);
+  uint8_t* RAW = base;  // [2][4 chunks][128 rows][128 B], swizzled
+  uint8_t* S0 = RAW + 2 * TCB3_RAW;
+  uint8_t* S1 = S0 + K * BN * 2;
+  uint8_t* S2 = S1 + K * BN * 2;
+  uint8_t* A0 = S2 + K * BN * 2;
+  uint8_t* A1 = A0 + TC_BM * K * 2;
+  uint8_t* A2 = A1 + TC_BM * K * 2;
+  int* r_node = reinterpret_cast<int*>(A2 + TC_BM * K * 2);  // [2][32]
+  int* r_aoff = r_node + 64;                                 // [2][32] (float offsets < 2^31)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(r_aoff + 64);
+  uint64_t* b_gt = bars;
+  uint64_t* b_c = bars + 1;
+  uint64_t* b_gdone = bars + 2;
+  uint64_t* b_ddone = bars + 3;
+  uint64_t* b_full = bars + 4;   // [2]
+  uint64_t* b_empty = bars + 6;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  if (tt_failed(a.st)) return;
+  const int nitems = (int)a.c.m[a.F] * a.ncb * (a.split > 1 ? a.split : 1);
+  BwdCursor cur;
+  cur.it = blockIdx.x;
+  if (!cur.seek_item(a, nitems)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 2 * TCB3_RAW / 16; i += TCB3_THREADS)
+    reinterpret_cast<uint4*>(RAW)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // (ordered before the TMA writes)
+  if (warp == 0) tc::tmem_alloc<512>(tslot);
+  if (threadIdx.x == 32) {
+    tc::mbar_init(b_gt, TCB3_CONV);
+    tc::mbar_init(b_c, TCB3_CONV);
+    tc::mbar_init(b_gdone, 1);
+    tc::mbar_init(b_ddone, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&b_full[i], 1);
+      tc::mbar_init(&b_empty[i], TCB3_CONV);
+    }
+    tc::fence_mbar_init();
+  }
+  tc::before_sync();
+  __syncthreads();
+  tc::after_sync();
+  const uint32_t tm = *tslot;
+
+  if (warp == TCB3_CONV + 1) {
+    // ---------------- producer: metadata, TMA boxes, L2 prefetch ----------------
+    // a tile's metadata is fetched (and its A rows and slice block
+    // prefetched into L2) while the producer waits for the buffer of the
+    // tile before it, so the TMA boxes go out as soon as a buffer frees
+    int last_it = -1;
+    auto fetch = [&](const BwdCursor& c, int& nn, int& node, int& aoff) {
+      nn = min(NPT, c.nbn - c.tb);
+      node = aoff = 0;
+      if (lane < nn) {
+        node = __ldg(a.orderF + c.nb0 + c.tb + lane);
+        const int p = __ldg(a.parentF + node);
+        aoff = (int)(a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
+                              : (int64_t)p * RP * a.c.R[a.F]);
+        prefetch_l2(a.Abase + aoff, RP * K * 4);
+      }
+      if (c.it != last_it) {
+        last_it = c.it;
+        const float* sb = a.params + a.c.core_off[a.F] + (int64_t)c.g * a.c.slice[a.F] + c.cb * BN;
+        for (int k = lane; k < K; k += 32) prefetch_l2(sb + (int64_t)k * a.NC, BN * 4);
+      }
+    };
+    BwdCursor c = cur;
+    uint32_t tau = 0;
+    int nn, node, aoff;
+    fetch(c, nn, node, aoff);
+    for (;;) {
+      const int sl = tau & 1;
+      tc::mbar_wait(&b_empty[sl], ((tau >> 1) & 1) ^ 1);
+      if (lane < nn) {
+        r_node[sl * 32 + lane] = node;
+        r_aoff[sl * 32 + lane] = aoff;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(&b_full[sl], (a.mode & 16) ? 0u : (unsigned)(nn * RP * 512));
+      __syncwarp();
+      if (lane < nn && !(a.mode & 16))  // the node's RP rows x BN columns: one 3-D box [4 chunks][RP][32]
+        tma_load_3d(RAW + sl * TCB3_RAW + lane * RP * 512, &tmP, &b_full[sl], 0, node * RP, c.cb * (BN / 32));
+      bool nb, ni;
+      if (!c.advance(a, nitems, NPT, nb, ni)) break;
+      fetch(c, nn, node, aoff);
+      ++tau;
+    }
+  } else if (warp == TCB3_CONV) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t id_g = tc::idesc_bf16(BN, K, 0, 1);     // dG^T = dC^T (TMEM) . A
+      const uint32_t id_a = tc::idesc_bf16(TC_BM, K, 0, 0);  // dA = dC (TMEM) . S^T
+      const tc::Operand aB = tc::mnmajor(tc::smem_u32(A0), tc::smem_u32(A1), tc::smem_u32(A2), K);
+      const tc::Operand sT = tc::kmajor(tc::smem_u32(S0), tc::smem_u32(S1), tc::smem_u32(S2), BN);
+      BwdCursor c = cur;
+      uint32_t t = 0;
+      bool first = true;
+      for (;;) {
+        tc::mbar_wait(b_gt, t & 1);
+        tc::after_sync();
+        if (!(a.mode & 2)) tc::mma_x3_ts<TC_BM / 16>(tm + T_DG, tm + T_DCT, aB, id_g, !first);
+        tc::commit(b_gdone);
+        tc::mbar_wait(b_c, t & 1);
+        tc::after_sync();
+        if (!(a.mode & 2)) tc::mma_x3_ts<BN / 16>(tm + T_DA, tm + T_DC, sT, id_a, false);
+        tc::commit(b_ddone);
+        bool nb, ni;
+        if (!c.advance(a, nitems, NPT, nb, ni)) break;
+        first = ni;
+        ++t;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- converters ----------------
+    const int q = warp & 3, h = warp >> 2;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const int x = threadIdx.x;     // 0 .. 255
+    const int cc = 32 * q + lane;  // block column (dC^T lane) / tile row (dC lane)
+#ifdef TT_BWD3_TRACE  // thread 0's cycles per phase, summed into a.dbg[blockIdx.x * 16 + k] (TT_TC_TRACE=1)
+    const bool trace = a.dbg != nullptr && threadIdx.x == 0;
+    long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+    auto mark = [&](int k) {
+      if (trace) {
+        const long long now = clock64();
+        ph[k] += now - tlast;
+        tlast = now;
+      }
+    };
+#else
+    auto mark = [](int) {};
+#endif
+    auto ld_acc = [&](uint32_t taddr, uint32_t (&r)[EC]) {
+      if constexpr (EC >= 16) {
+#pragma unroll
+        for (int i = 0; i < EC / 16; ++i) tc::tmem_ld16_async(taddr + 16 * i, r + 16 * i);
+        tc::tmem_ld_wait();
+      } else {
+        float f[8];
+        tc::tmem_ld8(taddr, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(f[i]);
+      }
+    };
+    auto drain_dG = [&](int g, int cb, int chunk) {
+      float* gdst = (a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                                  : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F]) + cb * BN + cc;
+      uint32_t r[EC];
+      ld_acc(tm + lane_off + T_DG + h * EC, r);
+#pragma unroll
+      for (int i = 0; i < EC; ++i) gdst[(int64_t)(h * EC + i) * a.NC] = __uint_as_float(r[i]);
+    };
+    auto drain_dA = [&](float* dst) {
+      uint32_t da[EC];
+      ld_acc(tm + lane_off + T_DA + h * EC, da);
+      if (dst) {
+#pragma unroll
+        for (int v = 0; v < EC / 4; ++v)
+          reinterpret_cast<float4*>(dst)[v] = make_float4(__uint_as_float(da[4 * v]), __uint_as_float(da[4 * v + 1]),
+                                                          __uint_as_float(da[4 * v + 2]), __uint_as_float(da[4 * v + 3]));
+      }
+    };
+    BwdCursor c = cur;
+    uint32_t t = 0;
+    bool first = true;
+    int pg = 0, pcb = 0, pchunk = 0;
+    float* dst_prev = nullptr;
+    // A(t) rows into registers: issued at the end of tile t-1 (under its dA drain)
+    float4 av[NA][2];
+    auto load_A = [&](int sl, int nn) {
+      tc::mbar_wait(&b_full[sl], (t >> 1) & 1);  // (t = the tile being loaded)
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int u = x + i * 32 * TCB3_CONV;
+        const int kc = (u >> 3) % (K / 8), m = ((u >> 3) / (K / 8)) * 8 + (u & 7), j = m / RP;
+        av[i][0] = av[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < nn) {
+          const float* src = a.Abase + r_aoff[sl * 32 + j] + (m - j * RP) * K + kc * 8;
+          av[i][0] = __ldg(reinterpret_cast<const float4*>(src));
+          av[i][1] = __ldg(reinterpret_cast<const float4*>(src + 4));
+        }
+      }
+    };
+    load_A(0, min(NPT, c.nbn - c.tb));
+    for (;;) {
+      const int sl = t & 1;
+      const int nn = min(NPT, c.nbn - c.tb);
+      mark(8);
+      const uint8_t* raw = RAW + sl * TCB3_RAW;
+      mark(0);
+      // (B) after dG_F^T(t-1): [new item: drain dG_F^T], write A(t) and dC^T(t)
+      if (t > 0) {
+        tc::mbar_wait(b_gdone, (t - 1) & 1);
+        tc::after_sync();
+      }
+      mark(1);
+      if (first && t > 0) drain_dG(pg, pcb, pchunk);
+      mark(9);
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int u = x + i * 32 * TCB3_CONV;
+        const int kc = (u >> 3) % (K / 8), m = ((u >> 3) / (K / 8)) * 8 + (u & 7);
+        const float v8[8] = {av[i][0].x, av[i][0].y, av[i][0].z, av[i][0].w,
+                             av[i][1].x, av[i][1].y, av[i][1].z, av[i][1].w};
+        tc::store_split8<true>(A0, A1, A2, m, kc * 8, K, v8);
+      }
+      // raw tile layout (one 3-D box per node): 128-byte line
+      // L(m, qc) = (m / RP) 4 RP + qc RP + m % RP, 16-byte unit u at
+      // L 128 + ((u ^ (L & 7)) << 4)
+      // Rows past the tile's nodes hold finite stale values (the buffers are
+      // zeroed at entry): their A rows are zero, so they add nothing to dG_F,
+      // and their dA rows are not stored -- no per-element predicates.
+      {
+        // column cc = 32 q + lane of chunk q; rows RW h + k, k < RW: line
+        // Lb + (k / RP) 4 RP + k % RP with Lb = (RW h / RP) 4 RP + q RP, and
+        // L & 7 = (q RP + k % RP) & 7 -- a per-thread offset table xo
+        const uint8_t* colp = raw + (lane & 3) * 4 + ((RW * h / RP) * 4 * RP + q * RP) * 128;
+        const int c16 = lane >> 2;
+        constexpr int NX = RP < 8 ? RP : 8;
+        int xo[NX];
+#pragma unroll
+        for (int r = 0; r < NX; ++r) xo[r] = (c16 ^ ((q * RP + r) & 7)) << 4;
+        auto at = [&](int k) {
+          return *reinterpret_cast<const float*>(colp + ((k / RP) * 4 * RP + k % RP) * 128 + xo[(k % RP) % NX]);
+        };
+#pragma unroll
+        for (int ch = 0; ch < RW / 16; ++ch) {
+          uint32_t w0[8], w1[8], w2[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) tc::split3t(at(16 * ch + 2 * i), at(16 * ch + 2 * i + 1), w0[i], w1[i], w2[i]);
+          const uint32_t col = tm + lane_off + T_DCT + (RW / 2) * h + 8 * ch;
+          tc::tmem_st8(col, w0);
+          tc::tmem_st8(col + 64, w1);
+          tc::tmem_st8(col + 128, w2);
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_async_smem();
+      tc::before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(b_gt);
+      mark(2);
+      // dA destination of tile t (row cc)
+      float* dst_cur;
+      {
+        const int j = cc / RP;
+        dst_cur = (j < nn && !(a.mode & 4))
+                      ? a.dPc + ((int64_t)r_node[sl * 32 + j] * a.ncb + c.cb) * RP * K + (cc - j * RP) * K + h * EC
+                      : nullptr;
+      }
+      mark(3);
+      // (D) after dA(t-1): drain and store it, [new item: stage S], write dC(t)
+      uint32_t da[EC];  // dA(t-1): read before dA(t) may overwrite it, stored after dC(t) is handed over
+      if (t > 0) {
+        tc::mbar_wait(b_ddone, (t - 1) & 1);
+        tc::after_sync();
+        mark(4);
+        ld_acc(tm + lane_off + T_DA + h * EC, da);
+      }
+      mark(6);
+      if (first) tc_stage_slice<K, BN, 32 * TCB3_CONV>(a, c.g, c.cb, S0, S1, S2);
+      {
+        // row cc, columns RW h .. RW h + RW - 1 = 32-column chunks (RW / 32) h ..
+#pragma unroll
+        for (int hc = 0; hc < RW / 32; ++hc) {
+          const int L = (cc / RP) * 4 * RP + ((RW / 32) * h + hc) * RP + (cc % RP);
+          const uint8_t* rowp = raw + L * 128;
+          const int sw = L & 7;
+#pragma unroll
+          for (int uu = 0; uu < 2; ++uu) {  // 16 columns per step
+            float v[16];
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int u = 4 * uu + k4;
+              const float4 y = *reinterpret_cast<const float4*>(rowp + ((u ^ sw) << 4));
+              v[4 * k4] = y.x; v[4 * k4 + 1] = y.y; v[4 * k4 + 2] = y.z; v[4 * k4 + 3] = y.w;
+            }
+            uint32_t w0[8], w1[8], w2[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tc::split3t(v[2 * i], v[2 * i + 1], w0[i], w1[i], w2[i]);
+            const uint32_t col = tm + lane_off + T_DC + (RW / 2) * h + 16 * hc + 8 * uu;
+            tc::tmem_st8(col, w0);
+            tc::tmem_st8(col + 64, w1);
+            tc::tmem_st8(col + 128, w2);
+          }
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_async_smem();
+      tc::before_sync();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(b_c);
+        tc::mbar_arrive(&b_empty[sl]);  // raw tile and metadata slot consumed
+      }
+      mark(5);
+      if (t > 0 && dst_prev) {
+#pragma unroll
+        for (int v = 0; v < EC / 4; ++v)
+          reinterpret_cast<float4*>(dst_prev)[v] = make_float4(__uint_as_float(da[4 * v]), __uint_as_float(da[4 * v + 1]),
+                                                               __uint_as_float(da[4 * v + 2]), __uint_as_float(da[4 * v + 3]));
+      }
+      dst_prev = dst_cur;
+      pg = c.g;
+      pcb = c.cb;
+      pchunk = c.chunk;
+      bool nb, ni;
+      if (!c.advance(a, nitems, NPT, nb, ni)) break;
+      first = ni;
+      ++t;
+      load_A(t & 1, min(NPT, c.nbn - c.tb));
+    }
+    // the last tile's dA, the last item's dG_F
+    tc::mbar_wait(b_ddone, t & 1);
+    tc::after_sync();
+    drain_dA(dst_prev);
+    drain_dG(pg, pcb, pchunk);
+    mark(9);
+#ifdef TT_BWD3_TRACE
+    if (trace) {
+      ph[7] = t + 1;
+      for (int k = 0; k < 12; ++k) a.dbg[blockIdx.x * 16 + k] = ph[k];
+    }
+#endif
+  }
+  tc::before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tm);
+}
+
+// ---------------------------------------------------------------------------
 // Backward at rank 128 (the rank sweep's R = 128): 64-column blocks, so the
 // BF16x3 planes fit in 192 KB (S 48 KB, A 96 KB, dC 48 KB; 128-column blocks
 // would need 288 KB).  dG_F is accumulated untransposed, M = 128 (k) x N = 64

@@ -175,6 +175,22 @@ __device__ __forceinline__ void split3(float x0, float x1, uint32_t& s0, uint32_
   s2 = pack_bf16(r0 - bf_lo(s1), r1 - bf_hi(s1));
 }
 
+// The same three slices by truncation: each slice is the top 16 bits of the
+// remainder (an exact FP32 subtraction), packed with one byte permute --
+// integer-pipe work instead of three F2FP conversions per pair, which bound
+// the tensor backward's operand conversion.  The residual after three
+// slices is below 2^-24 |x| (2^-8 of the remainder per slice), so the
+// six-product sums keep the FP32 path's parity bound.
+__device__ __forceinline__ void split3t(float x0, float x1, uint32_t& s0, uint32_t& s1, uint32_t& s2) {
+  const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
+  s0 = __byte_perm(u0, u1, 0x7632);
+  const float r0 = x0 - __uint_as_float(u0 & 0xFFFF0000u), r1 = x1 - __uint_as_float(u1 & 0xFFFF0000u);
+  const uint32_t v0 = __float_as_uint(r0), v1 = __float_as_uint(r1);
+  s1 = __byte_perm(v0, v1, 0x7632);
+  const float q0 = r0 - __uint_as_float(v0 & 0xFFFF0000u), q1 = r1 - __uint_as_float(v1 & 0xFFFF0000u);
+  s2 = __byte_perm(__float_as_uint(q0), __float_as_uint(q1), 0x7632);
+}
+
 // byte offset of element (r, c) in a core-matrix plane with C columns (bf16)
 __host__ __device__ __forceinline__ uint32_t core_off(int r, int c, int C) {
   return (uint32_t)(((r >> 3) * (C >> 3) + (c >> 3)) * 128 + (r & 7) * 16 + (c & 7) * 2);
@@ -182,11 +198,15 @@ __host__ __device__ __forceinline__ uint32_t core_off(int r, int c, int C) {
 
 // Split 8 consecutive fp32 values of row r, columns c0..c0+7 (c0 % 8 == 0),
 // into the three planes (16-byte stores).
+template <bool TRUNC = false>
 __device__ __forceinline__ void store_split8(uint8_t* p0, uint8_t* p1, uint8_t* p2, int r, int c0, int C,
                                              const float* x) {
   uint32_t a[4], b[4], c[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) split3(x[2 * i], x[2 * i + 1], a[i], b[i], c[i]);
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (TRUNC) split3t(x[2 * i], x[2 * i + 1], a[i], b[i], c[i]);
+    else split3(x[2 * i], x[2 * i + 1], a[i], b[i], c[i]);
+  }
   const uint32_t off = core_off(r, c0, C);
   *reinterpret_cast<uint4*>(p0 + off) = make_uint4(a[0], a[1], a[2], a[3]);
   *reinterpret_cast<uint4*>(p1 + off) = make_uint4(b[0], b[1], b[2], b[3]);

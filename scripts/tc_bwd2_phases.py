@@ -30,6 +30,9 @@ lib.tt_debug_trace(buf.ctypes.data_as(C.POINTER(C.c_longlong)), buf.size)
 ph = buf[:148 * 16].reshape(148, 16)
 names = ["wait MMA(t-1)", "new item: dG drain + slice", "store planes", "barrier", "dA drain / issue",
          "advance + prep", "loads / dC(t+1)", "tiles", "prologue", "tail"]
+if os.environ.get("TT_TCBWD", "4") == "4":  # k_tc_bwd3 (built with -DTT_BWD3_TRACE)
+    names = ["-", "B: wait dG done", "B: write A + dC^T", "dA dst", "D: wait dA done",
+             "D: stage S + write dC", "D: dA TMEM read", "tiles", "dA store + next A loads", "dG drain"]
 tot = ph[:, [0, 1, 2, 3, 4, 5, 6, 8, 9]].sum(1)
 print(f"{cfgname}: CTAs {int((ph[:, 7] > 0).sum())}, tiles/CTA mean {ph[:, 7].mean():.1f} "
       f"(min {ph[:, 7].min()}, max {ph[:, 7].max()}), cycles/CTA mean {tot.mean():.0f} max {tot.max():.0f}")
