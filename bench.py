@@ -454,9 +454,13 @@ def main():
                           "ms_per_launch": bwd_ms,
                           "note": "frac = algorithmic FLOPs (4 U_F c_F + 2 U_d c_d) over the dense BF16 peak; "
                                   "issued_mma_frac = the BF16 MMA FLOPs actually issued (6 per algorithmic MAC of "
-                                  "dG_F and dA, the BF16x3 split) over the same peak; the kernel is bound by forming "
-                                  "dC on the CUDA cores (latency of the per-ID loads), not by the tensor pipe "
-                                  "(DESIGN.md c2)"},
+                                  "dG_F and dA, the BF16x3 split) over the same peak; "
+                                  + ("the phase is k_fused_wdc (dC and the last core's W_u over the saved P_F, "
+                                     "HBM-bound) + k_tc_bwd3 (dC staged by TMA, both dC operands in TMEM, bound by "
+                                     "the CUDA cores' BF16x3 conversion), not by the tensor pipe (DESIGN.md c2)"
+                                     if (tc_run["kernels"]["bwd"] or "") == "k_tc_bwd3" else
+                                     "the kernel is bound by forming dC on the CUDA cores (latency of the per-ID "
+                                     "loads), not by the tensor pipe (DESIGN.md c2)")},
                       "gpu_launches": tc_run["launches"]}
         emb.set_path(a.path)
 

@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const 
     fetch(c, nn, node, aoff);
     for (;;) {
       const int sl = tau & 1;
-      tc::mbar_wait(&b_empty[sl], ((tau >> 1) & 1) ^ 1);
+      tc::mbar_wait_sleep(&b_empty[sl], ((tau >> 1) & 1) ^ 1);  // (parked: not latency-critical)
       if (lane < nn) {
         r_node[sl * 32 + lane] = node;
         r_aoff[sl * 32 + lane] = aoff;
