@@ -148,7 +148,8 @@ struct tt_engine {
 
   // bookkeeping
   bool plan_valid = false;
-  bool psave_valid = false;  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
+  bool psave_valid = false;
+  bool ll_fused = false;  // the last forward's GEMM also wrote the output rows (k_fused_fwd8<..., LL>)  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
   int64_t cores_version = 0, plan_version = -1;
   int64_t batch_count = 0;
   int64_t launches = 0;
@@ -772,6 +773,19 @@ int tcbwd_mode(const FusedShape& f) {
   }();
   return m ? m : (f.K == 64 ? 4 : 1);
 }
+// TT_FWD_LL=1: the FFMA forward writes the output rows itself
+// (k_fused_fwd8<..., LL>) instead of k_last_level re-reading P_F.  Off: at
+// papers the forward went 0.534 -> 0.915 ms for the 0.147 ms it saves (the
+// per-ID epilogue -- slice loads, a 16-lane reduce-scatter, position writes --
+// runs serially after every tile and stalls the GEMM), step 2.355 -> 2.600.
+bool fwd_ll_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_FWD_LL");
+    return e && *e == '1';
+  }();
+  return on;
+}
+
 // The FFMA backward loads dC formed by k_fused_wdc (mode 1) instead of
 // forming it per tile: TT_FFMA_WDC=1 always, 0 never; default at K = 64 with
 // NL = 8 (the rank sweep's R = 64: 8 IDs per level-F node, 8-wide last-core
@@ -920,7 +934,12 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
   if (fwd && f.BNf == 128 && fwd8_enabled()) {
 #define FWD8_CASE(k_, rp_)                                                                       \
   if (f.K == k_ && f.RP == rp_) {                                                                \
-    if (tma_enabled() && core_tmap(h, a.F)) {                                                    \
+    if (a.out && tma_enabled() && core_tmap(h, a.F)) { /* last level fused (fused_forward decided) */ \
+      CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)fwd8_smem(k_)));                                               \
+      tt_launch((k_fused_fwd8<k_, rp_, true, true>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
+      h->ll_fused = true;                                                                        \
+    } else if (tma_enabled() && core_tmap(h, a.F)) {                                             \
       CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
                               (int)fwd8_smem(k_)));                                               \
       tt_launch((k_fused_fwd8<k_, rp_, true>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
@@ -1053,6 +1072,12 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
   a.CH = 0;
   a.ncb = f.ncbf;
   a.BNj = f.BNjf;
+  h->ll_fused = false;
+  // TT_FWD_LL=1: the FFMA forward at K = 64, RP = 4, NL = 4 (papers) writes the
+  // output rows itself (k_fused_fwd8<..., LL>; measured slower, off by default)
+  if (d_out && !use_tc(h) && fwd_ll_enabled() && f.K == 64 && f.RP == 4 && f.NL == 4 && f.BNf == 128 &&
+      c.emb_dim % 2 == 0)
+    a.out = d_out;
   {
     Phase ph(h, 1, s);
     if (use_tc(h) && f.K == 128) {  // rank 128: the FFMA forward, the tcgen05 backward
@@ -1093,7 +1118,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
     }
   }
   if (rc) return rc;
-  if (d_out) {
+  if (d_out && !h->ll_fused) {
     FusedArgs o = fused_args(h, d_out);
     const int d = c.d;
     const int64_t cap = h->cap;

@@ -467,7 +467,15 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned phase) 
       : "memory");
 }
 
-template <int K, int RP, bool TMA>
+// LL (round 2; NL = 4, RP = 4): the last level is fused into the tile
+// epilogue -- for each distinct ID u of the thread's two nodes, the 16 lanes
+// of a row group each hold 4 of the tile's 64 rank columns per core-F column,
+// form the 32 partial outputs (4 rows x 2 column blocks x NL) over those 4
+// ranks, reduce-scatter them over the 16 lanes (shuffles xor 8, 4, 2, 1), and
+// write 2 contiguous floats of the output row to every batch position of u
+// (heavy IDs: their Yu row, scattered by k_scatter_heavy).  k_last_level then
+// does not run (it re-read all of P_F).
+template <int K, int RP, bool TMA, bool LL = false>
 __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
     k_fused_fwd8(FusedArgs a, const __grid_constant__ CUtensorMap tmS) {
   TT_PDL_ENTRY();
@@ -551,6 +559,68 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
           float* dst = a.Psave + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN;
           *reinterpret_cast<float4*>(dst + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
           *reinterpret_cast<float4*>(dst + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        }
+      }
+      if constexpr (LL) {
+        static_assert(K == 64 && RP == 4, "fused last level: 8 rows = 2 nodes per thread, 2 column blocks per tile");
+        constexpr int NLL = 4;
+        const unsigned gmask = 0xFFFFu << (lane & 16);
+        const int li = lane & 15;
+        const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+        const int64_t sliceL = a.c.slice[a.c.d - 1];
+        const int64_t emb = a.c.emb_dim, npad = a.c.npad;
+        // this lane's 2 outputs after the reduce-scatter: row a = li / 4, column
+        // block h = (li / 2) & 1, NL entries 2 (li & 1) .. + 1
+        const int oa = li >> 2, oh = (li >> 1) & 1;
+        const int64_t col = ((int64_t)oa * a.nF + 2 * cb + oh) * NLL + 2 * (li & 1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int j = r0 / RP + k;
+          if (j >= nn) break;
+          const int node = s_node[tb + j];
+          const int u0 = __ldg(a.cstartF + node), u1 = __ldg(a.cstartF + node + 1);
+          for (int u = u0; u < u1; ++u) {
+            const float4* gp = reinterpret_cast<const float4*>(Gl + (int64_t)__ldg(a.digitL + u) * sliceL + c0 * NLL);
+            float4 g[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) g[t] = __ldg(gp + t);
+            float v[32];  // v[ar * 8 + h * 4 + jl]
+#pragma unroll
+            for (int ar = 0; ar < 4; ++ar)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const float x = acc[4 * k + ar][4 * h + t];
+                  o0 = fmaf(x, g[t].x, o0); o1 = fmaf(x, g[t].y, o1); o2 = fmaf(x, g[t].z, o2); o3 = fmaf(x, g[t].w, o3);
+                }
+                v[ar * 8 + h * 4] = o0; v[ar * 8 + h * 4 + 1] = o1; v[ar * 8 + h * 4 + 2] = o2; v[ar * 8 + h * 4 + 3] = o3;
+              }
+            // reduce-scatter over the 16 lanes: after the xor-8 step a lane keeps
+            // the half of v its bit 3 selects, and so on down to 2 values
+#pragma unroll
+            for (int step = 0; step < 4; ++step) {
+              const int half = 16 >> step;
+              const bool hi = (li >> (3 - step)) & 1;
+#pragma unroll
+              for (int i = 0; i < half; ++i) {
+                const float give = hi ? v[i] : v[half + i];
+                const float keep = hi ? v[half + i] : v[i];
+                v[i] = keep + __shfl_xor_sync(gmask, give, 8 >> step);
+              }
+            }
+            const int s0 = __ldg(a.seg + u), s1 = __ldg(a.seg + u + 1);
+            if (s1 - s0 > HEAVY_POS) {
+              *reinterpret_cast<float2*>(a.Yu + (int64_t)u * npad + col) = make_float2(v[0], v[1]);
+            } else if (col < emb) {
+              for (int sl = s0; sl < s1; ++sl) {
+                float* orow = a.out + (int64_t)__ldg(a.spos + sl) * emb + col;
+                if (col + 1 < emb) *reinterpret_cast<float2*>(orow) = make_float2(v[0], v[1]);
+                else orow[0] = v[0];
+              }
+            }
+          }
         }
       }
     }

@@ -404,3 +404,16 @@ def test_second_backward_of_one_forward(path):
     g2 = emb._fetch_grads()
     for k in range(cfg.d):
         np.testing.assert_array_equal(g1[k], g2[k])
+
+
+def test_forward_parity_with_fused_last_level():
+    # k_fused_fwd8<..., LL> (TT_FWD_LL=1, off by default: measured slower) writes
+    # the output rows from the forward's tile epilogue; same parity bound
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TT_FWD_LL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "test_forward_parity and papers and auto"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
