@@ -552,6 +552,12 @@ int build_plan(tt_engine* h, const int64_t* d_idx, int64_t B, cudaStream_t s) {
       h->order[k] = ps.order[k];
     }
     ps.st = h->st;
+    if (getenv("TT_PS_TRACE")) {  // diagnostics: phase clocks of k_plan_small (tt_debug_trace)
+      static long long* ps_trace = nullptr;
+      if (!ps_trace) cudaMalloc(&ps_trace, sizeof(long long) * 4096 * 64);
+      ps.dbg = ps_trace;
+      g_trace_buf = ps_trace;
+    }
     CU(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PS_SMEM));
     LAUNCH(k_plan_small, 1, PS_THREADS, PS_SMEM, s, ps);
     h->skeys = h->keys_b;

@@ -19,9 +19,11 @@
 namespace tt {
 
 constexpr int PS_THREADS = 1024, PS_WARPS = PS_THREADS / 32, PS_MAXB = 8192, PS_IBITS = 13;
+constexpr int PS_DBITS = 9, PS_NB = 1 << PS_DBITS;  // radix digits of up to 9 bits (18-bit IDs: 2 passes)
 constexpr unsigned long long PS_IMASK = (1ull << PS_IBITS) - 1;
-// dynamic shared memory: two value buffers + the (digit, warp) offset table + scan scratch
-constexpr size_t PS_SMEM = sizeof(unsigned long long) * 2 * PS_MAXB + sizeof(int) * (PS_WARPS * 256 + 64);
+// dynamic shared memory: two value buffers + the (digit, warp) offset table
+// (reused as the levels' first-ID tables) + bucket starts + scan scratch
+constexpr size_t PS_SMEM = sizeof(unsigned long long) * 2 * PS_MAXB + sizeof(int) * (PS_WARPS * PS_NB + PS_NB + 64);
 
 struct PlanSmallArgs {
   DevCfg c;
@@ -44,6 +46,7 @@ struct PlanSmallArgs {
   int* order[TT_MAXD];
   int* goff[TT_MAXD];
   DevStatus* st;
+  long long* dbg;  // TT_PS_TRACE=1: clock64 at the end of each phase (thread 0), else nullptr
 };
 
 // exclusive block scan of one int per thread (1024 threads); total in *tot
@@ -75,31 +78,35 @@ __device__ __forceinline__ int ps_block_excl(int v, int* wsum, int* tot) {
 
 // stable LSD sort of a[0, n) on bits [lo, hi) of the values; returns the buffer
 // holding the result (a or b)
+// (bits per pass: PS_DBITS; a sort of at most PS_DBITS bits is one pass, and
+// then bstart[d] = the first output slot of digit d, if bstart is given)
 __device__ unsigned long long* ps_sort(unsigned long long* a, unsigned long long* b, int n, int lo, int hi, int* H,
-                                       int* wsum, int* tot) {
+                                       int* wsum, int* tot, int* bstart = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int segn = (n + PS_WARPS - 1) / PS_WARPS;
   const int s0 = min(n, warp * segn), s1 = min(n, s0 + segn);
-  for (int shift = lo; shift < hi; shift += 8) {
-    const int bits = min(8, hi - shift);
+  constexpr int EPT = PS_WARPS * PS_NB / PS_THREADS;  // offset-table entries per thread
+  for (int shift = lo; shift < hi; shift += PS_DBITS) {
+    const int bits = min(PS_DBITS, hi - shift);
     const unsigned long long dm = (1ull << bits) - 1;
-    for (int i = threadIdx.x; i < PS_WARPS * 256; i += PS_THREADS) H[i] = 0;
+    for (int i = threadIdx.x; i < PS_WARPS * PS_NB; i += PS_THREADS) H[i] = 0;
     __syncthreads();
-    for (int i = s0 + lane; i < s1; i += 32) atomicAdd(&H[warp * 256 + (int)((a[i] >> shift) & dm)], 1);
+    for (int i = s0 + lane; i < s1; i += 32) atomicAdd(&H[warp * PS_NB + (int)((a[i] >> shift) & dm)], 1);
     __syncthreads();
-    // offsets in (digit, warp) order: entry e = d * 32 + w, 8 entries per thread
-    int v[8], t = 0;
+    // offsets in (digit, warp) order: entry e = d * 32 + w, EPT entries per thread
+    int v[EPT], t = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int e = threadIdx.x * 8 + j, d = e >> 5, w = e & 31;
-      v[j] = H[w * 256 + d];
+    for (int j = 0; j < EPT; ++j) {
+      const int e = threadIdx.x * EPT + j, d = e >> 5, w = e & 31;
+      v[j] = H[w * PS_NB + d];
       t += v[j];
     }
     int run = ps_block_excl(t, wsum, tot);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int e = threadIdx.x * 8 + j, d = e >> 5, w = e & 31;
-      H[w * 256 + d] = run;
+    for (int j = 0; j < EPT; ++j) {
+      const int e = threadIdx.x * EPT + j, d = e >> 5, w = e & 31;
+      H[w * PS_NB + d] = run;
+      if (bstart && w == 0) bstart[d] = run;
       run += v[j];
     }
     __syncthreads();
@@ -107,14 +114,14 @@ __device__ unsigned long long* ps_sort(unsigned long long* a, unsigned long long
       const int i = c0 + lane;
       const bool ok = i < s1;
       const unsigned long long x = ok ? a[i] : 0ull;
-      const int d = ok ? (int)((x >> shift) & dm) : 256 + lane;  // invalid lanes match nobody
+      const int d = ok ? (int)((x >> shift) & dm) : PS_NB + lane;  // invalid lanes match nobody
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int rank = __popc(peers & lanemask_lt());
-      const int off = ok ? H[warp * 256 + d] : 0;
+      const int off = ok ? H[warp * PS_NB + d] : 0;
       __syncwarp();
       if (ok) {
         b[off + rank] = x;
-        if (rank == 0) H[warp * 256 + d] = off + __popc(peers);
+        if (rank == 0) H[warp * PS_NB + d] = off + __popc(peers);
       }
       __syncwarp();
     }
@@ -153,11 +160,18 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
   unsigned long long* A = ps_smem;
   unsigned long long* Bf = A + PS_MAXB;
   int* H = reinterpret_cast<int*>(Bf + PS_MAXB);
-  int* wsum = H + PS_WARPS * 256;
+  int* bst = H + PS_WARPS * PS_NB;  // [PS_NB] bucket starts of a one-pass sort
+  int* wsum = bst + PS_NB;
   int* tot = wsum + 40;
   const DevCfg& c = p.c;
   const int d = c.d, B = p.B;
   const int64_t cap = p.cap;
+  int nmark = 0;
+  auto mark = [&]() {
+    if (p.dbg && threadIdx.x == 0) p.dbg[nmark] = clock64();
+    ++nmark;
+  };
+  mark();
 
   // K1: validate, key = (relabelled) id, packed with the position
   for (int b = threadIdx.x; b < B; b += PS_THREADS) {
@@ -173,8 +187,10 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
     if (threadIdx.x < d) p.counts[threadIdx.x] = 0;
     return;
   }
+  mark();  // 1: validate
   // K2: stable sort by id, ties by position
   unsigned long long* S = ps_sort(A, Bf, B, PS_IBITS, PS_IBITS + p.idbits, H, wsum, tot);
+  mark();  // 2: sort
   for (int s = threadIdx.x; s < B; s += PS_THREADS) {
     p.skeys[s] = S[s] >> PS_IBITS;
     p.spos[s] = (int)(S[s] & PS_IMASK);
@@ -195,12 +211,17 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
     p.seg[U] = B;
   }
   __syncthreads();
+  mark();  // 3: sorted keys out, unique
   // levels 0..d-2: prefix flags over the distinct IDs (scans in the sort
   // buffers, which are free now: level k in Lc, level k-1 in Lp; the IDs'
   // level-k prefixes in Q, 32-bit when the IDs fit)
   int* Lp = reinterpret_cast<int*>(A);
   int* Lc = Lp + PS_MAXB;
   unsigned long long* Q = Bf;  // [U] level-k prefix of every distinct ID
+  // first distinct ID of every node of levels k - 1 and k (the sort table is
+  // free here): cstart without a round trip through p.first
+  int* Fp = H;
+  int* Fc = H + PS_MAXB;
   const bool id32 = c.num_nodes <= 0xFFFFFFFFll;
   for (int k = 0; k + 1 < d; ++k) {
     const unsigned long long Sk = (unsigned long long)c.S[k];
@@ -216,25 +237,37 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
         const int dg = id32 ? (int)((unsigned)q % (unsigned)c.m[k]) : (int)(q % (unsigned long long)c.m[k]);
         p.digit[k * cap + node] = dg;
         p.first[k * cap + node] = u;
+        Fc[node] = u;
         p.parent[k * cap + node] = k ? Lp[u] - 1 : -1;
         if (k == 0) {
           p.order[0][node] = node;
           p.sdig[0][node] = (unsigned)dg;
+          // level 0 is in digit order: goff[0][v] = first node with digit >= v
+          const int prev = u == 0 ? -1 : (int)(id32 ? (unsigned)Q[u - 1] % (unsigned)c.m[0] : Q[u - 1] % (unsigned long long)c.m[0]);
+          for (int v = prev + 1; v <= dg; ++v) p.goff[0][v] = node;
         }
       }
     }
     if (threadIdx.x == 0) p.counts[k] = nk;
+    if (k == 0 && threadIdx.x < 32) {  // digits past the last node's: goff = n_0
+      const int last = id32 ? (int)((unsigned)Q[U - 1] % (unsigned)c.m[0]) : (int)(Q[U - 1] % (unsigned long long)c.m[0]);
+      for (int v = last + 1 + threadIdx.x; v <= c.m[0]; v += 32) p.goff[0][v] = nk;
+    }
     __syncthreads();
     if (k >= 1) {  // children of level k-1: the level-k node of each one's first ID
       const int np = p.counts[k - 1];
       for (int n = threadIdx.x; n <= np; n += PS_THREADS)
-        p.cstart[(k - 1) * (cap + 1) + n] = n == np ? nk : Lc[p.first[(k - 1) * cap + n]] - 1;
+        p.cstart[(k - 1) * (cap + 1) + n] = n == np ? nk : Lc[Fp[n]] - 1;
     }
     __syncthreads();
     int* t = Lp;
     Lp = Lc;
     Lc = t;
+    t = Fp;
+    Fp = Fc;
+    Fc = t;
   }
+  mark();  // 4: prefix levels
   {  // the last level: the distinct IDs themselves
     const int k = d - 1;
     for (int u = threadIdx.x; u < U; u += PS_THREADS) {
@@ -247,7 +280,48 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
       p.cstart[(k - 1) * (cap + 1) + n] = n == np ? U : p.first[(k - 1) * cap + n];
   }
   __syncthreads();
-  // per-level digit order (stable by node index) for levels 1..d-1
+  mark();  // 5: last level
+  // per-level digit order (stable by node index) for levels 1..d-1: one
+  // one-pass sort over all levels at once on (level, digit) when the nodes fit
+  // the buffer and the key fits one radix digit; its bucket starts are the
+  // group offsets
+  int tot_nodes = 0, dmax = 1;
+  for (int k = 1; k < d; ++k) {
+    tot_nodes += p.counts[k];
+    while ((1ll << dmax) < c.m[k]) ++dmax;
+  }
+  int lbits = 0;
+  while ((1 << lbits) < d - 1) ++lbits;
+  if (tot_nodes <= PS_MAXB && dmax + lbits <= PS_DBITS) {
+    int off = 0;
+    for (int k = 1; k < d; ++k) {
+      const int nk = p.counts[k];
+      for (int n = threadIdx.x; n < nk; n += PS_THREADS)
+        A[off + n] = (((unsigned long long)(k - 1) << dmax | (unsigned long long)p.digit[k * cap + n]) << PS_IBITS) |
+                     (unsigned long long)n;
+      off += nk;
+    }
+    __syncthreads();
+    unsigned long long* O = ps_sort(A, Bf, tot_nodes, PS_IBITS, PS_IBITS + dmax + lbits, H, wsum, tot, bst);
+    off = 0;
+    for (int k = 1; k < d; ++k) {
+      const int nk = p.counts[k];
+      const unsigned dmask = (1u << dmax) - 1;
+      for (int n = threadIdx.x; n < nk; n += PS_THREADS) {
+        const unsigned long long x = O[off + n];
+        p.sdig[k][n] = (unsigned)(x >> PS_IBITS) & dmask;
+        p.order[k][n] = (int)(x & PS_IMASK);
+      }
+      for (int v = threadIdx.x; v <= c.m[k]; v += PS_THREADS)
+        p.goff[k][v] = v == c.m[k] ? nk : bst[((k - 1) << dmax) | v] - off;
+      off += nk;
+    }
+    __syncthreads();
+    mark();  // 6: digit orders + group offsets
+    mark();  // 7
+    if (p.dbg && threadIdx.x == 0) p.dbg[15] = nmark;
+    return;
+  }
   for (int k = 1; k < d; ++k) {
     const int nk = p.counts[k];
     int dbits = 1;
@@ -262,6 +336,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
     }
     __syncthreads();
   }
+  mark();  // 6: digit orders
   // group offsets: goff[k][v] = first slot whose sorted digit >= v
   for (int k = 0; k < d; ++k) {
     const int nk = p.counts[k];
@@ -275,6 +350,9 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_plan_small(PlanSmallArgs p) {
       p.goff[k][v] = lo;
     }
   }
+  __syncthreads();
+  mark();  // 7: group offsets
+  if (p.dbg && threadIdx.x == 0) p.dbg[15] = nmark;
 }
 
 }  // namespace tt
