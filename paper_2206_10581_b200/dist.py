@@ -80,6 +80,33 @@ def touch_counts(cfg: TTConfig, idx: np.ndarray) -> List[np.ndarray]:
     return out
 
 
+def native_enabled() -> bool:
+    """TT_DIST_NATIVE=0: torch.distributed collectives on the data plane even
+    under NCCL (the engine's own communicator is the default)."""
+    import os
+    return os.environ.get("TT_DIST_NATIVE", "1") != "0"
+
+
+def _native_init(emb, dist, rank: int, world: int) -> bool:
+    """The engine's NCCL communicator over the torch process group; every rank
+    agrees on the outcome, and on failure the wrappers keep the
+    torch.distributed (NCCL) data plane."""
+    import sys
+    import torch
+    ok = 1
+    try:
+        obj = [emb_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        emb.comm_init_rank(obj[0], rank, world)
+    except Exception as e:  # noqa: BLE001 -- reported, then the torch data plane
+        print(f"[tt] rank {rank}: engine NCCL communicator unavailable ({e}); torch.distributed data plane",
+              file=sys.stderr)
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=f"cuda:{emb.device}")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(flag.item())
+
+
 class DataParallelTT:
     """Wraps a TTEmbedding for one rank of a torch.distributed job (position
     sharding).
@@ -99,11 +126,11 @@ class DataParallelTT:
         self.emb = emb
         self.group = group
         self.dist = dist
-        self.native = (dist.is_initialized() and dist.get_backend(group) == "nccl" and group is None)
+        self.native = (dist.is_initialized() and dist.get_backend(group) == "nccl" and group is None
+                       and native_enabled())
         if self.native:
-            obj = [emb_nccl_id() if dist.get_rank() == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            emb.comm_init_rank(obj[0], dist.get_rank(), dist.get_world_size())
+            self.native = _native_init(emb, dist, dist.get_rank(), dist.get_world_size())
+        if self.native:
             self.buf = None
             return
         n = grad_buffer_len(emb.config)
@@ -259,11 +286,10 @@ class OwnerShardedTT:
         # (tt_owner_forward / _backward / _step over its communicator): no torch
         # ops on the rows; torch.distributed ships only the 128-byte NCCL id
         self.native = (comm is None and group is None and dist.is_initialized()
-                       and dist.get_backend() == "nccl")
+                       and dist.get_backend() == "nccl" and native_enabled())
         if self.native:
-            obj = [emb_nccl_id() if dist.get_rank() == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            emb.comm_init_rank(obj[0], self.rank, self.world)
+            self.native = _native_init(emb, dist, self.rank, self.world)
+        if self.native:
             self.buf = None
             return
         self.buf = torch.zeros(grad_buffer_len(cfg), dtype=torch.float32, device=f"cuda:{emb.device}")
