@@ -149,7 +149,9 @@ struct tt_engine {
   // bookkeeping
   bool plan_valid = false;
   bool psave_valid = false;
-  bool ll_fused = false;  // the last forward's GEMM also wrote the output rows (k_fused_fwd8<..., LL>)  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
+  bool ll_fused = false;
+  cudaStream_t s_aux = nullptr;  // side stream: k_fused_w beside the level-F backward (TT_AUX_STREAM)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // the last forward's GEMM also wrote the output rows (k_fused_fwd8<..., LL>)  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
   int64_t cores_version = 0, plan_version = -1;
   int64_t batch_count = 0;
   int64_t launches = 0;
@@ -804,6 +806,17 @@ bool ffma_wdc_enabled(const FusedShape& f) {
   }();
   return m >= 0 ? m == 1 : (f.K == 64 && f.NL == 8);
 }
+// TT_AUX_STREAM=1: k_fused_w on a side stream beside the level-F backward.
+// Off: the two time-share the SMs rather than overlap (papers 2.359 -> 2.357,
+// billion 4.898 -> 4.875, products 0.275 -> 0.319 ms/step)
+bool aux_stream_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_AUX_STREAM");
+    return e && *e == '1';
+  }();
+  return on;
+}
+
 // k_fused_wdc's shape condition (PIPE blocks, K in {32, 64})
 static bool wdc_ok(const FusedShape& f) {
   return (f.K == 32 || f.K == 64) && (int64_t)f.RP * f.nF * f.K <= 2048 && (int64_t)f.RP * f.nF * f.NL <= 256 &&
@@ -1179,6 +1192,45 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   a.mode = 0;
   int rc;
   bool wdc_done = false;  // W_u already formed (k_fused_wdc)
+  // W_u = P_F^T dY_u (k_fused_w) needs only dY and P_F: with TT_AUX_STREAM=1 it
+  // runs on a side stream beside the level-F backward, joined before its
+  // reduction
+  const int WE = f.K * f.NL;
+  auto launch_w = [&](cudaStream_t st) -> int {
+    FusedArgs aw = a;
+    aw.mode = 0;
+    if (false) {
+    }
+#define TT_W_CASE(k_, bn_, rp_, nl_) \
+  else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
+    const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (k_ + 4) + f.RP * f.nF * nl_); \
+    if ((int64_t)f.RP * f.nF * k_ <= 2048 && (int64_t)f.RP * f.nF * nl_ <= 256) { \
+      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_fused_w<k_, nl_, true>), 148 * 8, SK_WARPS * 32, sm_, st, aw, h->counts, h->parent + (d - 1) * cap); \
+    } else { \
+      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
+      LAUNCH((k_fused_w<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, st, aw, h->counts, h->parent + (d - 1) * cap); \
+    } \
+  }
+    TT_FUSED_SHAPES(TT_W_CASE)
+#undef TT_W_CASE
+    return TT_OK;
+  };
+  const bool tc_wdc = h->last_path == 2 && f.K != 128 && (tcbwd_mode(f) == 3 || tcbwd_mode(f) == 4) && wdc_ok(f);
+  const bool ffma_wdc = h->last_path != 2 && ffma_wdc_enabled(f) && wdc_ok(f);
+  const bool w_side = aux_stream_enabled() && !tc_wdc && !ffma_wdc;
+  if (w_side) {
+    if (!h->s_aux) {
+      CU(cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(h->ev_fork, s));
+    CU(cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+    int rcw = launch_w(h->s_aux);
+    if (rcw) return rcw;
+    CU(cudaEventRecord(h->ev_join, h->s_aux));
+  }
   {
     Phase ph(h, 2, s);
     if (h->last_path == 2 && f.K == 128) {
@@ -1328,22 +1380,12 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
     h->gF_ready = true;
   }
   Phase ph_aux(h, 3, s);
-  const int WE = f.K * f.NL;
-#define TT_W_CASE(k_, bn_, rp_, nl_) \
-  else if (f.K == k_ && f.NL == nl_ && f.BN == bn_ && f.RP == rp_) { \
-    const size_t sm_ = sizeof(float) * SK_WARPS * (f.RP * f.nF * (k_ + 4) + f.RP * f.nF * nl_); \
-    if ((int64_t)f.RP * f.nF * k_ <= 2048 && (int64_t)f.RP * f.nF * nl_ <= 256) { \
-      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-      LAUNCH((k_fused_w<k_, nl_, true>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
-    } else { \
-      CU(cudaFuncSetAttribute((k_fused_w<k_, nl_, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_)); \
-      LAUNCH((k_fused_w<k_, nl_, false>), 148 * 8, SK_WARPS * 32, sm_, s, a, h->counts, h->parent + (d - 1) * cap); \
-    } \
+  if (w_side) {
+    CU(cudaStreamWaitEvent(s, h->ev_join, 0));
+  } else if (!wdc_done) {
+    rc = launch_w(s);
+    if (rc) return rc;
   }
-  if (wdc_done) {
-  }
-  TT_FUSED_SHAPES(TT_W_CASE)
-#undef TT_W_CASE
   // wide W rows (128+ float4 columns): 1024 threads, so several sub-groups
   // split each digit group's rows
   if (WE / 4 >= 128)
@@ -1647,6 +1689,12 @@ void tt_engine_destroy(tt_engine* h) {
   if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   if (h->s_h2d) { cudaStreamSynchronize(h->s_h2d); cudaStreamDestroy(h->s_h2d); }
   if (h->s_d2h) { cudaStreamSynchronize(h->s_d2h); cudaStreamDestroy(h->s_d2h); }
+  if (h->s_aux) {
+    cudaStreamSynchronize(h->s_aux);
+    cudaStreamDestroy(h->s_aux);
+    cudaEventDestroy(h->ev_fork);
+    cudaEventDestroy(h->ev_join);
+  }
   for (cudaEvent_t e : {h->ev_up, h->ev_fwd, h->ev_in})
     if (e) cudaEventDestroy(e);
   delete h;
