@@ -1200,10 +1200,12 @@ __global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const 
     bool first = true;
     int pg = 0, pcb = 0, pchunk = 0;
     float* dst_prev = nullptr;
-    // A(t) rows into registers: issued at the end of tile t-1 (under its dA drain)
+    // A rows of tile tt into registers: issued under the previous tile's dC
+    // conversion when tile tt's buffer has landed by then, else after it
     float4 av[NA][2];
-    auto load_A = [&](int sl, int nn) {
-      tc::mbar_wait(&b_full[sl], (t >> 1) & 1);  // (t = the tile being loaded)
+    auto load_A = [&](uint32_t tt, int nn) {
+      const int sl = tt & 1;
+      tc::mbar_wait(&b_full[sl], (tt >> 1) & 1);
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
         const int u = x + i * 32 * TCB3_CONV;
@@ -1217,6 +1219,7 @@ __global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const 
       }
     };
     load_A(0, min(NPT, c.nbn - c.tb));
+    bool a_ready = true;  // av holds tile t's A rows
     for (;;) {
       const int sl = t & 1;
       const int nn = min(NPT, c.nbn - c.tb);
@@ -1275,6 +1278,15 @@ __global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const 
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(b_gt);
       mark(2);
+      // the next tile, and its A rows now if its buffer is already in
+      BwdCursor nx = c;
+      bool nb, ni;
+      const bool more = nx.advance(a, nitems, NPT, nb, ni);
+      a_ready = false;
+      if (more && tc::mbar_test(&b_full[(t + 1) & 1], ((t + 1) >> 1) & 1)) {
+        load_A(t + 1, min(NPT, nx.nbn - nx.tb));
+        a_ready = true;
+      }
       // dA destination of tile t (row cc)
       float* dst_cur;
       {
@@ -1339,11 +1351,11 @@ __global__ void __launch_bounds__(TCB3_THREADS, 1) k_tc_bwd3(FusedArgs a, const 
       pg = c.g;
       pcb = c.cb;
       pchunk = c.chunk;
-      bool nb, ni;
-      if (!c.advance(a, nitems, NPT, nb, ni)) break;
+      if (!more) break;
+      c = nx;
       first = ni;
       ++t;
-      load_A(t & 1, min(NPT, c.nbn - c.tb));
+      if (!a_ready) load_A(t, min(NPT, c.nbn - c.tb));
     }
     // the last tile's dA, the last item's dG_F
     tc::mbar_wait(b_ddone, t & 1);
