@@ -711,6 +711,16 @@ FusedArgs fused_args(tt_engine* h, float* d_out) {
 #define FUSED_CASE_B(k_, bn_, rp_, nl_) \
   else if (f.K == k_ && f.BN == bn_ && f.RP == rp_ && f.NL == nl_) FUSED_LAUNCH((k_fused_bwd<k_, bn_, rp_, nl_>), f.smem_bwd, grid, s, a);
 
+// TT_FWD8W=0 keeps the CTA-synchronous k_fused_fwd8 (tile barriers) instead of
+// the warp-private-tile k_fused_fwd8w
+bool fwd8w_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_FWD8W");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 // TT_FWD8=0 selects the 8 x 4-tile forward (k_fused_fwd) where the 8 x 8 one exists
 bool fwd8_enabled() {
   static const bool on = [] {
@@ -953,11 +963,17 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
   if (fwd && f.BNf == 128 && fwd8_enabled()) {
 #define FWD8_CASE(k_, rp_)                                                                       \
   if (f.K == k_ && f.RP == rp_) {                                                                \
+    bool w8 = false;                                                                             \
     if (a.out && tma_enabled() && core_tmap(h, a.F)) { /* last level fused (fused_forward decided) */ \
       CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
                               (int)fwd8_smem(k_)));                                               \
       tt_launch((k_fused_fwd8<k_, rp_, true, true>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
       h->ll_fused = true;                                                                        \
+    } else if (tma_enabled() && core_tmap(h, a.F) && fwd8w_enabled()) {                         \
+      CU(cudaFuncSetAttribute((k_fused_fwd8w<k_, rp_>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)fwd8w_smem(k_)));                                              \
+      tt_launch((k_fused_fwd8w<k_, rp_>), dim3(grid), dim3(F8_THREADS), fwd8w_smem(k_), s, a, h->tmap[a.F]); \
+      w8 = true;                                                                                 \
     } else if (tma_enabled() && core_tmap(h, a.F)) {                                             \
       CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
                               (int)fwd8_smem(k_)));                                               \
@@ -968,7 +984,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
       tt_launch((k_fused_fwd8<k_, rp_, false>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \
     }                                                                                            \
     ++h->launches;                                                                               \
-    if (a.mode == 0) h->fwd_kernel = "k_fused_fwd8";                                             \
+    if (a.mode == 0) h->fwd_kernel = w8 ? "k_fused_fwd8w" : "k_fused_fwd8";                      \
     return TT_OK;                                                                                \
   }
     TT_FWD8_SHAPES(FWD8_CASE)
@@ -1021,7 +1037,7 @@ WideShape wide_shape(const DevCfg& c, int k) {
   const size_t ints = sizeof(int64_t) * FB_NB + sizeof(int) * (3 * FB_NB + 12) + 16;
   f.smem_fwd = sizeof(float) * (K * (f.BNf + 4) + 2 * FB_BM * K) + ints + sizeof(int) * (3 * FB_IDS + 8) + 16;
   f.CHF = 0;
-  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * BN) + ints + sizeof(int) * (FB_IDS + 8);
+  f.smem_bwd = sizeof(float) * (K * (BN + 4) + FB_BM * K + FB_BM * (BN + 4)) + ints + sizeof(int) * (FB_IDS + 8);
   // the instantiation list pairs (K, BN) -- make sure the forward/backward kernels exist
   bool fwd_ok = false, bwd_ok = false;
 #define TT_CHECK_F(k_, bn_, rp_, nl_) if (K == k_ && f.BNf == bn_ && RP == rp_ && nl == nl_) fwd_ok = true;

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(FB_THREADS, 2) k_fused_fwd(FusedArgs a) {
 
 // dC rows m0..m0+7 of the warp (GEMM layout) for the tile's nodes into Ds:
 // dC[row][col] = sum over the node's IDs and jl of dY_u[(ar, jf, jl)] G_l(u)[r, jl]
-template <int K, int BN, int RP, int NL>
+template <int K, int BN, int RP, int NL, int DS = BN>
 __device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int cb, const int* s_pref, const int* s_cs0,
                                         const int* s_bd, float* Ds, int m0) {
   constexpr int TN = BN / 32;
@@ -426,7 +426,7 @@ __device__ __forceinline__ void form_dC(const FusedArgs& a, int tb, int nn, int 
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * BN, lane, dacc[i]);
+  for (int i = 0; i < 8; ++i) store_row_frag<BN>(Ds + (m0 + i) * DS, lane, dacc[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -628,6 +628,124 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_fused_fwd8 without CTA barriers in the tile loop (round 2, TT_FWD8W):
+// every warp walks its own 16-row warp tiles (16 / RP nodes) of the group --
+// warp tiles w, w + 4, ... -- with a private double-buffered A tile (cp.async,
+// cp.async.wait_group + __syncwarp), so the warps drift apart instead of
+// meeting at a barrier after every 64-row tile, and one warp's A loads and
+// P_F stores overlap the other warps' FFMAs.  The slice block arrives once by
+// TMA.  Lane (rh, cl) owns rows rh, rh + 2, ..., rh + 14 of the warp tile and
+// columns cl*4 ..+4, 64 + cl*4 ..+4; the A tile's row stride is K + 4 floats,
+// so the two half-warps' rows (adjacent) sit in different banks.
+constexpr int F8W_ROWS = 16;
+template <int K>
+__host__ __device__ constexpr int f8w_astride() { return K + 4; }
+inline size_t fwd8w_smem(int K) {
+  return sizeof(float) * ((size_t)K * 128 + (size_t)(F8_THREADS / 32) * 2 * F8W_ROWS * (K + 4)) +
+         sizeof(int) * (F8_THREADS / 32) * 2 * F8W_ROWS + 16;
+}
+
+template <int K, int RP>
+__global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
+    k_fused_fwd8w(FusedArgs a, const __grid_constant__ CUtensorMap tmS) {
+  TT_PDL_ENTRY();
+  constexpr int BN = 128, AS = f8w_astride<K>(), WR = F8W_ROWS, NPW = WR / RP, NW = F8_THREADS / 32;
+  static_assert(WR % RP == 0, "warp tiles hold whole nodes");
+  extern __shared__ __align__(128) float smem[];
+  float* Bs = smem;  // [K][128] (TMA, dense)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* Aw = Bs + K * BN + warp * 2 * WR * AS;                                             // [2][WR][AS]
+  int* s_wnode = reinterpret_cast<int*>(Bs + K * BN + NW * 2 * WR * AS) + warp * 2 * WR;  // [2][NPW]
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<int*>(Bs + K * BN + NW * 2 * WR * AS) + NW * 2 * WR);
+
+  if (tt_failed(a.st)) return;
+  int g, cb, g0, g1, chunk;
+  if (!work_item(a, g, cb, chunk, g0, g1)) return;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(s_bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_expect_tx(s_bar, K * BN * 4);
+    tma_load_2d(Bs, &tmS, s_bar, cb * BN, g * K);
+  }
+  __syncthreads();  // the barrier is initialised before any warp waits on it
+
+  const int ntiles = (g1 - g0 + NPW - 1) / NPW;
+  // A rows of warp tile wt into buffer b: node metadata by lanes < NPW, then
+  // K/4 16-byte cp.async per row (32 lanes x WR*K/128 copies)
+  auto load_tile = [&](int wt, int b) {
+    const int n0 = g0 + wt * NPW;
+    const int nn = min(NPW, g1 - n0);
+    int64_t aoff = 0;
+    if (lane < nn) {
+      const int node = a.orderF[n0 + lane];
+      const int p = a.parentF[node];
+      s_wnode[b * WR + lane] = node;
+      aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0] : (int64_t)p * RP * K;
+    }
+    float* dst = Aw + b * WR * AS;
+#pragma unroll
+    for (int t = 0; t < WR * K / 128; ++t) {
+      const int i = lane + 32 * t, m = i / (K / 4), q = i - m * (K / 4);
+      const int j = m / RP;
+      const int64_t off = __shfl_sync(0xffffffffu, aoff, j);
+      if (j < nn) cp_async16(dst + m * AS + q * 4, a.Abase + off + (m - j * RP) * K + q * 4);
+    }
+  };
+
+  const int rh = lane >> 4, c0 = (lane & 15) * 4;
+  int wt = warp;
+  if (wt < ntiles) load_tile(wt, 0);
+  cp_async_commit();
+  bool s_ready = false;
+  for (int b = 0; wt < ntiles; wt += NW, b ^= 1) {
+    if (wt + NW < ntiles) load_tile(wt + NW, b ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    if (!s_ready) {
+      mbar_wait_parity(s_bar, 0);
+      s_ready = true;
+    }
+    const int nn = min(NPW, g1 - (g0 + wt * NPW));
+    const float* As = Aw + b * WR * AS;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+    for (int kk = 0; kk < K; kk += 4) {
+      float4 av[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float4*>(As + (rh + 2 * i) * AS + kk);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float4 b0 = *reinterpret_cast<const float4*>(Bs + (kk + t) * BN + c0);
+        const float4 b1 = *reinterpret_cast<const float4*>(Bs + (kk + t) * BN + 64 + c0);
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = t == 0 ? av[i].x : t == 1 ? av[i].y : t == 2 ? av[i].z : av[i].w;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(x, bv[j], acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = rh + 2 * i, j = m / RP;
+      if (j < nn) {
+        float* dst = a.Psave + ((int64_t)s_wnode[b * WR + j] * RP + (m - j * RP)) * a.NC + cb * BN;
+        *reinterpret_cast<float4*>(dst + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        *reinterpret_cast<float4*>(dst + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+    __syncwarp();  // buffer b (A rows, node ids) is refilled by the next iteration's load
+  }
+  cp_async_wait<0>();
+}
+
 // (K, RP) instantiations of k_fused_fwd8 (papers, sweep64).  Measured (papers,
 // 1 B200): 0.552 -> 0.541 ms; at K = 32 it was slower (products 0.023 ->
 // 0.025 ms, billion's fused level 1.58 -> 1.73 ms), so those keep k_fused_fwd.
@@ -645,6 +763,9 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   TT_PDL_ENTRY();
   constexpr int BM = FB_BM, SB = BN + 4, TN = BN / 32, TK = K / 8, NPT = BM / RP;
   constexpr int WE = K * NL;
+  // dC row stride: padded by 4 floats so the dA phase's two half-warps (rows
+  // mg, mg + 1) read different banks
+  constexpr int DS = BN + 4;
   constexpr int KG = K < 16 ? K : 16, MG = FB_THREADS / KG, TKA = K / KG, TMA = BM / MG;
   using CM = ColMap<BN>;
   constexpr int W4 = CM::W4, NQ = CM::NQ;
@@ -654,8 +775,8 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
   extern __shared__ __align__(16) float smem[];
   float* Bs = smem;               // [K][SB]
   float* As = Bs + K * SB;        // [BM][K]
-  float* Ds = As + BM * K;        // [BM][BN]  dC
-  int64_t* s_aoff = reinterpret_cast<int64_t*>(Ds + BM * BN);
+  float* Ds = As + BM * K;        // [BM][DS]  dC
+  int64_t* s_aoff = reinterpret_cast<int64_t*>(Ds + BM * DS);
   int* s_node = reinterpret_cast<int*>(s_aoff + FB_NB);
   int* s_cs0 = s_node + FB_NB;
   int* s_pref = s_cs0 + FB_NB;
@@ -715,14 +836,14 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         for (int i = threadIdx.x; i < BM * BN / 4; i += FB_THREADS) {
           const int m = i / (BN / 4), q = i - m * (BN / 4);
           const int j = m / RP;
-          float* dst = Ds + m * BN + q * 4;
+          float* dst = Ds + m * DS + q * 4;
           if (j < nn) cp_async16(dst, a.dPin + ((int64_t)s_node[tb + j] * RP + (m - j * RP)) * a.NC + cb * BN + q * 4);
           else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
       cp_async_commit();
       if (a.mode == 0) {
-        form_dC<K, BN, RP, NL>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds, (threadIdx.x >> 5) * 8);
+        form_dC<K, BN, RP, NL, DS>(a, tb, nn, cb, s_pref, s_cs0, s_bd, Ds, (threadIdx.x >> 5) * 8);
         cp_async_wait<0>();  // slice block + A tile landed
       } else {
         cp_async_wait<0>();  // slice block + A tile + dC tile
@@ -755,11 +876,11 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
 #pragma unroll 8
         for (int m = 0; m < BM; m += 2) {
           ldA(m + 1, a1);
-          load_row_frag<BN>(Ds + (m + 1) * BN, lane, b1);
+          load_row_frag<BN>(Ds + (m + 1) * DS, lane, b1);
           fma_tile(a0, b0);
           if (m + 2 < BM) {
             ldA(m + 2, a0);
-            load_row_frag<BN>(Ds + (m + 2) * BN, lane, b0);
+            load_row_frag<BN>(Ds + (m + 2) * DS, lane, b0);
           }
           fma_tile(a1, b1);
         }
@@ -775,7 +896,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
           for (int j = 0; j < TKA; ++j) xacc[i][j] = 0.f;
         auto ldX = [&](int n, float4* cv, float4* bv) {
 #pragma unroll
-          for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * BN + n);
+          for (int i = 0; i < TMA; ++i) cv[i] = *reinterpret_cast<const float4*>(Ds + (mg + MG * i) * DS + n);
 #pragma unroll
           for (int j = 0; j < TKA; ++j) bv[j] = *reinterpret_cast<const float4*>(Bs + (kg + KG * j) * SB + n);
         };
@@ -1827,7 +1948,7 @@ inline bool fused_plan_shape(const DevCfg& c, FusedShape* s) {
   s->CHF = (int)std::min<size_t>(32, base_f < half ? (half - base_f) / per_id : 0);
   if (s->CHF < 1) s->CHF = (int)std::min<size_t>(8, ((size_t)FB_SMEM_MAX - base_f) / per_id);
   s->smem_fwd = base_f + s->CHF * per_id;
-  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * BN) + ints + sizeof(int) * (FB_IDS + 8);
+  s->smem_bwd = sizeof(float) * (K * SB + FB_BM * K + FB_BM * (BN + 4)) + ints + sizeof(int) * (FB_IDS + 8);
   (void)SG;
   if (s->smem_fwd > (size_t)FB_SMEM_MAX || s->smem_bwd > (size_t)FB_SMEM_MAX) return false;
   s->CHB = 0;
