@@ -28,7 +28,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     extra = os.environ.get("TT_NVCC_EXTRA", "").split()  # diagnostics only, e.g. -DTT_BWD3_TRACE
-    cmd = [NVCC, *FLAGS, *extra, "-o", LIB, os.path.join(SRC, "engine.cu"), "-ldl"]
+    out = os.environ.get("TT_BUILD_OUT", LIB)  # A/B variants (with TT_NVCC_EXTRA=-D...) go elsewhere
+    cmd = [NVCC, *FLAGS, *extra, "-o", out, os.path.join(SRC, "engine.cu"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

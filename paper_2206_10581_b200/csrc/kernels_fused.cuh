@@ -673,33 +673,47 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
   const int ntiles = (g1 - g0 + NPW - 1) / NPW;
   // A rows of warp tile wt into buffer b: node metadata by lanes < NPW, then
   // K/4 16-byte cp.async per row (32 lanes x WR*K/128 copies)
-  auto load_tile = [&](int wt, int b) {
-    const int n0 = g0 + wt * NPW;
-    const int nn = min(NPW, g1 - n0);
-    int64_t aoff = 0;
-    if (lane < nn) {
-      const int node = a.orderF[n0 + lane];
+  // Node metadata for TPB = 32 / NPW consecutive warp tiles at a time (lane l:
+  // tile l / NPW of the batch, node l % NPW): the dependent orderF -> parentF
+  // -> digit0 loads are paid once per TPB tiles, not before every tile's A copy.
+  constexpr int TPB = 32 / NPW;
+  int m_node = 0;
+  int64_t m_aoff = 0;
+  auto fetch_meta = [&](int it0) {
+    const int n = g0 + (warp + NW * (it0 + lane / NPW)) * NPW + lane % NPW;
+    if (n < g1) {
+      const int node = a.orderF[n];
       const int p = a.parentF[node];
-      s_wnode[b * WR + lane] = node;
-      aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0] : (int64_t)p * RP * K;
+      m_node = node;
+      m_aoff = a.F == 1 ? a.c.core_off[0] + (int64_t)a.digit0[p] * a.c.slice[0] : (int64_t)p * RP * K;
     }
+  };
+  // A rows of the warp's tile ordinal `it` (warp tile warp + NW it) into buffer b
+  auto load_tile = [&](int it, int b) {
+    if (it % TPB == 0) fetch_meta(it);
+    const int wt = warp + NW * it;
+    const int nn = min(NPW, g1 - (g0 + wt * NPW));
+    const int lb = (it % TPB) * NPW;  // the tile's first lane in the metadata batch
+    const int node = __shfl_sync(0xffffffffu, m_node, lb + (lane % NPW));
+    if (lane < nn) s_wnode[b * WR + lane] = node;
     float* dst = Aw + b * WR * AS;
 #pragma unroll
     for (int t = 0; t < WR * K / 128; ++t) {
       const int i = lane + 32 * t, m = i / (K / 4), q = i - m * (K / 4);
       const int j = m / RP;
-      const int64_t off = __shfl_sync(0xffffffffu, aoff, j);
+      const int64_t off = __shfl_sync(0xffffffffu, m_aoff, lb + j);
       if (j < nn) cp_async16(dst + m * AS + q * 4, a.Abase + off + (m - j * RP) * K + q * 4);
     }
   };
 
   const int rh = lane >> 4, c0 = (lane & 15) * 4;
-  int wt = warp;
-  if (wt < ntiles) load_tile(wt, 0);
+  const int nit = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;  // this warp's tiles
+  if (nit > 0) load_tile(0, 0);
   cp_async_commit();
   bool s_ready = false;
-  for (int b = 0; wt < ntiles; wt += NW, b ^= 1) {
-    if (wt + NW < ntiles) load_tile(wt + NW, b ^ 1);
+  for (int it = 0, b = 0; it < nit; ++it, b ^= 1) {
+    const int wt = warp + NW * it;
+    if (it + 1 < nit) load_tile(it + 1, b ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();

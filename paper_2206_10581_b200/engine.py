@@ -69,7 +69,7 @@ def load_library(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("TT_LIB_VARIANT") or _build.LIB  # A/B builds of compile-time switches only
     if not os.path.exists(path):
         if not build_if_missing:
             raise ImportError(f"{path} missing: run `python -m paper_2206_10581_b200._build`")
