@@ -561,8 +561,9 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
           *reinterpret_cast<float4*>(dst + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
         }
       }
-      if constexpr (LL) {
-        static_assert(K == 64 && RP == 4, "fused last level: 8 rows = 2 nodes per thread, 2 column blocks per tile");
+      if constexpr (LL && !(K == 64 && RP == 4)) {
+        __trap();  // the fused last level exists for K = 64, RP = 4 only (the host never selects it otherwise)
+      } else if constexpr (LL) {
         constexpr int NLL = 4;
         const unsigned gmask = 0xFFFFu << (lane & 16);
         const int li = lane & 15;
@@ -647,7 +648,7 @@ inline size_t fwd8w_smem(int K) {
 }
 
 template <int K, int RP>
-__global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
+__global__ void __launch_bounds__(F8_THREADS, 3)
     k_fused_fwd8w(FusedArgs a, const __grid_constant__ CUtensorMap tmS) {
   TT_PDL_ENTRY();
   constexpr int BN = 128, AS = f8w_astride<K>(), WR = F8W_ROWS, NPW = WR / RP, NW = F8_THREADS / 32;
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
 // (K, RP) instantiations of k_fused_fwd8 (papers, sweep64).  Measured (papers,
 // 1 B200): 0.552 -> 0.541 ms; at K = 32 it was slower (products 0.023 ->
 // 0.025 ms, billion's fused level 1.58 -> 1.73 ms), so those keep k_fused_fwd.
-#define TT_FWD8_SHAPES(X) X(64, 4)
+#define TT_FWD8_SHAPES(X) X(64, 4) X(32, 16) X(32, 4)
 
 inline size_t fwd8_smem(int K) {
   const size_t NB = F8_THREADS;
