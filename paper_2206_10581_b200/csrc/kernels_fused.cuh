@@ -761,10 +761,13 @@ __global__ void __launch_bounds__(F8_THREADS, 3)
   cp_async_wait<0>();
 }
 
-// (K, RP) instantiations of k_fused_fwd8 (papers, sweep64).  Measured (papers,
-// 1 B200): 0.552 -> 0.541 ms; at K = 32 it was slower (products 0.023 ->
-// 0.025 ms, billion's fused level 1.58 -> 1.73 ms), so those keep k_fused_fwd.
-#define TT_FWD8_SHAPES(X) X(64, 4) X(32, 16) X(32, 4)
+// (K, RP) instantiations of k_fused_fwd8 / k_fused_fwd8w (papers, sweep64,
+// billion, products, sweep32, the papers100M Table-4 shape).  Measured (1 B200):
+// k_fused_fwd8 at papers 0.552 -> 0.541 ms but slower at K = 32 (products 0.023
+// -> 0.025, billion 1.58 -> 1.73 ms); the warp-tile k_fused_fwd8w (the default
+// where TMA is on) is faster everywhere: papers 0.534 -> 0.497, billion 0.969
+// -> 0.796, products 0.023 -> 0.021 (profiles/r02/NOTES.md).
+#define TT_FWD8_SHAPES(X) X(64, 4) X(32, 16) X(32, 4) X(64, 8)
 
 inline size_t fwd8_smem(int K) {
   const size_t NB = F8_THREADS;
