@@ -964,7 +964,13 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
 #define FWD8_CASE(k_, rp_)                                                                       \
   if (f.K == k_ && f.RP == rp_) {                                                                \
     bool w8 = false;                                                                             \
-    if (a.out && tma_enabled() && core_tmap(h, a.F)) { /* last level fused (fused_forward decided) */ \
+    if (a.out && tma_enabled() && core_tmap(h, a.F) && fwd8w_enabled()) { /* last level fused */  \
+      CU(cudaFuncSetAttribute((k_fused_fwd8w<k_, rp_, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)fwd8w_smem(k_)));                                              \
+      tt_launch((k_fused_fwd8w<k_, rp_, true>), dim3(grid), dim3(F8_THREADS), fwd8w_smem(k_), s, a, h->tmap[a.F]); \
+      h->ll_fused = true;                                                                        \
+      w8 = true;                                                                                 \
+    } else if (a.out && tma_enabled() && core_tmap(h, a.F)) { /* last level fused (fused_forward decided) */ \
       CU(cudaFuncSetAttribute((k_fused_fwd8<k_, rp_, true, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, \
                               (int)fwd8_smem(k_)));                                               \
       tt_launch((k_fused_fwd8<k_, rp_, true, true>), dim3(grid), dim3(F8_THREADS), fwd8_smem(k_), s, a, h->tmap[a.F]); \

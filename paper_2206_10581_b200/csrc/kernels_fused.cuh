@@ -647,7 +647,17 @@ inline size_t fwd8w_smem(int K) {
          sizeof(int) * (F8_THREADS / 32) * 2 * F8W_ROWS + 16;
 }
 
-template <int K, int RP>
+// LL (K = 64, RP = 4, NL = 4; TT_FWD_LL=1): the last level in the warp tile's
+// epilogue.  For each distinct ID u of the tile's 4 nodes, lane (rh, cl) forms
+// the 16 partial outputs (a = rh + 2 aa, column block 2 cb + h, jl) over its 4
+// ranks c0..c0+3, the 16 lanes of a half-warp reduce-scatter them (xor 8, 4,
+// 2, 1: 15 shuffles) so lane cl keeps output (aa, h, jl) = (cl / 8, cl / 4 % 2,
+// cl % 4), and write it to every batch position of u (heavy IDs: their Yu row,
+// scattered later by k_scatter_heavy).  The nodes' ID ranges are fetched before
+// the tile's GEMM and the IDs' digits / position ranges lane-parallel after it,
+// so one warp's epilogue latency runs under the other warps' FFMAs (no CTA
+// barrier couples them).  k_last_level then does not run.
+template <int K, int RP, bool LL = false>
 __global__ void __launch_bounds__(F8_THREADS, 3)
     k_fused_fwd8w(FusedArgs a, const __grid_constant__ CUtensorMap tmS) {
   TT_PDL_ENTRY();
@@ -724,6 +734,14 @@ __global__ void __launch_bounds__(F8_THREADS, 3)
     }
     const int nn = min(NPW, g1 - (g0 + wt * NPW));
     const float* As = Aw + b * WR * AS;
+    int ll_c0 = 0, ll_c1 = 0;  // LL: lane j < nn holds node j's distinct-ID range
+    if constexpr (LL) {
+      if (lane < nn) {
+        const int node = s_wnode[b * WR + lane];
+        ll_c0 = __ldg(a.cstartF + node);
+        ll_c1 = __ldg(a.cstartF + node + 1);
+      }
+    }
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -754,6 +772,88 @@ __global__ void __launch_bounds__(F8_THREADS, 3)
         float* dst = a.Psave + ((int64_t)s_wnode[b * WR + j] * RP + (m - j * RP)) * a.NC + cb * BN;
         *reinterpret_cast<float4*>(dst + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
         *reinterpret_cast<float4*>(dst + 64 + c0) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+    if constexpr (LL && !(K == 64 && RP == 4)) {
+      __trap();  // the fused last level exists for K = 64, RP = 4, NL = 4 only (the host never selects it otherwise)
+    } else if constexpr (LL) {
+      constexpr int NLL = 4;
+      const int cl = lane & 15;
+      const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+      const int64_t sliceL = a.c.slice[a.c.d - 1];
+      const int64_t emb = a.c.emb_dim, npad = a.c.npad;
+      const int oaa = cl >> 3, oh = (cl >> 2) & 1, ojl = cl & 3;
+      const int64_t col = ((int64_t)(rh + 2 * oaa) * a.nF + 2 * cb + oh) * NLL + ojl;
+      // exclusive prefix of the nodes' ID counts (lanes 0..3)
+      const int cnt = ll_c1 - ll_c0;
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < NPW; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const int T = __shfl_sync(0xffffffffu, x, NPW - 1);
+      const int off = x - cnt;
+      for (int t0 = 0; t0 < T; t0 += 32) {
+        // lane i: metadata of the tile's ID t0 + i (node j, u, last digit, positions)
+        const int f = t0 + lane;
+        int jf_ = 0;
+#pragma unroll
+        for (int jj = 1; jj < NPW; ++jj)
+          if (f >= __shfl_sync(0xffffffffu, off, jj)) jf_ = jj;
+        const int fo = __shfl_sync(0xffffffffu, off, jf_), fc0 = __shfl_sync(0xffffffffu, ll_c0, jf_);
+        int mu = 0, mdg = 0, ms0 = 0, ms1 = 0;
+        if (f < T) {
+          mu = fc0 + (f - fo);
+          mdg = __ldg(a.digitL + mu);
+          ms0 = __ldg(a.seg + mu);
+          ms1 = __ldg(a.seg + mu + 1);
+        }
+        const int nk = min(32, T - t0);
+        for (int k = 0; k < nk; ++k) {
+          const int j = __shfl_sync(0xffffffffu, jf_, k), u = __shfl_sync(0xffffffffu, mu, k);
+          const int dg = __shfl_sync(0xffffffffu, mdg, k);
+          const int s0 = __shfl_sync(0xffffffffu, ms0, k), s1 = __shfl_sync(0xffffffffu, ms1, k);
+          const float4* gp = reinterpret_cast<const float4*>(Gl + (int64_t)dg * sliceL + c0 * NLL);
+          float4 gv[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) gv[t] = __ldg(gp + t);
+          float v[16];  // v[aa * 8 + h * 4 + jl]
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < NPW; ++jj) {
+            if (jj != j) continue;  // warp-uniform: the node's two rows of this lane
+#pragma unroll
+            for (int aa = 0; aa < 2; ++aa)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const float xv = acc[2 * jj + aa][4 * hh + t];
+                  v[aa * 8 + hh * 4 + 0] = fmaf(xv, gv[t].x, v[aa * 8 + hh * 4 + 0]);
+                  v[aa * 8 + hh * 4 + 1] = fmaf(xv, gv[t].y, v[aa * 8 + hh * 4 + 1]);
+                  v[aa * 8 + hh * 4 + 2] = fmaf(xv, gv[t].z, v[aa * 8 + hh * 4 + 2]);
+                  v[aa * 8 + hh * 4 + 3] = fmaf(xv, gv[t].w, v[aa * 8 + hh * 4 + 3]);
+                }
+          }
+#pragma unroll
+          for (int step = 0; step < 4; ++step) {
+            const int half = 8 >> step;
+            const bool hi = (cl >> (3 - step)) & 1;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const float give = hi ? v[i] : v[half + i];
+              const float keep = hi ? v[half + i] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, give, half);
+            }
+          }
+          if (s1 - s0 > HEAVY_POS) {
+            a.Yu[(int64_t)u * npad + col] = v[0];
+          } else if (col < emb) {
+            for (int sl = s0; sl < s1; ++sl) a.out[(int64_t)__ldg(a.spos + sl) * emb + col] = v[0];
+          }
+        }
       }
     }
     __syncwarp();  // buffer b (A rows, node ids) is refilled by the next iteration's load
