@@ -913,10 +913,47 @@ bool core_tmap(tt_engine* h, int k) {
   return h->tmap_ok[k];
 }
 
+// TT_LRBWD=0 keeps k_fused_bwd at ranks <= 16 instead of the low-rank
+// streaming backward k_lowrank_bwd
+bool lrbwd_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TT_LRBWD");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaStream_t s) {
   const FusedShape& f = h->fs;
   FusedArgs a = a0;
   const int groups = grid0 / a.ncb;
+  if (!fwd && a.mode == 0 && a.ncb == 1 && f.K <= 16 && lrbwd_enabled()) {
+    // low-rank streaming backward: one warp per (digit group, chunk of >= 1 node)
+    a.split = LR_SPLIT;
+    a.split_rows = f.RP;
+    const int64_t need = (int64_t)groups * a.split * h->dc.slice[a.F];
+    if (h->F.cap_gsplit < need) {
+      cudaFree(h->F.gsplit);
+      h->F.gsplit = nullptr;
+      h->F.cap_gsplit = 0;
+      CU(dalloc(&h->F.gsplit, need));
+      h->F.cap_gsplit = need;
+    }
+    a.gsplit = h->F.gsplit;
+    const int lgrid = (int)(((int64_t)groups * a.split + LR_WARPS - 1) / LR_WARPS);
+#define LR_CASE(k_, rp_, nl_, cpl_)                                                              \
+    if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC == 32 * cpl_) {                          \
+      LAUNCH((k_lowrank_bwd<k_, rp_, nl_, cpl_>), lgrid, LR_WARPS * 32, 0, s, a);                 \
+      LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
+             a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
+      h->bwd_kernel = "k_lowrank_bwd";                                                           \
+      return TT_OK;                                                                              \
+    }
+    TT_LOWRANK_SHAPES(LR_CASE)
+#undef LR_CASE
+    a.split = 0;  // (no instantiation: the general kernels below)
+    a.gsplit = nullptr;
+  }
   a.split = split_for(h, grid0, a.F, fwd);
   // min rows per chunk: the forward (a short GEMM per tile, then stores) only
   // pays off with long chunks; the backward (dC formation latency-bound) with

@@ -2004,6 +2004,163 @@ __global__ void k_fused_reduce_gsplit(DevCfg c, int F, int split, int split_rows
   }
 }
 
+// ---------------------------------------------------------------------------
+// Low-rank streaming backward (round 2, K <= 16: small, sweep8, sweep16).  At
+// these ranks the level-F GEMMs are a few FMAs per upstream float and
+// k_fused_bwd is bound by forming dC one ID at a time per warp, then waiting
+// at the tile barrier for the warp with the most IDs (sweep8 ncu: barrier 47%,
+// long_scoreboard 34% of stall samples, issue 17%).  Here every warp owns a
+// chunk of one digit group's nodes (work_item_at over groups x LR_SPLIT
+// chunks; the chunks' dG_F partials are summed by k_fused_reduce_gsplit in
+// chunk order) and walks it with no barrier at all:
+//   lane l owns the CPL columns c = l + 32 i of the level-F block (NC = 32 CPL,
+//   column c = jf K + r) and keeps S_g[:, c] (the slice) and dG_F[:, c] in
+//   registers;
+//   per node: its A rows (core-0 slice or P_{F-1} rows, RP x K) staged in the
+//   warp's shared memory; dC[ar][c] = sum over the node's IDs u (digits
+//   fetched lane-parallel, up to 32 per load) of sum_jl dY_u[ar, jf, jl]
+//   G_last[i_d(u)][r, jl]; dG_F[k][c] += sum_ar A[ar][k] dC[ar][c];
+//   dA[ar][k] = sum_c dC[ar][c] S[k][c] as RP K per-lane partials,
+//   reduce-scattered over the warp (lane l ends with entries l RP K / 32 ..)
+//   and written as the node's dP_{F-1} partial (ncb = 1).
+// Every sum runs in a fixed order (IDs in distinct-ID order, lanes in a fixed
+// butterfly), so results are deterministic.
+constexpr int LR_WARPS = 4, LR_SPLIT = 32;
+template <int K, int RP, int NL, int CPL>
+__global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int NC = 32 * CPL, V = RP * K, VL = V / 32;
+  static_assert(V % 32 == 0 && V >= 32, "RP K must be a multiple of 32");
+  __shared__ float s_A[LR_WARPS][RP * K];
+  if (tt_failed(a.st)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * LR_WARPS + warp;
+  if (it >= a.c.m[a.F] * a.split) return;
+  int g, cb, chunk, g0, g1;
+  if (!work_item_at(a, it, g, cb, chunk, g0, g1)) return;
+  const int nF = a.nF;
+  const int64_t npad = a.c.npad;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const float* S = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F];
+  int jf[CPL], rr[CPL];
+  float sv[K][CPL], gacc[K][CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int col = lane + 32 * i;
+    jf[i] = col / K;
+    rr[i] = col % K;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      sv[k][i] = __ldg(S + (int64_t)k * NC + col);
+      gacc[k][i] = 0.f;
+    }
+  }
+  float* sA = s_A[warp];
+  for (int n = g0; n < g1; ++n) {
+    const int node = __ldg(a.orderF + n);
+    const int p = __ldg(a.parentF + node);
+    const float* Ap = a.Abase + (a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
+                                          : (int64_t)p * RP * K);
+    __syncwarp();  // the previous node's A rows are no longer read
+#pragma unroll
+    for (int t = 0; t < V / 32; ++t) sA[lane + 32 * t] = __ldg(Ap + lane + 32 * t);
+    const int c0 = __ldg(a.cstartF + node), c1 = __ldg(a.cstartF + node + 1);
+    float dc[RP][CPL];
+#pragma unroll
+    for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) dc[ar][i] = 0.f;
+    // an ID's operands: its last-core slice row r of column c and the node's
+    // RP upstream row parts (jf(c), 0..NL) -- two IDs in flight (registers
+    // double-buffered; static buffers, the loop is unrolled by two)
+    float gA[CPL][NL], yA[CPL][RP][NL], gB[CPL][NL], yB[CPL][RP][NL];
+    auto ld_id = [&](int u, int dg, float (&gv)[CPL][NL], float (&yv)[CPL][RP][NL]) {
+      const float* Gp = Gl + (int64_t)dg * sliceL;
+      const float* Yp = a.dY + (int64_t)u * npad;
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        ldg_vec<NL>(Gp + rr[i] * NL, gv[i]);
+#pragma unroll
+        for (int ar = 0; ar < RP; ++ar) ldg_vec<NL>(Yp + ((int64_t)ar * nF + jf[i]) * NL, yv[i][ar]);
+      }
+    };
+    auto acc_id = [&](const float (&gv)[CPL][NL], const float (&yv)[CPL][RP][NL]) {
+#pragma unroll
+      for (int i = 0; i < CPL; ++i)
+#pragma unroll
+        for (int ar = 0; ar < RP; ++ar) {
+          float s = dc[ar][i];
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[i][ar][jl], gv[i][jl], s);
+          dc[ar][i] = s;
+        }
+    };
+    for (int u0 = c0; u0 < c1; u0 += 32) {
+      const int nu = min(32, c1 - u0);
+      const int my_dg = lane < nu ? __ldg(a.digitL + u0 + lane) : 0;
+      ld_id(u0, __shfl_sync(0xffffffffu, my_dg, 0), gA, yA);
+      for (int q = 0; q < nu; q += 2) {
+        const int dgB = __shfl_sync(0xffffffffu, my_dg, (q + 1) & 31);
+        const int dgA = __shfl_sync(0xffffffffu, my_dg, (q + 2) & 31);
+        if (q + 1 < nu) ld_id(u0 + q + 1, dgB, gB, yB);
+        acc_id(gA, yA);
+        if (q + 1 < nu) {
+          if (q + 2 < nu) ld_id(u0 + q + 2, dgA, gA, yA);
+          acc_id(gB, yB);
+        }
+      }
+    }
+    __syncwarp();  // sA complete
+    // dG_F[k][c] += sum_ar A[ar][k] dC[ar][c]
+#pragma unroll
+    for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float av = sA[ar * K + k];
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) gacc[k][i] = fmaf(av, dc[ar][i], gacc[k][i]);
+      }
+    // dA[ar][k] = sum_c dC[ar][c] S[k][c], 32 entries at a time: per-lane
+    // partials, then a butterfly reduce-scatter (lane l keeps entry t 32 + l)
+    float* dst = a.dPc + (int64_t)node * V;  // ncb = 1
+#pragma unroll
+    for (int t = 0; t < VL; ++t) {
+      float v[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int ar = (t * 32 + e) / K, k = (t * 32 + e) % K;
+        float x = 0.f;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) x = fmaf(dc[ar][i], sv[k][i], x);
+        v[e] = x;
+      }
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        const int half = 16 >> st;
+        const bool hi = (lane >> (4 - st)) & 1;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const float give = hi ? v[i] : v[half + i];
+          const float keep = hi ? v[half + i] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, give, half);
+        }
+      }
+      dst[t * 32 + lane] = v[0];
+    }
+  }
+  float* gdst = a.split > 1 ? a.gsplit + ((int64_t)g * a.split + chunk) * a.c.slice[a.F]
+                            : a.grads + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) gdst[(int64_t)k * NC + lane + 32 * i] = gacc[k][i];
+}
+
+// (K, RP, NL, CPL) instantiations of k_lowrank_bwd: sweep8 (at R = 16 --
+// sweep16, small -- it measured slower than k_fused_bwd: profiles/r02/NOTES.md)
+#define TT_LOWRANK_SHAPES(X) X(8, 4, 8, 1)
+
 // The (K, BN, RP, NL) instantiations compiled into the library (engine.cu
 // FUSED_SWITCH): papers, products / sweep32, small (and the paper's Table-4
 // arxiv / papers100M shapes at R = 16), billion, sweep16, sweep64, sweep128,
