@@ -107,6 +107,20 @@ def test_every_bwdk32_instantiation_has_a_parity_case():
     assert not missing, f"compiled rank-32 backward instantiations with no parity case: {missing}"
 
 
+def test_every_lowrank_backward_instantiation_has_a_parity_case():
+    # k_lowrank_bwd<K, RP, NL, CPL> (TT_LOWRANK_SHAPES): one column block of NC = 32 CPL
+    src = open(os.path.join(CSRC, "kernels_fused.cuh")).read()
+    m = re.search(r"#define\s+TT_LOWRANK_SHAPES\(X\)([^\n]*)", src)
+    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", m.group(1))}
+    assert compiled
+    covered = set()
+    for name in FUSED_SHAPES:
+        ffma, _ = reached(SHAPES[name][0]())
+        covered |= {(t[0], t[2], t[3], t[1] // 32) for t in ffma if t[0] <= 16 and t[3] != "*" and t[1] % 32 == 0}
+    missing = sorted(t for t in compiled if t not in covered)
+    assert not missing, f"compiled low-rank backward instantiations with no parity case: {missing}"
+
+
 def test_every_rank128_tcgen05_instantiation_has_a_parity_case():
     src = open(os.path.join(CSRC, "kernels_tcgen05.cuh")).read()
     m = re.search(r"#define\s+TT_TC128_SHAPES\(X\)([^\n]*)", src)
