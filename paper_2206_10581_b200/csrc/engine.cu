@@ -150,6 +150,7 @@ struct tt_engine {
   bool plan_valid = false;
   bool psave_valid = false;
   bool ll_fused = false;
+  bool lr_w = false;  // the last backward's k_lowrank_bwd also formed W_u (k_fused_w skipped)
   cudaStream_t s_aux = nullptr;  // side stream: k_fused_w beside the level-F backward (TT_AUX_STREAM)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // the last forward's GEMM also wrote the output rows (k_fused_fwd8<..., LL>)  // Psave holds P_F (false once k_fused_wdc wrote dC over it)
   int64_t cores_version = 0, plan_version = -1;
@@ -944,6 +945,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
 #define LR_CASE(k_, rp_, nl_, cpl_)                                                              \
     if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC == 32 * cpl_) {                          \
       LAUNCH((k_lowrank_bwd<k_, rp_, nl_, cpl_>), lgrid, LR_WARPS * 32, 0, s, a);                 \
+      h->lr_w = cpl_ == 1 && f.NC == 32 && (32 / f.K) >= 2 && (32 / f.K) * 2 <= f.NL;           \
       LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
              a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
       h->bwd_kernel = "k_lowrank_bwd";                                                           \
@@ -1251,6 +1253,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   a.mode = 0;
   int rc;
   bool wdc_done = false;  // W_u already formed (k_fused_wdc)
+  h->lr_w = false;
   // W_u = P_F^T dY_u (k_fused_w) needs only dY and P_F: with TT_AUX_STREAM=1 it
   // runs on a side stream beside the level-F backward, joined before its
   // reduction
@@ -1441,7 +1444,7 @@ int fused_backward(tt_engine* h, const float* d_up, cudaStream_t s) {
   Phase ph_aux(h, 3, s);
   if (w_side) {
     CU(cudaStreamWaitEvent(s, h->ev_join, 0));
-  } else if (!wdc_done) {
+  } else if (!wdc_done && !h->lr_w) {
     rc = launch_w(s);
     if (rc) return rc;
   }

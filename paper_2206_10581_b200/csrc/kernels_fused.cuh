@@ -2085,7 +2085,17 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
         for (int ar = 0; ar < RP; ++ar) ldg_vec<NL>(Yp + ((int64_t)ar * nF + jf[i]) * NL, yv[i][ar]);
       }
     };
-    auto acc_id = [&](const float (&gv)[CPL][NL], const float (&yv)[CPL][RP][NL]) {
+    // WF (CPL = 1): the last core's W_u = P_F^T dY_u here too (k_fused_w does
+    // not run): lane (jf, r) forms sum_ar P_F[ar][(jf, r)] dY_u[ar, jf, :], the
+    // lanes of one r (jf = 0..nF-1, K apart) reduce-scatter the NL sums, and
+    // each writes NL / nF of W_u[r][:]
+    constexpr bool WF = CPL == 1 && NC == 32 && (NC / K) * 2 <= NL && (NC / K) >= 2 && ((NC / K) & (NC / K - 1)) == 0;
+    float pf[RP];
+    if constexpr (WF) {
+#pragma unroll
+      for (int ar = 0; ar < RP; ++ar) pf[ar] = __ldg(a.Psave + (int64_t)node * RP * NC + ar * NC + lane);
+    }
+    auto acc_id = [&](int u, const float (&gv)[CPL][NL], const float (&yv)[CPL][RP][NL]) {
 #pragma unroll
       for (int i = 0; i < CPL; ++i)
 #pragma unroll
@@ -2095,6 +2105,42 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
           for (int jl = 0; jl < NL; ++jl) s = fmaf(yv[i][ar][jl], gv[i][jl], s);
           dc[ar][i] = s;
         }
+      if constexpr (WF) {
+        constexpr int NFL = NC / K;  // lanes sharing a rank column r
+        float w[NL];
+#pragma unroll
+        for (int jl = 0; jl < NL; ++jl) {
+          float x = 0.f;
+#pragma unroll
+          for (int ar = 0; ar < RP; ++ar) x = fmaf(pf[ar], yv[0][ar][jl], x);
+          w[jl] = x;
+        }
+        // reduce-scatter over the jf bits of the lane (distances 16, 8, .. K)
+        int len = NL;
+#pragma unroll
+        for (int dist = 16; dist >= K; dist >>= 1) {
+          const int half = len >> 1;
+          const bool hi = (lane & dist) != 0;
+#pragma unroll
+          for (int i = 0; i < NL / 2; ++i)
+            if (i < half) {
+              const float give = hi ? w[i] : w[half + i];
+              const float keep = hi ? w[half + i] : w[i];
+              w[i] = keep + __shfl_xor_sync(0xffffffffu, give, dist);
+            }
+          len = half;
+        }
+        // lane (jf, r) holds W_u[r][jl0 .. jl0 + NL / NFL), jl0 = the jf bits read high to low
+        int jl0 = 0, blk = NL;
+#pragma unroll
+        for (int dist = 16; dist >= K; dist >>= 1) {
+          blk >>= 1;
+          if (lane & dist) jl0 += blk;
+        }
+        float* wd = a.W + (int64_t)u * K * NL + (lane % K) * NL + jl0;
+#pragma unroll
+        for (int i = 0; i < NL / NFL; ++i) wd[i] = w[i];
+      }
     };
     for (int u0 = c0; u0 < c1; u0 += 32) {
       const int nu = min(32, c1 - u0);
@@ -2104,10 +2150,10 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
         const int dgB = __shfl_sync(0xffffffffu, my_dg, (q + 1) & 31);
         const int dgA = __shfl_sync(0xffffffffu, my_dg, (q + 2) & 31);
         if (q + 1 < nu) ld_id(u0 + q + 1, dgB, gB, yB);
-        acc_id(gA, yA);
+        acc_id(u0 + q, gA, yA);
         if (q + 1 < nu) {
           if (q + 2 < nu) ld_id(u0 + q + 2, dgA, gA, yA);
-          acc_id(gB, yB);
+          acc_id(u0 + q + 1, gB, yB);
         }
       }
     }
