@@ -945,7 +945,7 @@ int fused_dispatch(tt_engine* h, bool fwd, const FusedArgs& a0, int grid0, cudaS
 #define LR_CASE(k_, rp_, nl_, cpl_)                                                              \
     if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC == 32 * cpl_) {                          \
       LAUNCH((k_lowrank_bwd<k_, rp_, nl_, cpl_>), lgrid, LR_WARPS * 32, 0, s, a);                 \
-      h->lr_w = cpl_ == 1 && f.NC == 32 && (32 / f.K) >= 2 && (32 / f.K) * 2 <= f.NL;           \
+      h->lr_w = (32 / f.K) >= 1 && f.NL % (32 / f.K) == 0;                                       \
       LAUNCH(k_fused_reduce_gsplit, grid_for((int64_t)groups * h->dc.slice[a.F] / 4, 256, 148 * 8), 256, 0, s, h->dc, \
              a.F, a.split, a.split_rows, a.goffF, (const float*)a.gsplit, a.grads, a.st);      \
       h->bwd_kernel = "k_lowrank_bwd";                                                           \

@@ -2074,7 +2074,7 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
     // an ID's operands: its last-core slice row r of column c and the node's
     // RP upstream row parts (jf(c), 0..NL) -- two IDs in flight (registers
     // double-buffered; static buffers, the loop is unrolled by two)
-    float gA[CPL][NL], yA[CPL][RP][NL], gB[CPL][NL], yB[CPL][RP][NL];
+    float gA[CPL][NL], yA[CPL][RP][NL], gB[CPL == 1 ? CPL : 1][NL], yB[CPL == 1 ? CPL : 1][RP][NL];
     auto ld_id = [&](int u, int dg, float (&gv)[CPL][NL], float (&yv)[CPL][RP][NL]) {
       const float* Gp = Gl + (int64_t)dg * sliceL;
       const float* Yp = a.dY + (int64_t)u * npad;
@@ -2089,11 +2089,14 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
     // not run): lane (jf, r) forms sum_ar P_F[ar][(jf, r)] dY_u[ar, jf, :], the
     // lanes of one r (jf = 0..nF-1, K apart) reduce-scatter the NL sums, and
     // each writes NL / nF of W_u[r][:]
-    constexpr bool WF = CPL == 1 && NC == 32 && (NC / K) * 2 <= NL && (NC / K) >= 2 && ((NC / K) & (NC / K - 1)) == 0;
-    float pf[RP];
+    constexpr int NFL = 32 / K;  // lanes sharing a rank column r (the jf bits of the lane)
+    constexpr bool WF = NFL >= 1 && NL % NFL == 0;
+    float pf[RP][CPL];
     if constexpr (WF) {
 #pragma unroll
-      for (int ar = 0; ar < RP; ++ar) pf[ar] = __ldg(a.Psave + (int64_t)node * RP * NC + ar * NC + lane);
+      for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) pf[ar][i] = __ldg(a.Psave + (int64_t)node * RP * NC + ar * NC + lane + 32 * i);
     }
     auto acc_id = [&](int u, const float (&gv)[CPL][NL], const float (&yv)[CPL][RP][NL]) {
 #pragma unroll
@@ -2106,13 +2109,14 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
           dc[ar][i] = s;
         }
       if constexpr (WF) {
-        constexpr int NFL = NC / K;  // lanes sharing a rank column r
         float w[NL];
 #pragma unroll
         for (int jl = 0; jl < NL; ++jl) {
           float x = 0.f;
 #pragma unroll
-          for (int ar = 0; ar < RP; ++ar) x = fmaf(pf[ar], yv[0][ar][jl], x);
+          for (int i = 0; i < CPL; ++i)
+#pragma unroll
+            for (int ar = 0; ar < RP; ++ar) x = fmaf(pf[ar][i], yv[i][ar][jl], x);
           w[jl] = x;
         }
         // reduce-scatter over the jf bits of the lane (distances 16, 8, .. K)
@@ -2145,6 +2149,12 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
     for (int u0 = c0; u0 < c1; u0 += 32) {
       const int nu = min(32, c1 - u0);
       const int my_dg = lane < nu ? __ldg(a.digitL + u0 + lane) : 0;
+      if constexpr (CPL > 1) {  // (two IDs' operands would not fit the registers)
+        for (int q = 0; q < nu; ++q) {
+          ld_id(u0 + q, __shfl_sync(0xffffffffu, my_dg, q), gA, yA);
+          acc_id(u0 + q, gA, yA);
+        }
+      } else {
       ld_id(u0, __shfl_sync(0xffffffffu, my_dg, 0), gA, yA);
       for (int q = 0; q < nu; q += 2) {
         const int dgB = __shfl_sync(0xffffffffu, my_dg, (q + 1) & 31);
@@ -2155,6 +2165,7 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
           if (q + 2 < nu) ld_id(u0 + q + 2, dgA, gA, yA);
           acc_id(u0 + q + 1, gB, yB);
         }
+      }
       }
     }
     __syncwarp();  // sA complete
@@ -2203,8 +2214,9 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
     for (int i = 0; i < CPL; ++i) gdst[(int64_t)k * NC + lane + 32 * i] = gacc[k][i];
 }
 
-// (K, RP, NL, CPL) instantiations of k_lowrank_bwd: sweep8 (at R = 16 --
-// sweep16, small -- it measured slower than k_fused_bwd: profiles/r02/NOTES.md)
+// (K, RP, NL, CPL) instantiations of k_lowrank_bwd: sweep8.  At R = 16 (CPL 2:
+// one ID's operands at a time) it measured slower than k_fused_bwd + k_fused_w
+// (sweep16 0.454 -> 0.485 ms/step, small 0.144 -> 0.146; profiles/r02/NOTES.md)
 #define TT_LOWRANK_SHAPES(X) X(8, 4, 8, 1)
 
 // The (K, BN, RP, NL) instantiations compiled into the library (engine.cu
