@@ -2214,6 +2214,115 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
     for (int i = 0; i < CPL; ++i) gdst[(int64_t)k * NC + lane + 32 * i] = gacc[k][i];
 }
 
+// Low-rank streaming forward (round 2, R = 8 with one 32-column block: the
+// rank sweep's R = 8).  k_fused_fwd's 64-row GEMM tiles are a few FMAs per
+// loaded float here, and k_last_level then re-reads every P_F block; instead
+// a warp walks a chunk of one digit group's nodes (the backward's work items):
+//   lane l = level-F column (jf, r) keeps S_g[:, l] in registers;
+//   per node: P_F[ar][l] = sum_k A[ar][k] S[k][l] (A rows broadcast by
+//   shuffles), stored for the backward; then for each distinct ID u of the
+//   node (digits / position ranges fetched lane-parallel) the lane's 32
+//   partial outputs P_F[ar][l] G_last[i_d(u)][r, jl] are reduce-scattered over
+//   the 8 lanes of its jf (xor 4, 2, 1) so lane (jf, r) holds outputs
+//   (ar = r / 2, jf, jl = 4 (r % 2) ..+4): one float4 per lane and position, the
+//   warp writing the whole 128-float row (heavy IDs: their Yu row, scattered
+//   later by k_scatter_heavy).
+template <int K, int RP, int NL>
+__global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_fwd(FusedArgs a) {
+  TT_PDL_ENTRY();
+  constexpr int NC = 32, NFJ = NC / K;
+  static_assert(RP * K == 32 && RP * NL == 32 && K == 8, "one lane per A element and per output quad");
+  if (tt_failed(a.st)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * LR_WARPS + warp;
+  if (it >= a.c.m[a.F] * a.split) return;
+  int g, cb, chunk, g0, g1;
+  if (!work_item_at(a, it, g, cb, chunk, g0, g1)) return;
+  const int r = lane % K, jf = lane / K;
+  const float* Gl = a.params + a.c.core_off[a.c.d - 1];
+  const int64_t sliceL = a.c.slice[a.c.d - 1];
+  const int64_t emb = a.c.emb_dim, npad = a.c.npad;
+  const float* S = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F];
+  float sv[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) sv[k] = __ldg(S + k * NC + lane);
+  // this lane's output quad: entries e0 .. e0 + 3 of (ar NL + jl), e0 = 4 r
+  const int oar = (4 * r) / NL, ojl = (4 * r) % NL;
+  const int64_t ocol = ((int64_t)oar * NFJ + jf) * NL + ojl;
+  for (int n = g0; n < g1; ++n) {
+    const int node = __ldg(a.orderF + n);
+    const int p = __ldg(a.parentF + node);
+    const float* Ap = a.Abase + (a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
+                                          : (int64_t)p * RP * K);
+    const float my_a = __ldg(Ap + lane);  // A[ar][k] at lane ar K + k
+    const int c0 = __ldg(a.cstartF + node), c1 = __ldg(a.cstartF + node + 1);
+    float pf[RP];
+#pragma unroll
+    for (int ar = 0; ar < RP; ++ar) {
+      float x = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) x = fmaf(__shfl_sync(0xffffffffu, my_a, ar * K + k), sv[k], x);
+      pf[ar] = x;
+      a.Psave[(int64_t)node * RP * NC + ar * NC + lane] = x;
+    }
+    for (int u0 = c0; u0 < c1; u0 += 32) {
+      const int nu = min(32, c1 - u0);
+      int my_dg = 0, my_s0 = 0, my_s1 = 0, my_p0 = 0;
+      if (lane < nu) {
+        my_dg = __ldg(a.digitL + u0 + lane);
+        my_s0 = __ldg(a.seg + u0 + lane);
+        my_s1 = __ldg(a.seg + u0 + lane + 1);
+        my_p0 = __ldg(a.spos + my_s0);  // the first position (most IDs have one or two)
+      }
+      // the next ID's slice row is loaded under this ID's reduction (static
+      // double buffer: the loop is unrolled by two)
+      float gA[NL], gB[NL];
+      auto ldg_g = [&](int q, float (&gv)[NL]) {
+        ldg_vec<NL>(Gl + (int64_t)__shfl_sync(0xffffffffu, my_dg, q & 31) * sliceL + r * NL, gv);
+      };
+      auto emit = [&](int q, const float (&gv)[NL]) {
+        const int u = u0 + q;
+        const int s0 = __shfl_sync(0xffffffffu, my_s0, q), s1 = __shfl_sync(0xffffffffu, my_s1, q);
+        const int p0 = __shfl_sync(0xffffffffu, my_p0, q);
+        float v[32];  // v[ar NL + jl]
+#pragma unroll
+        for (int ar = 0; ar < RP; ++ar)
+#pragma unroll
+          for (int jl = 0; jl < NL; ++jl) v[ar * NL + jl] = pf[ar] * gv[jl];
+#pragma unroll
+        for (int st = 0; st < 3; ++st) {  // over the r bits of the lane: xor 4, 2, 1
+          const int half = 16 >> st, dist = 4 >> st;
+          const bool hi = (lane & dist) != 0;
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const float give = hi ? v[i] : v[half + i];
+            const float keep = hi ? v[half + i] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, give, dist);
+          }
+        }
+        const float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (s1 - s0 > HEAVY_POS) {
+          *reinterpret_cast<float4*>(a.Yu + (int64_t)u * npad + ocol) = o;
+        } else {
+          *reinterpret_cast<float4*>(a.out + (int64_t)p0 * emb + ocol) = o;
+          for (int sl = s0 + 1; sl < s1; ++sl)
+            *reinterpret_cast<float4*>(a.out + (int64_t)__ldg(a.spos + sl) * emb + ocol) = o;
+        }
+      };
+      ldg_g(0, gA);
+      for (int q = 0; q < nu; q += 2) {
+        if (q + 1 < nu) ldg_g(q + 1, gB);
+        emit(q, gA);
+        if (q + 1 < nu) {
+          if (q + 2 < nu) ldg_g(q + 2, gA);
+          emit(q + 1, gB);
+        }
+      }
+    }
+  }
+}
+#define TT_LOWRANK_FWD_SHAPES(X) X(8, 4, 8)
+
 // (K, RP, NL, CPL) instantiations of k_lowrank_bwd: sweep8.  At R = 16 (CPL 2:
 // one ID's operands at a time) it measured slower than k_fused_bwd + k_fused_w
 // (sweep16 0.454 -> 0.485 ms/step, small 0.144 -> 0.146; profiles/r02/NOTES.md)
