@@ -121,6 +121,20 @@ def test_every_lowrank_backward_instantiation_has_a_parity_case():
     assert not missing, f"compiled low-rank backward instantiations with no parity case: {missing}"
 
 
+def test_every_lowrank_forward_instantiation_has_a_parity_case():
+    # k_lowrank_fwd<K, RP, NL> (TT_LOWRANK_FWD_SHAPES): one 32-column block
+    src = open(os.path.join(CSRC, "kernels_fused.cuh")).read()
+    m = re.search(r"#define\s+TT_LOWRANK_FWD_SHAPES\(X\)([^\n]*)", src)
+    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+)\)", m.group(1))}
+    assert compiled
+    covered = set()
+    for name in FUSED_SHAPES:
+        ffma, _ = reached(SHAPES[name][0]())
+        covered |= {(t[0], t[2], t[3]) for t in ffma if t[1] == 32 and t[3] != "*"}
+    missing = sorted(t for t in compiled if t not in covered)
+    assert not missing, f"compiled low-rank forward instantiations with no parity case: {missing}"
+
+
 def test_every_rank128_tcgen05_instantiation_has_a_parity_case():
     src = open(os.path.join(CSRC, "kernels_tcgen05.cuh")).read()
     m = re.search(r"#define\s+TT_TC128_SHAPES\(X\)([^\n]*)", src)
