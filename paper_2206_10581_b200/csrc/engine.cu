@@ -925,7 +925,7 @@ bool lrbwd_enabled() {
 }
 
 bool lrfwd_shape(const FusedShape& f) {
-#define LRF_EQ(k_, rp_, nl_) if (f.K == k_ && f.RP == rp_ && f.NL == nl_) return true;
+#define LRF_EQ(k_, rp_, nl_, cpl_) if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC == 32 * cpl_) return true;
   TT_LOWRANK_FWD_SHAPES(LRF_EQ)
 #undef LRF_EQ
   return false;
@@ -1200,7 +1200,7 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
 #undef TT_TC_FWD_CASE
       h->fwd_kernel = "k_tc_fwd";
       h->last_path = 2;
-    } else if (d_out && lrbwd_enabled() && f.K == 8 && f.NC == 32 && f.ncbf == 1 &&
+    } else if (d_out && lrbwd_enabled() && f.K <= 16 && f.ncbf == 1 &&
                c.emb_dim == (int64_t)f.RP * f.nF * f.NL && c.npad % 4 == 0 && lrfwd_shape(f)) {
       // low-rank streaming forward with the last level (k_lowrank_fwd): a warp
       // per chunk of a digit group's nodes, as the low-rank backward
@@ -1212,8 +1212,8 @@ int fused_forward(tt_engine* h, float* d_out, cudaStream_t s) {
       const int lgrid = (int)(((int64_t)groups * al.split + LR_WARPS - 1) / LR_WARPS);
       if (false) {
       }
-#define LRF_CASE(k_, rp_, nl_) \
-  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_) LAUNCH((k_lowrank_fwd<k_, rp_, nl_>), lgrid, LR_WARPS * 32, 0, s, al);
+#define LRF_CASE(k_, rp_, nl_, cpl_) \
+  else if (f.K == k_ && f.RP == rp_ && f.NL == nl_ && f.NC == 32 * cpl_) LAUNCH((k_lowrank_fwd<k_, rp_, nl_, cpl_>), lgrid, LR_WARPS * 32, 0, s, al);
       TT_LOWRANK_FWD_SHAPES(LRF_CASE)
 #undef LRF_CASE
       h->ll_fused = true;

@@ -2227,43 +2227,61 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_bwd(FusedArgs a) {
 //   (ar = r / 2, jf, jl = 4 (r % 2) ..+4): one float4 per lane and position, the
 //   warp writing the whole 128-float row (heavy IDs: their Yu row, scattered
 //   later by k_scatter_heavy).
-template <int K, int RP, int NL>
+template <int K, int RP, int NL, int CPL>
 __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_fwd(FusedArgs a) {
   TT_PDL_ENTRY();
-  constexpr int NC = 32, NFJ = NC / K;
-  static_assert(RP * K == 32 && RP * NL == 32 && K == 8, "one lane per A element and per output quad");
+  // lane l owns columns l + 32 i (i < CPL): jf_i = (l + 32 i) / K, r = l % K;
+  // an ID's CPL RP NL partial outputs are reduce-scattered over the log2(K) r
+  // bits of the lane, leaving V / K = 4 per lane: entries 4 (l % K) ..+4 of
+  // [i][ar][jl]
+  constexpr int NC = 32 * CPL, NFJ = NC / K, V = CPL * RP * NL, AE = RP * K / 32;
+  static_assert(V == 4 * K && (RP * K) % 32 == 0 && 32 % K == 0, "one float4 of outputs per lane");
   if (tt_failed(a.st)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int it = blockIdx.x * LR_WARPS + warp;
   if (it >= a.c.m[a.F] * a.split) return;
   int g, cb, chunk, g0, g1;
   if (!work_item_at(a, it, g, cb, chunk, g0, g1)) return;
-  const int r = lane % K, jf = lane / K;
+  const int r = lane % K;
   const float* Gl = a.params + a.c.core_off[a.c.d - 1];
   const int64_t sliceL = a.c.slice[a.c.d - 1];
   const int64_t emb = a.c.emb_dim, npad = a.c.npad;
   const float* S = a.params + a.c.core_off[a.F] + (int64_t)g * a.c.slice[a.F];
-  float sv[K];
+  float sv[CPL][K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) sv[k] = __ldg(S + k * NC + lane);
-  // this lane's output quad: entries e0 .. e0 + 3 of (ar NL + jl), e0 = 4 r
-  const int oar = (4 * r) / NL, ojl = (4 * r) % NL;
-  const int64_t ocol = ((int64_t)oar * NFJ + jf) * NL + ojl;
+  for (int i = 0; i < CPL; ++i)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sv[i][k] = __ldg(S + k * NC + lane + 32 * i);
+  // this lane's output quad: entries e0 .. e0 + 3 of [i][ar][jl], e0 = 4 r
+  const int e0 = 4 * r, oi = e0 / (RP * NL), oar = (e0 % (RP * NL)) / NL, ojl = e0 % NL;
+  const int ojf = (lane + 32 * oi) / K;
+  const int64_t ocol = ((int64_t)oar * NFJ + ojf) * NL + ojl;
   for (int n = g0; n < g1; ++n) {
     const int node = __ldg(a.orderF + n);
     const int p = __ldg(a.parentF + node);
     const float* Ap = a.Abase + (a.F == 1 ? a.c.core_off[0] + (int64_t)__ldg(a.digit0 + p) * a.c.slice[0]
                                           : (int64_t)p * RP * K);
-    const float my_a = __ldg(Ap + lane);  // A[ar][k] at lane ar K + k
+    float my_a[AE];  // A[ar][k] = element ar K + k, held by lane (ar K + k) % 32 in slot / 32
+#pragma unroll
+    for (int t = 0; t < AE; ++t) my_a[t] = __ldg(Ap + lane + 32 * t);
     const int c0 = __ldg(a.cstartF + node), c1 = __ldg(a.cstartF + node + 1);
-    float pf[RP];
+    float pf[RP][CPL];
 #pragma unroll
     for (int ar = 0; ar < RP; ++ar) {
-      float x = 0.f;
+      float x[CPL];
 #pragma unroll
-      for (int k = 0; k < K; ++k) x = fmaf(__shfl_sync(0xffffffffu, my_a, ar * K + k), sv[k], x);
-      pf[ar] = x;
-      a.Psave[(int64_t)node * RP * NC + ar * NC + lane] = x;
+      for (int i = 0; i < CPL; ++i) x[i] = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float av = __shfl_sync(0xffffffffu, my_a[(ar * K + k) / 32], (ar * K + k) % 32);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) x[i] = fmaf(av, sv[i][k], x[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        pf[ar][i] = x[i];
+        a.Psave[(int64_t)node * RP * NC + ar * NC + lane + 32 * i] = x[i];
+      }
     }
     for (int u0 = c0; u0 < c1; u0 += 32) {
       const int nu = min(32, c1 - u0);
@@ -2284,14 +2302,16 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_fwd(FusedArgs a) {
         const int u = u0 + q;
         const int s0 = __shfl_sync(0xffffffffu, my_s0, q), s1 = __shfl_sync(0xffffffffu, my_s1, q);
         const int p0 = __shfl_sync(0xffffffffu, my_p0, q);
-        float v[32];  // v[ar NL + jl]
+        float v[V];  // v[(i RP + ar) NL + jl]
 #pragma unroll
-        for (int ar = 0; ar < RP; ++ar)
+        for (int i = 0; i < CPL; ++i)
 #pragma unroll
-          for (int jl = 0; jl < NL; ++jl) v[ar * NL + jl] = pf[ar] * gv[jl];
+          for (int ar = 0; ar < RP; ++ar)
 #pragma unroll
-        for (int st = 0; st < 3; ++st) {  // over the r bits of the lane: xor 4, 2, 1
-          const int half = 16 >> st, dist = 4 >> st;
+            for (int jl = 0; jl < NL; ++jl) v[(i * RP + ar) * NL + jl] = pf[ar][i] * gv[jl];
+#pragma unroll
+        for (int dist = K / 2; dist >= 1; dist >>= 1) {  // over the r bits of the lane, high to low
+          const int half = (V * dist) / K;
           const bool hi = (lane & dist) != 0;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
@@ -2321,7 +2341,10 @@ __global__ void __launch_bounds__(LR_WARPS * 32) k_lowrank_fwd(FusedArgs a) {
     }
   }
 }
-#define TT_LOWRANK_FWD_SHAPES(X) X(8, 4, 8)
+// (K, RP, NL, CPL) instantiations of k_lowrank_fwd: sweep8.  The two-column
+// version (R = 16) is parity-tested but measured slower or equal (sweep16 0.454
+// -> 0.475, small 0.143 -> 0.142 ms/step; profiles/r02/NOTES.md)
+#define TT_LOWRANK_FWD_SHAPES(X) X(8, 4, 8, 1)
 
 // (K, RP, NL, CPL) instantiations of k_lowrank_bwd: sweep8.  At R = 16 (CPL 2:
 // one ID's operands at a time) it measured slower than k_fused_bwd + k_fused_w

@@ -122,15 +122,15 @@ def test_every_lowrank_backward_instantiation_has_a_parity_case():
 
 
 def test_every_lowrank_forward_instantiation_has_a_parity_case():
-    # k_lowrank_fwd<K, RP, NL> (TT_LOWRANK_FWD_SHAPES): one 32-column block
+    # k_lowrank_fwd<K, RP, NL, CPL> (TT_LOWRANK_FWD_SHAPES): one block of NC = 32 CPL columns
     src = open(os.path.join(CSRC, "kernels_fused.cuh")).read()
     m = re.search(r"#define\s+TT_LOWRANK_FWD_SHAPES\(X\)([^\n]*)", src)
-    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+)\)", m.group(1))}
+    compiled = {tuple(int(v) for v in t) for t in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", m.group(1))}
     assert compiled
     covered = set()
     for name in FUSED_SHAPES:
         ffma, _ = reached(SHAPES[name][0]())
-        covered |= {(t[0], t[2], t[3]) for t in ffma if t[1] == 32 and t[3] != "*"}
+        covered |= {(t[0], t[2], t[3], t[1] // 32) for t in ffma if t[0] <= 16 and t[1] % 32 == 0 and t[3] != "*"}
     missing = sorted(t for t in compiled if t not in covered)
     assert not missing, f"compiled low-rank forward instantiations with no parity case: {missing}"
 
