@@ -19,14 +19,14 @@ for cfg in products small sweep8 sweep16 sweep32 sweep64 sweep128 arxivT4_r32 pa
 done
 timeout 900 python bench.py --impl reference --config papers --steps 3 --warmup 1 > gpurun_out/s2_ref_papers.json 2> gpurun_out/s2_ref_papers.err
 cat gpurun_out/s2_ref_papers.json
-for run in "papers auto" "papers tc" "billion auto"; do
+for run in "papers auto" "papers tc" "billion auto" "sweep8 auto"; do
   set -- $run
   CMD="python bench.py --config $1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-tensor-path --path $2"
   $CMD > gpurun_out/s2_plain_$1_$2.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/s2_launches_$1_$2.csv $CMD > gpurun_out/s2_ncu_$1_$2.log 2>&1
   python scripts/ncu_summary.py gpurun_out/s2_launches_$1_$2.csv > gpurun_out/s2_launches_$1_$2.txt
 done
-for run in "papers auto k_fused_fwd8|k_fused_bwd|k_last_level|k_fused_w 4" "papers tc k_tc_fwd|k_tc_bwd3|k_fused_wdc 3" "billion auto k_fused_bwd_ws|k_fused_fwd8w 2"; do
+for run in "papers auto k_fused_fwd8|k_fused_bwd|k_last_level|k_fused_w 4" "papers tc k_tc_fwd|k_tc_bwd3|k_fused_wdc 3" "billion auto k_fused_bwd_ws|k_fused_fwd8w<32,.16 2" "sweep8 auto k_lowrank_fwd|k_lowrank_bwd 2"; do
   set -- $run
   CMD="python bench.py --config $1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-tensor-path --path $2 --graph 0"
   ncu --set full --clock-control none --import-source on -k regex:"$3" -c $4 -o gpurun_out/s2_full_$1_$2 $CMD > gpurun_out/s2_ncu_full_$1_$2.log 2>&1
