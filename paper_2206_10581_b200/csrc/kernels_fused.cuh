@@ -36,6 +36,10 @@
 namespace tt {
 
 constexpr int FB_THREADS = 256;
+#ifndef TT_DG_UNROLL
+#define TT_DG_UNROLL 8
+#endif
+constexpr int DG_UNROLL = TT_DG_UNROLL;  // k_fused_bwd's dG_F row loop unroll (A/B builds)
 constexpr int FB_BM = 64;
 constexpr int FB_SMEM_MAX = 227 * 1024;
 
@@ -640,6 +644,10 @@ __global__ void __launch_bounds__(F8_THREADS, (K <= 32) ? 4 : 3)
 // columns cl*4 ..+4, 64 + cl*4 ..+4; the A tile's row stride is K + 4 floats,
 // so the two half-warps' rows (adjacent) sit in different banks.
 constexpr int F8W_ROWS = 16;
+#ifndef TT_F8W_UNROLL
+#define TT_F8W_UNROLL 4
+#endif
+constexpr int F8W_UNROLL = TT_F8W_UNROLL;  // k-step unroll of k_fused_fwd8w (A/B builds)
 template <int K>
 __host__ __device__ constexpr int f8w_astride() { return K + 4; }
 inline size_t fwd8w_smem(int K) {
@@ -747,7 +755,7 @@ __global__ void __launch_bounds__(F8_THREADS, 3)
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
+#pragma unroll F8W_UNROLL
     for (int kk = 0; kk < K; kk += 4) {
       float4 av[8];
 #pragma unroll
@@ -991,7 +999,7 @@ __global__ void __launch_bounds__(FB_THREADS, (K * BN <= 64 * 128) ? 2 : 1) k_fu
         float a0[TK], b0[TN], a1[TK], b1[TN];
         ldA(0, a0);
         load_row_frag<BN>(Ds, lane, b0);
-#pragma unroll 8
+#pragma unroll DG_UNROLL
         for (int m = 0; m < BM; m += 2) {
           ldA(m + 1, a1);
           load_row_frag<BN>(Ds + (m + 1) * DS, lane, b1);
