@@ -747,6 +747,11 @@ int split_for(tt_engine* h, int grid, int level, bool fwd) {
     const char* e = getenv("TT_SPLIT");
     return e && *e ? atoi(e) : 0;
   }();
+  static const int env_f = [] {  // forward only (A/B of the forward's wave tail)
+    const char* e = getenv("TT_SPLIT_FWD");
+    return e && *e ? atoi(e) : 0;
+  }();
+  if (fwd && env_f > 0) return env_f;
   if (env > 0) return env;
   const DevCfg& c = h->dc;
   long double prefixes = 1;
