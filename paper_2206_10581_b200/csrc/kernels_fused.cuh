@@ -1479,7 +1479,13 @@ inline size_t bwd_ws_smem(int K) {
 // (grid-stride).  The ID's prefix block P_F[p] (RP x NC floats, contiguous)
 // is staged into the warp's shared buffer with coalesced 16-byte loads (all
 // independent: the whole block is in flight at once), rows padded to K + 4.
-constexpr int SK_WARPS = 8;
+#ifndef TT_SK_WARPS
+#define TT_SK_WARPS 8
+#endif
+#ifndef TT_SK_MINB
+#define TT_SK_MINB 2
+#endif
+constexpr int SK_WARPS = TT_SK_WARPS;  // warps per CTA of the streaming P_F kernels (A/B builds)
 
 template <int K>
 __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp, int nrow, float* buf, int lane) {
@@ -1513,7 +1519,7 @@ __device__ __forceinline__ void stage_prefix_block(const float* __restrict__ Cp,
 // memory, so every warp keeps a block in flight; the indices run one ID ahead
 // of that.
 template <int K, int NL, bool PIPE, int KS>
-__global__ void __launch_bounds__(SK_WARPS * 32, 2) k_last_level(FusedArgs a, const int* __restrict__ counts,
+__global__ void __launch_bounds__(SK_WARPS * 32, TT_SK_MINB) k_last_level(FusedArgs a, const int* __restrict__ counts,
                                                               const int* __restrict__ parentL) {
   TT_PDL_ENTRY();
   extern __shared__ __align__(16) float sk_smem[];
